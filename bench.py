@@ -1,0 +1,347 @@
+"""Benchmark: filtered points/s of the CudaPre hot path (Steps 1-3) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C5] [--impl ours|reference]
+    python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 ... bench.py --gpus N
+
+One step = one pass of the whole hot path over the workload resident in HBM:
+Step 1 (seed + K1 kernels, D2H of the 16 picks; for N>1 the NCCL all-gather of
+the per-rank picks and the host merge), Step 2 (host monotone chain + kernel
+parameters), Step 3 (K2 classify + ordered compaction writing each survivor's
+int64 index and float2 coordinates into HBM, D2H of the count).  Workload:
+BASELINE.json configs[4] ("C5": 2e9 points uniform in the unit disk, seeded
+synthetic, sharded contiguously over the N ranks: strong scaling).
+
+Prints ONE JSON line (rank 0).  See DESIGN.md §8 for every field.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "filtered points/sec (Gpts/s) and % of HBM roofline at 1/2/4/8 B200; discard %"
+K1_BYTES_PER_PT = 8          # K1 reads each float2 once
+K2_BYTES_PER_PT = 8          # K2 reads each float2 once ...
+K2_BYTES_PER_SURVIVOR = 16   # ... and writes int64 index + float2 point per survivor
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="C5")
+    ap.add_argument("--n", type=int, default=0, help="override total points")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--angles", default="A")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except OSError:
+        return None
+
+
+class ClockSampler:
+    """NVML samples of SM clock + throttle reasons during the timed region."""
+
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown"}
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def result(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+def oracle_rate(pts_host: np.ndarray, threads: int, angles: str):
+    """Time the oracle (as it stands) on a host sample; returns (pts/s, n)."""
+    import oracle
+
+    oracle.build()
+    t0 = time.perf_counter()
+    oracle.cudapre(pts_host, angles, threads=threads)
+    dt = time.perf_counter() - t0
+    return len(pts_host) / dt, dt
+
+
+def sized_sample(pts_dev, target_s: float, threads: int, angles: str, cap: int):
+    """Pick a sample size that takes about target_s seconds of oracle work."""
+    pilot = min(cap, 2_000_000)
+    rate, _ = oracle_rate(pts_dev[:pilot].cpu().numpy(), threads, angles)
+    n = int(min(cap, max(pilot, rate * target_s)))
+    return n, rate
+
+
+def main():
+    args = parse()
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus and world > 1:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    import synth
+
+    cfg = dict(synth.CONFIGS[args.config])
+    n_total = args.n or cfg.pop("n")
+    cfg.pop("n", None)
+    family, seed = cfg.pop("family"), cfg.pop("seed")
+    threads = os.cpu_count() or 1
+
+    # ------------------------------------------------------------ reference arm: the oracle
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        import synth.cuda as scuda
+
+        torch.cuda.set_device(local)
+        scuda.build()
+        sample_cap = min(n_total, 200_000_000)
+        dev = scuda.generate(family, sample_cap, seed=seed, **cfg)
+        n_s, _ = sized_sample(dev, 2.0, threads, args.angles, sample_cap)
+        host = dev[:n_s].cpu().numpy()
+        del dev
+        import oracle
+
+        for _ in range(args.warmup):
+            oracle.cudapre(host, args.angles, threads=threads)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            oracle.cudapre(host, args.angles, threads=threads)
+        dt = time.perf_counter() - t0
+        v = n_s * args.steps / dt / 1e9
+        line = {"metric": METRIC, "value": v, "unit": "Gpts/s", "n_gpus": args.gpus,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic", "impl": "reference",
+                "config": {"workload": f"{args.config}: {n_total} pts {family} seed {seed}",
+                           "sample_points_per_step": n_s},
+                "cpu_baseline": {"value": v, "unit": "Gpts/s", "cores": threads, "kind": "oracle",
+                                 "sample": f"first {n_s} points of {args.config} per step"},
+                "e2e": {"value": v, "unit": "Gpts/s", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    # ------------------------------------------------------------ our arm
+    import torch.distributed as dist
+
+    import paper_1405_3454_b200 as cp
+    import synth.cuda as scuda
+    from paper_1405_3454_b200 import build as pbuild
+
+    torch.cuda.set_device(local)
+    if rank == 0:
+        pbuild.build()
+        scuda.build()
+    group = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        group = dist.group.WORLD
+        dist.barrier()
+    n_local = n_total // world + (1 if rank < n_total % world else 0)
+    base = rank * (n_total // world) + min(rank, n_total % world)
+    pts = scuda.generate(family, n_local, seed=seed, base=base, **cfg)
+    ws = cp.Workspace(n_local)
+    cap = max(1024, n_local // 8)
+    out_idx = torch.empty(cap, dtype=torch.int64, device="cuda")
+    out_pts = torch.empty((cap, 2), dtype=torch.float32, device="cuda")
+    torch.cuda.synchronize()
+
+    def step(rep1):
+        ext = cp.extremes(pts, args.angles, index_base=base, group=group, ws=ws, report=rep1)
+        idx, sp, rep2 = cp.filter(pts, ext, index_base=base, ws=ws, out_idx=out_idx, out_pts=out_pts)
+        return idx.shape[0], rep2
+
+    rep1 = cp.ReportT()
+    for _ in range(args.warmup):
+        step(rep1)
+    k1_ms, k2_ms, launches = [], [], 0
+    surv = 0
+    clocks = ClockSampler(torch.cuda.current_device())
+    if group is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with clocks:
+        start.record()
+        for _ in range(args.steps):
+            surv, rep2 = step(rep1)
+            k1_ms.append(rep1.ms_extremes_kernels)
+            k2_ms.append(rep2["ms_filter_kernel"])
+            launches += rep1.launches + rep2["launches"]
+        end.record()
+        torch.cuda.synchronize()
+    ms = start.elapsed_time(end)
+    if group is not None:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        s = torch.tensor([surv], device="cuda", dtype=torch.int64)
+        dist.all_reduce(s)
+        surv_total = int(s.item())
+    else:
+        surv_total = surv
+    value = n_total * args.steps / (ms / 1e3) / 1e9
+
+    # ------------------------------------------------------------ roofline of the dominant kernel
+    pk = peaks()
+    peak = pk["hbm_gbs"] if pk else 6650.0
+    k1 = statistics.mean(k1_ms)
+    k2 = statistics.mean(k2_ms)
+    k1_bytes = K1_BYTES_PER_PT * n_local
+    k2_bytes = K2_BYTES_PER_PT * n_local + K2_BYTES_PER_SURVIVOR * surv
+    kernels = {"k1_extremes(+seed)": (k1, k1_bytes), "k2_filter": (k2, k2_bytes)}
+    dom = max(kernels, key=lambda k: kernels[k][0])
+    d_ms, d_bytes = kernels[dom]
+    achieved = d_bytes / (d_ms / 1e3) / 1e9
+    traffic = None
+    try:
+        prof = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+        ent = prof.get(args.config, {}).get(dom)
+        if ent and int(ent.get("n_local", -1)) == n_local:
+            traffic = ent["dram_bytes_per_launch"]
+    except (OSError, ValueError):
+        pass
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": traffic, "kernel": dom,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, measured)" if pk else "fallback",
+                "per_kernel_ms": {k: round(v[0], 4) for k, v in kernels.items()},
+                "per_kernel_GBps": {k: round(v[1] / (v[0] / 1e3) / 1e9, 1) for k, v in kernels.items()},
+                "pipeline_GBps": round((k1_bytes + k2_bytes) * args.steps / (ms / 1e3) / 1e9, 1)}
+
+    # ------------------------------------------------------------ e2e: host buffers through the API
+    e2e = None
+    if not args.no_e2e:
+        e_steps = max(1, min(args.steps, 3))
+        try:
+            h_pts = torch.empty((n_local, 2), dtype=torch.float32).pin_memory()
+        except RuntimeError:
+            h_pts = torch.empty((n_local, 2), dtype=torch.float32)
+        h_pts.copy_(pts)
+        h_surv = torch.empty(cap, dtype=torch.int64).pin_memory()
+        d2h = 0
+        if group is None:
+            m, _ = cp.run_host(h_pts, pts, out_idx, h_surv, args.angles, ws=ws)   # warm-up
+            torch.cuda.synchronize()
+            t0 = torch.cuda.Event(enable_timing=True)
+            t1 = torch.cuda.Event(enable_timing=True)
+            t0.record()
+            for _ in range(e_steps):
+                m, _ = cp.run_host(h_pts, pts, out_idx, h_surv, args.angles, ws=ws)
+            t1.record()
+            torch.cuda.synchronize()
+            e_ms = t0.elapsed_time(t1)
+            d2h = 8 * m + cp.EXTREMES_BYTES + 8
+        else:
+            def e2e_step():
+                pts.copy_(h_pts, non_blocking=True)
+                ext = cp.extremes(pts, args.angles, index_base=base, group=group, ws=ws)
+                idx, _, _ = cp.filter(pts, ext, index_base=base, ws=ws, out_idx=out_idx,
+                                      return_points=False)
+                h_surv[: idx.shape[0]].copy_(idx)
+                return idx.shape[0]
+            e2e_step()
+            dist.barrier()
+            torch.cuda.synchronize()
+            t0 = torch.cuda.Event(enable_timing=True)
+            t1 = torch.cuda.Event(enable_timing=True)
+            t0.record()
+            for _ in range(e_steps):
+                m = e2e_step()
+            t1.record()
+            torch.cuda.synchronize()
+            t = torch.tensor([t0.elapsed_time(t1)], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = float(t.item())
+            d2h = 8 * m + world * cp.EXTREMES_BYTES + 8
+        e2e = {"value": n_total * e_steps / (e_ms / 1e3) / 1e9, "unit": "Gpts/s",
+               "h2d_bytes_per_step": 8 * n_local, "d2h_bytes_per_step": d2h, "steps": e_steps,
+               "pinned": bool(h_pts.is_pinned())}
+        del h_pts
+
+    # ------------------------------------------------------------ CPU baseline (oracle), rank 0, N=1
+    cpu = None
+    if world == 1 and rank == 0 and not args.no_cpu_baseline:
+        import oracle
+
+        n_s, _ = sized_sample(pts, 15.0, threads, args.angles, min(n_local, 200_000_000))
+        host = pts[:n_s].cpu().numpy()
+        rate, dt = oracle_rate(host, threads, args.angles)
+        cpu = {"value": rate / 1e9, "unit": "Gpts/s", "cores": threads, "kind": "oracle",
+               "sample": f"first {n_s} points of {args.config} (oracle Steps 1-3, {dt:.1f} s)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": "Gpts/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32+f64",
+            "data": "synthetic",
+            "config": {"workload": f"{args.config}: {n_total} pts uniform {family} (seed {seed}), "
+                                   f"contiguous shards of {n_local}", "n_total": n_total,
+                       "angles": args.angles, "l2": "inputs larger than L2 (16 GB vs 126 MB), no flush",
+                       "parallelism": f"dp{world} (point shards; 912 B NCCL all-gather per step)"},
+            "discard_pct": round(100 * (1 - surv_total / n_total), 4),
+            "remaining_pct": round(100 * surv_total / n_total, 4),
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches, "clocks": clocks.result(),
+        }
+        print(json.dumps(line), flush=True)
+    if group is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

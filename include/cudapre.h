@@ -1,0 +1,229 @@
+/*
+ * cudapre.h — C ABI of the B200-native CudaPre interior-point filter
+ * (G. Mei, arXiv 1405.3454).  Library: paper_1405_3454_b200/libcudapre.so
+ *
+ * The method (§2):
+ *   Step 1  locate the extreme points: for the original point set and the
+ *           point set rotated by each further angle, the points with min/max
+ *           x and y.                        -> cudapre_extremes
+ *   Step 2  Andrew's monotone chain on those <= 16 points, on the CPU
+ *           (correction P:71).               -> cudapre_polygon
+ *   Step 3  discard every point inside that convex polygon and
+ *           keep the rest, in ascending index order.  -> cudapre_filter
+ *   Then    the convex hull of the remaining points -> cudapre_hull
+ *
+ * Citations: "P:nn" = PAPER.md line nn, "S:nn" = SPEC.md line nn, "A#" =
+ * the reading numbered # in DESIGN.md §3 (where the paper is silent).
+ *
+ * Conventions for every entry point:
+ *   - Nothing throws across the ABI; every function returns cudapre_status and,
+ *     on a non-OK status, cudapre_last_error() returns a thread-local message.
+ *   - Ownership: the CALLER allocates and frees every buffer (device buffers
+ *     are plain device pointers, e.g. from torch; host structs are plain
+ *     memory).  The library keeps no device state between calls; everything
+ *     persistent lives in the caller's workspace (d_ws).
+ *   - Device pointers marked d_*, host pointers h_*.  Streams are passed as
+ *     `void*` holding a cudaStream_t (NULL = legacy default stream).
+ *   - Points are float2 AoS ("cudapre_pt": x then y, 8 bytes), at least 8-byte
+ *     aligned; 16-byte alignment enables the 128-bit vector path (any 8-byte
+ *     aligned pointer works).
+ *   - Indices are int64 and GLOBAL: index_base + local position, so a caller
+ *     that shards one point set over several GPUs gets the same indices as a
+ *     single GPU would.
+ *   - A workspace is bound to one stream at a time: do not run two calls that
+ *     share a workspace concurrently.  It must be zero-filled once before
+ *     first use (cudapre_workspace_init); every call leaves it re-usable.
+ *   - Limits: n_local <= 4294967295 points per call; at most
+ *     CUDAPRE_MAX_ANGLES angles; the first angle must be 0 degrees (the
+ *     original, unrotated set, "together with the group of extreme
+ *     points of the original point set").
+ */
+#ifndef CUDAPRE_H
+#define CUDAPRE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CUDAPRE_MAX_ANGLES 8
+#define CUDAPRE_MAX_SLOTS (4 * CUDAPRE_MAX_ANGLES)
+
+typedef enum {
+    CUDAPRE_OK = 0,
+    CUDAPRE_ERR_EMPTY_INPUT = 1,      /* no points at all where extremes are required */
+    CUDAPRE_ERR_INVALID_ARGUMENT = 2, /* NULL / misaligned pointer, bad size, bad angle list */
+    CUDAPRE_ERR_NONFINITE_INPUT = 3,  /* a NaN / Inf coordinate was seen (precondition S:32, A16) */
+    CUDAPRE_ERR_CUDA = 4,             /* a CUDA runtime call failed (message has the CUDA error) */
+    CUDAPRE_ERR_CAPACITY = 5,         /* survivor buffer too small; *h_count holds the needed size */
+    CUDAPRE_ERR_WORKSPACE = 6         /* workspace smaller than cudapre_workspace_bytes(n) */
+} cudapre_status;
+
+typedef struct { float x, y; } cudapre_pt; /* == float2 */
+
+/* Step 1 result.  Slot 4k+{0,1,2,3} = {argmin X_k, argmax X_k, argmin Y_k,
+ * argmax Y_k} for angle k in list order (A8), where
+ *   X_k = RN(RN(x*c_k) + RN(y*s_k)),  Y_k = RN(RN(y*c_k) - RN(x*s_k))
+ * in IEEE binary64 without FMA (A3, A6), lowest index on equal keys
+ * (A7).  A slot of an empty shard has idx = -1 and never wins a merge.      */
+typedef struct {
+    int32_t nang;                        /* number of angles (slots = 4*nang) */
+    int32_t nonfinite;                   /* 1 if a non-finite coordinate was seen */
+    int64_t n;                           /* points reduced (summed over merged parts) */
+    int64_t idx[CUDAPRE_MAX_SLOTS];      /* global index of each pick, -1 if none */
+    double key[CUDAPRE_MAX_SLOTS];       /* the binary64 key value of each pick */
+    cudapre_pt pt[CUDAPRE_MAX_SLOTS];    /* coordinates of each pick */
+    double c[CUDAPRE_MAX_ANGLES];        /* cos of each angle used (correctly rounded, A5) */
+    double s[CUDAPRE_MAX_ANGLES];        /* sin of each angle used */
+} cudapre_extremes_t;
+
+/* Step 2 result: the filter polygon and the parameters the Step-3 kernel
+ * uses.  ring = Andrew's monotone chain of the distinct picks: CCW, starting
+ * at the lexicographically smallest vertex, collinear points excluded (A10,
+ * A17).  nv < 3 means degenerate: nothing is discarded (A13). */
+typedef struct {
+    int32_t nv;                          /* ring length, 0..CUDAPRE_MAX_SLOTS */
+    int32_t degenerate;                  /* 1 if nv < 3 */
+    int32_t n_distinct;                  /* distinct pick coordinates ("less than 16") */
+    int32_t exact_only;                  /* 1 if the float fast path was disabled (extreme ranges) */
+    int64_t vidx[CUDAPRE_MAX_SLOTS];     /* global index of each ring vertex */
+    cudapre_pt v[CUDAPRE_MAX_SLOTS];     /* ring vertex coordinates */
+    float box[4];                        /* inner box x0,x1,y0,y1 strictly inside the ring (x0>x1: none) */
+    float err_max;                       /* largest per-edge float error bound E_j */
+    int32_t pad;
+    /* Step-3 kernel line tests, edge j = v[j] -> v[j+1]:  g_j(p) = fma(A_j, p.x,
+     * fma(B_j, p.y, C_j)) with C_j already lowered by E_j, where E_j bounds
+     * |float evaluation - exact orient(v_j, v_j+1, p)| over the exact data
+     * bounding box.                                        */
+    float A[CUDAPRE_MAX_SLOTS], B[CUDAPRE_MAX_SLOTS], C[CUDAPRE_MAX_SLOTS], E[CUDAPRE_MAX_SLOTS];
+} cudapre_polygon_t;
+
+/* Per-call report (S:118-123 FilterReport; per-phase timings S:189). */
+typedef struct {
+    int64_t n;                           /* points filtered by this call */
+    int64_t survivors;                   /* points kept (== *h_count) */
+    double ms_extremes_kernels;          /* device time of the Step-1 kernels (CUDA events) */
+    double ms_filter_kernel;             /* device time of the Step-3 kernel (CUDA events) */
+    double ms_polygon_host;              /* host time of Step 2 */
+    int32_t launches;                    /* kernels launched by the call */
+    int32_t pad;
+} cudapre_report_t;
+
+/* ---------------------------------------------------------------- helpers */
+
+/* Library version string. */
+const char* cudapre_version(void);
+
+/* Message for the last non-OK status returned on this thread ("" if none). */
+const char* cudapre_last_error(void);
+
+/* Angle presets (A1).  preset 0 = {0, 30, 45, 60} degrees (default);
+ * preset 1 = {0, 30, 45, 45} (P:25, P:35 literal text); preset 2 = {0}
+ * (Akl-Toussaint quadrilateral); preset 3 = {0, 22.5, 45, 67.5}.
+ * Writes *nang and the correctly rounded c[k] = cos, s[k] = sin (A5) into
+ * caller arrays of CUDAPRE_MAX_ANGLES doubles.  INVALID_ARGUMENT for an
+ * unknown preset.                                                          */
+cudapre_status cudapre_angles_preset(int preset, int32_t* nang, double* c, double* s);
+
+/* Bytes of device workspace needed for shards of up to n_local points. */
+size_t cudapre_workspace_bytes(int64_t n_local);
+
+/* Zero-fill a workspace on `stream` (required once before first use). */
+cudapre_status cudapre_workspace_init(void* d_ws, size_t ws_bytes, void* stream);
+
+/* --------------------------------------------------------------- Step 1 */
+
+/* Step 1 over the local shard d_pts[0, n_local):
+ * one streaming pass (HBM read of 8 bytes/point) reduces all 4*nang keys.
+ *   d_pts       device, n_local points (may be NULL iff n_local == 0)
+ *   index_base  global index of d_pts[0]
+ *   nang, c, s  angle list (host arrays of nang doubles; c[0]=1, s[0]=0
+ *               required); NULL c/s = preset 0
+ *   d_ws        workspace of ws_bytes >= cudapre_workspace_bytes(n_local)
+ *   stream      cudaStream_t as void*
+ *   d_out       nullable DEVICE cudapre_extremes_t receiving the result
+ *               (e.g. for an NCCL all-gather across ranks)
+ *   h_out       nullable HOST cudapre_extremes_t; if given the call blocks
+ *               until it is valid
+ *   h_rep       nullable report (ms_extremes_kernels, launches)
+ * Errors: EMPTY_INPUT if n_local == 0 — the empty part (n = 0, every idx
+ * = -1) is still written to d_out / h_out, so a caller that shards one point
+ * set may treat EMPTY_INPUT from one shard as benign and merge it;
+ * NONFINITE_INPUT (result still written, flagged); INVALID_ARGUMENT;
+ * WORKSPACE; CUDA.                                                         */
+cudapre_status cudapre_extremes(const cudapre_pt* d_pts, int64_t n_local, int64_t index_base,
+                                int32_t nang, const double* c, const double* s,
+                                void* d_ws, size_t ws_bytes, void* stream,
+                                cudapre_extremes_t* d_out, cudapre_extremes_t* h_out,
+                                cudapre_report_t* h_rep);
+
+/* Combine per-shard Step-1 results (host): for every slot the lexicographic
+ * (key, global index) extreme — the same rule as inside one GPU, so the
+ * result is independent of how the points were sharded.
+ * EMPTY_INPUT if the parts hold no point at all.                           */
+cudapre_status cudapre_extremes_merge(const cudapre_extremes_t* h_parts, int32_t count,
+                                      cudapre_extremes_t* h_out);
+
+/* --------------------------------------------------------------- Step 2 */
+
+/* Step 2 on the host: distinct picks -> Andrew's
+ * monotone chain with the EXACT orientation predicate (A11) -> ring, plus
+ * the Step-3 kernel parameters (per-edge float coefficients with rigorous
+ * error bounds over the exact data bounding box, inner box).               */
+cudapre_status cudapre_polygon(const cudapre_extremes_t* h_ext, cudapre_polygon_t* h_poly);
+
+/* --------------------------------------------------------------- Step 3 */
+
+/* Steps 2+3: builds the polygon from h_ext (the GLOBAL
+ * extremes, merged if sharded), then one streaming pass over the local shard
+ * classifies every point and stream-compacts the survivors.
+ * Point i is DISCARDED iff orient(v_j, v_j+1, p_i) > 0 exactly for every
+ * ring edge j (strictly inside, A12); everything else survives.  Survivors
+ * are written in ascending global index order (A15):
+ *   d_surv_idx  device int64[capacity]   global indices (required)
+ *   d_surv_pts  device cudapre_pt[capacity] their coordinates (nullable)
+ *   h_count     host: number of survivors (always written on OK/CAPACITY)
+ *   h_poly      nullable host copy of the polygon used
+ *   h_rep       nullable report
+ * The call blocks until *h_count is valid.  Degenerate polygon: every point
+ * survives — not an error.  CAPACITY if *h_count > capacity (the
+ * first `capacity` survivors are written).                                 */
+cudapre_status cudapre_filter(const cudapre_pt* d_pts, int64_t n_local, int64_t index_base,
+                              const cudapre_extremes_t* h_ext,
+                              int64_t* d_surv_idx, cudapre_pt* d_surv_pts, int64_t capacity,
+                              void* d_ws, size_t ws_bytes, void* stream,
+                              int64_t* h_count, cudapre_polygon_t* h_poly,
+                              cudapre_report_t* h_rep);
+
+/* ----------------------------------------------------------- final hull */
+
+/* Convex hull on the host by Andrew's monotone chain with
+ * the exact orientation predicate, over h_pts[h_ids[j]] (h_ids NULL =
+ * identity over 0..n-1).  h_ring (capacity n) receives the canonical ring
+ * of point ids: CCW, starting at the lexicographically smallest (x, y)
+ * vertex, collinear points excluded, duplicate coordinates represented by
+ * their lowest id (A17).  *h_ring_len = 1 or 2 means a degenerate
+ * point / segment; 0 for n == 0.                                           */
+cudapre_status cudapre_hull(const cudapre_pt* h_pts, const int64_t* h_ids, int64_t n,
+                            int64_t* h_ring, int64_t* h_ring_len);
+
+/* ------------------------------------------------------- end to end */
+
+/* The whole Steps 1-3 starting from HOST points (pinned memory recommended):
+ * copies h_pts into the caller's device buffer d_pts (n points) on `stream`,
+ * runs Step 1, Step 2 and Step 3 there, and copies the survivors' global
+ * indices back into h_surv_idx (host int64[capacity]).  index_base = 0.
+ * Same errors as cudapre_extremes / cudapre_filter.                        */
+cudapre_status cudapre_run_host(const cudapre_pt* h_pts, int64_t n, int32_t nang,
+                                const double* c, const double* s, cudapre_pt* d_pts,
+                                void* d_ws, size_t ws_bytes, int64_t* d_surv_idx,
+                                int64_t* h_surv_idx, int64_t capacity, void* stream,
+                                int64_t* h_count, cudapre_report_t* h_rep);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CUDAPRE_H */

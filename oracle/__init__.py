@@ -67,7 +67,8 @@ def _ptr(a: np.ndarray):
     return a.ctypes.data_as(ctypes.c_void_p)
 
 
-PRESETS = {"A": (0.0, 30.0, 45.0, 60.0), "B": (0.0, 30.0, 45.0, 45.0)}
+PRESETS = {"A": (0.0, 30.0, 45.0, 60.0), "B": (0.0, 30.0, 45.0, 45.0), "AT": (0.0,),
+           "C": (0.0, 22.5, 45.0, 67.5)}
 
 
 def coeffs(angles) -> tuple[np.ndarray, np.ndarray]:

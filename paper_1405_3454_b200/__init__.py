@@ -1,0 +1,396 @@
+"""B200-native CudaPre interior-point filter (G. Mei, arXiv 1405.3454).
+
+Thin ctypes binding over ``libcudapre.so`` (include/cudapre.h).  This module
+only marshals arguments: every step of the hot path runs in the library's
+CUDA kernels (Step 1, Step 3) and host C++ (Step 2, final hull).  PyTorch
+supplies device memory, streams and process groups.  There is no CPU
+fallback: importing works anywhere, but any compute call raises if the
+library or a CUDA device is missing.
+
+    pts = torch.as_tensor(xy, device="cuda")           # (n, 2) float32
+    ext = cudapre.extremes(pts)                        # Step 1
+    idx, surv, rep = cudapre.filter(pts, ext)          # Steps 2+3
+    ring = cudapre.hull(surv.cpu().numpy())            # final hull
+
+Multi-GPU (one process per GPU, torch.distributed over NCCL): each rank
+passes its shard and ``index_base``; ``extremes(..., group=pg)`` all-gathers
+the per-rank results (one 912-byte struct per rank) and merges them with the
+library's lexicographic rule, so every rank gets the single-GPU answer.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libcudapre.so")
+MAX_ANGLES = 8
+MAX_SLOTS = 32
+
+OK, ERR_EMPTY, ERR_ARG, ERR_NONFINITE, ERR_CUDA, ERR_CAPACITY, ERR_WORKSPACE = range(7)
+_STATUS = {1: "EMPTY_INPUT", 2: "INVALID_ARGUMENT", 3: "NONFINITE_INPUT", 4: "CUDA",
+           5: "CAPACITY", 6: "WORKSPACE"}
+PRESETS = {"A": 0, "B": 1, "AT": 2, "C": 3}   # {0,30,45,60} {0,30,45,45} {0} {0,22.5,45,67.5}
+
+
+class CudaPreError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"cudapre {_STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class Pt(ctypes.Structure):
+    _fields_ = [("x", ctypes.c_float), ("y", ctypes.c_float)]
+
+
+class ExtremesT(ctypes.Structure):
+    _fields_ = [("nang", ctypes.c_int32), ("nonfinite", ctypes.c_int32), ("n", ctypes.c_int64),
+                ("idx", ctypes.c_int64 * MAX_SLOTS), ("key", ctypes.c_double * MAX_SLOTS),
+                ("pt", Pt * MAX_SLOTS), ("c", ctypes.c_double * MAX_ANGLES),
+                ("s", ctypes.c_double * MAX_ANGLES)]
+
+
+class PolygonT(ctypes.Structure):
+    _fields_ = [("nv", ctypes.c_int32), ("degenerate", ctypes.c_int32),
+                ("n_distinct", ctypes.c_int32), ("exact_only", ctypes.c_int32),
+                ("vidx", ctypes.c_int64 * MAX_SLOTS), ("v", Pt * MAX_SLOTS),
+                ("box", ctypes.c_float * 4), ("err_max", ctypes.c_float), ("pad", ctypes.c_int32),
+                ("A", ctypes.c_float * MAX_SLOTS), ("B", ctypes.c_float * MAX_SLOTS),
+                ("C", ctypes.c_float * MAX_SLOTS), ("E", ctypes.c_float * MAX_SLOTS)]
+
+
+class ReportT(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int64), ("survivors", ctypes.c_int64),
+                ("ms_extremes_kernels", ctypes.c_double), ("ms_filter_kernel", ctypes.c_double),
+                ("ms_polygon_host", ctypes.c_double), ("launches", ctypes.c_int32),
+                ("pad", ctypes.c_int32)]
+
+
+EXTREMES_BYTES = ctypes.sizeof(ExtremesT)
+
+SYMBOLS = ["cudapre_version", "cudapre_last_error", "cudapre_angles_preset",
+           "cudapre_workspace_bytes", "cudapre_workspace_init", "cudapre_extremes",
+           "cudapre_extremes_merge", "cudapre_polygon", "cudapre_filter", "cudapre_hull",
+           "cudapre_run_host"]
+
+_lib = None
+
+
+def lib():
+    """Load libcudapre.so (built by paper_1405_3454_b200.build); raise if absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_1405_3454_b200.build` "
+                          "(there is no CPU fallback)")
+    L = ctypes.CDLL(LIB_PATH)
+    vp, i64, i32, sz = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_size_t
+    P = ctypes.POINTER
+    L.cudapre_version.restype = ctypes.c_char_p
+    L.cudapre_last_error.restype = ctypes.c_char_p
+    L.cudapre_angles_preset.argtypes = [ctypes.c_int, P(i32), P(ctypes.c_double), P(ctypes.c_double)]
+    L.cudapre_workspace_bytes.argtypes = [i64]
+    L.cudapre_workspace_bytes.restype = sz
+    L.cudapre_workspace_init.argtypes = [vp, sz, vp]
+    L.cudapre_extremes.argtypes = [vp, i64, i64, i32, vp, vp, vp, sz, vp, vp, P(ExtremesT), P(ReportT)]
+    L.cudapre_extremes_merge.argtypes = [P(ExtremesT), i32, P(ExtremesT)]
+    L.cudapre_polygon.argtypes = [P(ExtremesT), P(PolygonT)]
+    L.cudapre_filter.argtypes = [vp, i64, i64, P(ExtremesT), vp, vp, i64, vp, sz, vp, P(i64),
+                                 P(PolygonT), P(ReportT)]
+    L.cudapre_hull.argtypes = [vp, vp, i64, vp, P(i64)]
+    L.cudapre_run_host.argtypes = [vp, i64, i32, vp, vp, vp, vp, sz, vp, vp, i64, vp, P(i64), P(ReportT)]
+    for name in SYMBOLS[2:]:
+        if name not in ("cudapre_workspace_bytes",):
+            getattr(L, name).restype = ctypes.c_int
+    _lib = L
+    return L
+
+
+def _check(status: int, allow=()):
+    if status != OK and status not in allow:
+        raise CudaPreError(status, lib().cudapre_last_error().decode())
+    return status
+
+
+# ------------------------------------------------------------------ angles
+def angles(preset="A"):
+    """(nang, c[8], s[8]) of a preset — correctly rounded coefficients (A5)."""
+    n = ctypes.c_int32()
+    c = (ctypes.c_double * MAX_ANGLES)()
+    s = (ctypes.c_double * MAX_ANGLES)()
+    _check(lib().cudapre_angles_preset(PRESETS.get(preset, preset), ctypes.byref(n), c, s))
+    return n.value, np.frombuffer(c, np.float64).copy(), np.frombuffer(s, np.float64).copy()
+
+
+# ------------------------------------------------------------------ torch plumbing
+def _torch():
+    import torch
+
+    return torch
+
+
+def _stream_ptr(stream=None):
+    torch = _torch()
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _points(pts):
+    torch = _torch()
+    if not isinstance(pts, torch.Tensor) or not pts.is_cuda:
+        raise TypeError("points must be a CUDA tensor of shape (n, 2), float32")
+    if pts.dtype != torch.float32 or pts.dim() != 2 or pts.shape[1] != 2 or not pts.is_contiguous():
+        raise TypeError("points must be a contiguous (n, 2) float32 tensor")
+    return pts
+
+
+class Workspace:
+    """Caller-owned device workspace (a zero-filled uint8 tensor)."""
+
+    def __init__(self, n_local: int, device=None):
+        torch = _torch()
+        self.nbytes = int(lib().cudapre_workspace_bytes(int(n_local)))
+        self.capacity_points = int(n_local)
+        self.tensor = torch.zeros(self.nbytes, dtype=torch.uint8, device=device or "cuda")
+
+    @property
+    def ptr(self):
+        return ctypes.c_void_p(self.tensor.data_ptr())
+
+
+_ws_cache: dict = {}
+
+
+def _workspace(n: int, device, ws):
+    if ws is not None:
+        return ws
+    torch = _torch()
+    dev = torch.device(device)
+    key = (dev.index if dev.index is not None else torch.cuda.current_device())
+    cur = _ws_cache.get(key)
+    if cur is None or cur.capacity_points < n:
+        cur = Workspace(max(n, 1), device=dev)
+        _ws_cache[key] = cur
+    return cur
+
+
+@dataclass
+class Extremes:
+    """Step-1 result (slot 4k+{argmin X, argmax X, argmin Y, argmax Y})."""
+    raw: ExtremesT
+
+    @property
+    def nang(self):
+        return self.raw.nang
+
+    @property
+    def n(self):
+        return self.raw.n
+
+    @property
+    def idx(self) -> np.ndarray:
+        return np.frombuffer(self.raw.idx, np.int64)[: 4 * self.nang].copy()
+
+    @property
+    def key(self) -> np.ndarray:
+        return np.frombuffer(self.raw.key, np.float64)[: 4 * self.nang].copy()
+
+    @property
+    def pt(self) -> np.ndarray:
+        return np.frombuffer(self.raw.pt, np.float32).reshape(-1, 2)[: 4 * self.nang].copy()
+
+
+@dataclass
+class Polygon:
+    raw: PolygonT
+
+    @property
+    def nv(self):
+        return self.raw.nv
+
+    @property
+    def degenerate(self):
+        return bool(self.raw.degenerate)
+
+    @property
+    def vidx(self) -> np.ndarray:
+        return np.frombuffer(self.raw.vidx, np.int64)[: self.nv].copy()
+
+    @property
+    def v(self) -> np.ndarray:
+        return np.frombuffer(self.raw.v, np.float32).reshape(-1, 2)[: self.nv].copy()
+
+    @property
+    def box(self):
+        return tuple(self.raw.box)
+
+
+def _angle_arrays(angle_set):
+    if isinstance(angle_set, (str, int)):
+        return angles(angle_set)
+    c, s = angle_set
+    c = np.asarray(c, np.float64)
+    s = np.asarray(s, np.float64)
+    cc = np.zeros(MAX_ANGLES)
+    ss = np.zeros(MAX_ANGLES)
+    cc[: len(c)] = c
+    ss[: len(s)] = s
+    return len(c), cc, ss
+
+
+# ------------------------------------------------------------------ Step 1
+def extremes(pts, angles_="A", index_base: int = 0, group=None, ws=None, stream=None,
+             report: ReportT | None = None, device_out=None) -> Extremes:
+    """Step 1 on the local shard; with ``group`` the
+    per-rank results are all-gathered (torch.distributed) and merged."""
+    torch = _torch()
+    pts = _points(pts)
+    n = pts.shape[0]
+    nang, c, s = _angle_arrays(angles_)
+    w = _workspace(n, pts.device, ws)
+    out = ExtremesT()
+    on_device = False
+    if group is not None:
+        import torch.distributed as dist
+
+        on_device = dist.get_backend(group) == "nccl"
+    dev_buf = device_out
+    if on_device and dev_buf is None:
+        dev_buf = torch.empty(EXTREMES_BYTES, dtype=torch.uint8, device=pts.device)
+    want_host = not on_device
+    st = lib().cudapre_extremes(
+        ctypes.c_void_p(pts.data_ptr()), n, index_base, nang,
+        c.ctypes.data_as(ctypes.c_void_p), s.ctypes.data_as(ctypes.c_void_p),
+        w.ptr, w.nbytes, _stream_ptr(stream),
+        ctypes.c_void_p(dev_buf.data_ptr()) if dev_buf is not None else None,
+        ctypes.byref(out) if want_host else None,
+        ctypes.byref(report) if report is not None else None)
+    if group is None:
+        _check(st)
+        return Extremes(out)
+    _check(st, allow=(ERR_EMPTY, ERR_NONFINITE))
+    return exchange(out, group, dev_buf if on_device else None)
+
+
+def exchange(local: ExtremesT, group, device_buf=None) -> Extremes:
+    """Cross-rank combine: all-gather every rank's Step-1
+    struct (NCCL: straight from the device buffer K1 wrote; gloo: host bytes)
+    and merge them with the library's lexicographic rule."""
+    torch = _torch()
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    if device_buf is not None:
+        gathered = torch.empty(world * EXTREMES_BYTES, dtype=torch.uint8, device=device_buf.device)
+        dist.all_gather_into_tensor(gathered, device_buf, group=group)
+        host = gathered.cpu().numpy().tobytes()
+    else:
+        mine = torch.frombuffer(bytearray(bytes(local)), dtype=torch.uint8)
+        bufs = [torch.empty(EXTREMES_BYTES, dtype=torch.uint8) for _ in range(world)]
+        dist.all_gather(bufs, mine, group=group)
+        host = b"".join(bytes(b.numpy().tobytes()) for b in bufs)
+    parts = (ExtremesT * world).from_buffer_copy(host)
+    return merge(list(parts))
+
+
+def merge(parts) -> Extremes:
+    """Combine per-shard Step-1 results."""
+    arr = (ExtremesT * len(parts))(*[p.raw if isinstance(p, Extremes) else p for p in parts])
+    out = ExtremesT()
+    _check(lib().cudapre_extremes_merge(arr, len(parts), ctypes.byref(out)))
+    return Extremes(out)
+
+
+# ------------------------------------------------------------------ Step 2
+def polygon(ext: Extremes) -> Polygon:
+    out = PolygonT()
+    _check(lib().cudapre_polygon(ctypes.byref(ext.raw), ctypes.byref(out)))
+    return Polygon(out)
+
+
+# ------------------------------------------------------------------ Step 3
+def filter(pts, ext: Extremes, index_base: int = 0, return_points: bool = True, ws=None,
+           out_idx=None, out_pts=None, stream=None):
+    """Steps 2+3: survivors' global indices (ascending,
+    int64 CUDA tensor), optionally their coordinates, and a report dict."""
+    torch = _torch()
+    pts = _points(pts)
+    n = pts.shape[0]
+    w = _workspace(n, pts.device, ws)
+    if out_idx is None:
+        out_idx = torch.empty(max(n, 1), dtype=torch.int64, device=pts.device)
+    if return_points and out_pts is None:
+        out_pts = torch.empty((max(n, 1), 2), dtype=torch.float32, device=pts.device)
+    cap = out_idx.shape[0]
+    if out_pts is not None:
+        cap = min(cap, out_pts.shape[0])
+    count = ctypes.c_int64()
+    poly = PolygonT()
+    rep = ReportT()
+    _check(lib().cudapre_filter(
+        ctypes.c_void_p(pts.data_ptr()), n, index_base, ctypes.byref(ext.raw),
+        ctypes.c_void_p(out_idx.data_ptr()),
+        ctypes.c_void_p(out_pts.data_ptr()) if out_pts is not None else None,
+        cap, w.ptr, w.nbytes, _stream_ptr(stream), ctypes.byref(count), ctypes.byref(poly),
+        ctypes.byref(rep)))
+    m = count.value
+    return (out_idx[:m], out_pts[:m] if out_pts is not None else None,
+            {"n": n, "survivors": m, "polygon": Polygon(poly),
+             "ms_filter_kernel": rep.ms_filter_kernel, "ms_polygon_host": rep.ms_polygon_host,
+             "launches": rep.launches})
+
+
+# ------------------------------------------------------------------ final hull
+def hull(xy, ids=None) -> np.ndarray:
+    """Canonical convex-hull ring of host points (numpy
+    (n, 2) float32 or CPU tensor), over ``ids`` if given."""
+    p = np.ascontiguousarray(np.asarray(xy, np.float32).reshape(-1, 2))
+    if ids is None:
+        m = len(p)
+        ids_a = None
+    else:
+        ids_a = np.ascontiguousarray(np.asarray(ids, np.int64))
+        m = len(ids_a)
+    ring = np.empty(max(m, 1), np.int64)
+    k = ctypes.c_int64()
+    _check(lib().cudapre_hull(p.ctypes.data_as(ctypes.c_void_p),
+                              None if ids_a is None else ids_a.ctypes.data_as(ctypes.c_void_p),
+                              m, ring.ctypes.data_as(ctypes.c_void_p), ctypes.byref(k)))
+    return ring[: k.value].copy()
+
+
+# ------------------------------------------------------------------ whole method
+def cuda_pre(pts, angles_="A", group=None, index_base: int = 0, return_points=True, ws=None):
+    """Steps 1-3.  Empty input: survivors = input, filter skipped."""
+    torch = _torch()
+    pts = _points(pts)
+    if group is None and pts.shape[0] == 0:
+        e = torch.empty(0, dtype=torch.int64, device=pts.device)
+        return e, pts[:0], {"n": 0, "survivors": 0, "skipped": True}
+    ext = extremes(pts, angles_, index_base=index_base, group=group, ws=ws)
+    idx, sp, rep = filter(pts, ext, index_base=index_base, return_points=return_points, ws=ws)
+    rep["extremes"] = ext
+    rep["skipped"] = rep["polygon"].degenerate
+    return idx, sp, rep
+
+
+def run_host(h_pts: np.ndarray, d_pts, d_surv_idx, h_surv_idx: np.ndarray, angles_="A", ws=None,
+             stream=None):
+    """End to end from host memory through the C ABI (cudapre_run_host)."""
+    n = len(h_pts)
+    nang, c, s = _angle_arrays(angles_)
+    w = _workspace(n, d_pts.device, ws)
+    count = ctypes.c_int64()
+    rep = ReportT()
+    hp = h_pts.data_ptr() if hasattr(h_pts, "data_ptr") else h_pts.ctypes.data
+    hs = h_surv_idx.data_ptr() if hasattr(h_surv_idx, "data_ptr") else h_surv_idx.ctypes.data
+    _check(lib().cudapre_run_host(
+        ctypes.c_void_p(hp), n, nang, c.ctypes.data_as(ctypes.c_void_p),
+        s.ctypes.data_as(ctypes.c_void_p), ctypes.c_void_p(d_pts.data_ptr()), w.ptr, w.nbytes,
+        ctypes.c_void_p(d_surv_idx.data_ptr()), ctypes.c_void_p(hs), d_surv_idx.shape[0],
+        _stream_ptr(stream), ctypes.byref(count), ctypes.byref(rep)))
+    return count.value, rep

@@ -1,0 +1,389 @@
+// api.cpp — the C ABI (include/cudapre.h): argument checking, workspace
+// layout, kernel launches, host Step 2, device<->host transfers, errors.
+#include <cuda_runtime.h>
+
+#include <chrono>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "internal.h"
+
+using namespace cudapre;
+
+namespace {
+
+thread_local std::string g_err;
+
+cudapre_status fail(cudapre_status st, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return st;
+}
+
+#define CUDA_TRY(expr)                                                                     \
+    do {                                                                                   \
+        cudaError_t e_ = (cudaError_t)(expr);                                              \
+        if (e_ != cudaSuccess)                                                             \
+            return fail(CUDAPRE_ERR_CUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_), \
+                        __FILE__, __LINE__);                                               \
+    } while (0)
+
+// Small pinned staging buffer per host thread for the 8-byte count and the
+// result struct (a pageable destination would force a staged synchronous copy).
+struct Staging {
+    void* p = nullptr;
+    ~Staging() {
+        if (p) cudaFreeHost(p);
+    }
+};
+thread_local Staging g_stage;
+
+cudapre_status staging(void** out) {
+    if (!g_stage.p) CUDA_TRY(cudaHostAlloc(&g_stage.p, 4096, cudaHostAllocPortable));
+    *out = g_stage.p;
+    return CUDAPRE_OK;
+}
+
+// Per-thread timing events (created on first use).
+struct Events {
+    cudaEvent_t e[4] = {nullptr, nullptr, nullptr, nullptr};
+    ~Events() {
+        for (auto& x : e)
+            if (x) cudaEventDestroy(x);
+    }
+};
+thread_local Events g_ev;
+
+cudapre_status events(cudaEvent_t** out) {
+    if (!g_ev.e[0])
+        for (auto& x : g_ev.e) CUDA_TRY(cudaEventCreate(&x));
+    *out = g_ev.e;
+    return CUDAPRE_OK;
+}
+
+// Correctly rounded coefficients (reading A5): the binary64 nearest to the
+// exact cos/sin of each angle.  Typed from the closed forms sqrt(3)/2,
+// sqrt(2)/2, sqrt(2 +- sqrt(2))/2 (tests/test_abi.py checks them against
+// 80-digit decimal evaluations).
+struct Coef {
+    double deg, c, s;
+};
+const Coef kCoef[] = {
+    {0.0, 1.0, 0.0},
+    {22.5, 0x1.d906bcf328d46p-1, 0x1.87de2a6aea963p-2},
+    {30.0, 0x1.bb67ae8584caap-1, 0x1.0p-1},
+    {45.0, 0x1.6a09e667f3bcdp-1, 0x1.6a09e667f3bcdp-1},
+    {60.0, 0x1.0p-1, 0x1.bb67ae8584caap-1},
+    {67.5, 0x1.87de2a6aea963p-2, 0x1.d906bcf328d46p-1},
+};
+
+void preset_coef(double deg, double* c, double* s) {
+    for (const Coef& k : kCoef)
+        if (k.deg == deg) {
+            *c = k.c;
+            *s = k.s;
+            return;
+        }
+}
+
+WsHeader* ws_header(void* d_ws) { return reinterpret_cast<WsHeader*>(d_ws); }
+K1Partial* ws_partials(void* d_ws) {
+    return reinterpret_cast<K1Partial*>(reinterpret_cast<char*>(d_ws) + kWsHeaderBytes);
+}
+unsigned long long* ws_status(void* d_ws) {
+    return reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(d_ws) + kWsHeaderBytes +
+                                                 kWsPartialBytes);
+}
+
+cudapre_status check_points(const cudapre_pt* d_pts, int64_t n) {
+    if (n < 0 || n > (int64_t)0xffffffffll)
+        return fail(CUDAPRE_ERR_INVALID_ARGUMENT, "n_local=%lld out of range [0, 2^32-1]", (long long)n);
+    if (n > 0 && !d_pts) return fail(CUDAPRE_ERR_INVALID_ARGUMENT, "d_pts is NULL");
+    if (((uintptr_t)d_pts & 7u) != 0)
+        return fail(CUDAPRE_ERR_INVALID_ARGUMENT, "d_pts must be 8-byte aligned");
+    return CUDAPRE_OK;
+}
+
+cudapre_status check_ws(void* d_ws, size_t ws_bytes, int64_t n) {
+    if (!d_ws || ((uintptr_t)d_ws & 15u) != 0)
+        return fail(CUDAPRE_ERR_INVALID_ARGUMENT, "d_ws must be a 16-byte aligned device pointer");
+    if (ws_bytes < ws_bytes_for(n))
+        return fail(CUDAPRE_ERR_WORKSPACE, "workspace %zu B < %zu B needed for n=%lld", ws_bytes,
+                    ws_bytes_for(n), (long long)n);
+    return CUDAPRE_OK;
+}
+
+void empty_result(cudapre_extremes_t* r, int nang, const double* c, const double* s) {
+    std::memset(r, 0, sizeof(*r));
+    r->nang = nang;
+    for (int k = 0; k < CUDAPRE_MAX_SLOTS; ++k) r->idx[k] = -1;
+    for (int k = 0; k < nang; ++k) {
+        r->c[k] = c[k];
+        r->s[k] = s[k];
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* cudapre_version(void) { return "cudapre-b200 0.1.0 (sm_100a)"; }
+
+const char* cudapre_last_error(void) { return g_err.c_str(); }
+
+cudapre_status cudapre_angles_preset(int preset, int32_t* nang, double* c, double* s) {
+    static const double lists[4][4] = {
+        {0.0, 30.0, 45.0, 60.0}, {0.0, 30.0, 45.0, 45.0}, {0.0, 0, 0, 0}, {0.0, 22.5, 45.0, 67.5}};
+    static const int counts[4] = {4, 4, 1, 4};
+    if (preset < 0 || preset > 3 || !nang || !c || !s)
+        return fail(CUDAPRE_ERR_INVALID_ARGUMENT, "unknown angle preset %d", preset);
+    *nang = counts[preset];
+    for (int k = 0; k < CUDAPRE_MAX_ANGLES; ++k) c[k] = s[k] = 0.0;
+    for (int k = 0; k < counts[preset]; ++k) preset_coef(lists[preset][k], &c[k], &s[k]);
+    return CUDAPRE_OK;
+}
+
+size_t cudapre_workspace_bytes(int64_t n_local) { return ws_bytes_for(n_local < 0 ? 0 : n_local); }
+
+cudapre_status cudapre_workspace_init(void* d_ws, size_t ws_bytes, void* stream) {
+    if (!d_ws) return fail(CUDAPRE_ERR_INVALID_ARGUMENT, "d_ws is NULL");
+    CUDA_TRY(cudaMemsetAsync(d_ws, 0, ws_bytes, (cudaStream_t)stream));
+    return CUDAPRE_OK;
+}
+
+cudapre_status cudapre_extremes(const cudapre_pt* d_pts, int64_t n_local, int64_t index_base,
+                                int32_t nang, const double* c, const double* s, void* d_ws,
+                                size_t ws_bytes, void* stream, cudapre_extremes_t* d_out,
+                                cudapre_extremes_t* h_out, cudapre_report_t* h_rep) {
+    g_err.clear();
+    double c0[CUDAPRE_MAX_ANGLES], s0[CUDAPRE_MAX_ANGLES];
+    if (!c || !s) {
+        int32_t na = 0;
+        cudapre_angles_preset(0, &na, c0, s0);
+        nang = na;
+        c = c0;
+        s = s0;
+    }
+    if (!(nang == 1 || nang == 2 || nang == 3 || nang == 4 || nang == 8))
+        return fail(CUDAPRE_ERR_INVALID_ARGUMENT, "nang=%d not in {1,2,3,4,8}", nang);
+    if (c[0] != 1.0 || s[0] != 0.0)
+        return fail(CUDAPRE_ERR_INVALID_ARGUMENT, "the first angle must be 0 degrees (c=1, s=0)");
+    for (int k = 0; k < nang; ++k)
+        if (!(c[k] >= -1.0 && c[k] <= 1.0 && s[k] >= -1.0 && s[k] <= 1.0))
+            return fail(CUDAPRE_ERR_INVALID_ARGUMENT, "angle %d: |c|,|s| must be <= 1", k);
+    cudapre_status st = check_points(d_pts, n_local);
+    if (st) return st;
+    if (h_rep) std::memset(h_rep, 0, sizeof(*h_rep));
+    cudaStream_t strm = (cudaStream_t)stream;
+    if (n_local == 0) {
+        cudapre_extremes_t r;
+        empty_result(&r, nang, c, s);
+        if (h_out) *h_out = r;
+        if (d_out) {
+            CUDA_TRY(cudaMemcpyAsync(d_out, &r, sizeof(r), cudaMemcpyHostToDevice, strm));
+            CUDA_TRY(cudaStreamSynchronize(strm));
+        }
+        return fail(CUDAPRE_ERR_EMPTY_INPUT, "empty input (n_local == 0)");
+    }
+    st = check_ws(d_ws, ws_bytes, n_local);
+    if (st) return st;
+
+    K1Params p;
+    std::memset(&p, 0, sizeof(p));
+    p.pts = reinterpret_cast<const float*>(d_pts);
+    p.n = (unsigned)n_local;
+    p.nang = nang;
+    p.base = index_base;
+    for (int k = 0; k < nang; ++k) {
+        p.c[k] = c[k];
+        p.s[k] = s[k];
+        p.cf[k] = (float)c[k];
+        p.sf[k] = (float)s[k];
+        p.nsf[k] = -(float)s[k];
+    }
+    p.ws = ws_header(d_ws);
+    p.partials = ws_partials(d_ws);
+    p.d_out = d_out;
+    if (n_local >= 65536) {
+        int64_t ch = n_local / 16384;
+        p.seed_chunks = (unsigned)(ch < 16 ? 16 : (ch > 4096 ? 4096 : ch));
+    }
+    const int vec16 = (((uintptr_t)d_pts & 15u) == 0);
+    cudaEvent_t* ev = nullptr;
+    if (h_rep) {
+        st = events(&ev);
+        if (st) return st;
+        CUDA_TRY(cudaEventRecord(ev[0], strm));
+    }
+    int launches = 0;
+    CUDA_TRY(launch_extremes(p, vec16, stream, &launches));
+    if (h_rep) CUDA_TRY(cudaEventRecord(ev[1], strm));
+    if (h_out) {
+        void* stage = nullptr;
+        st = staging(&stage);
+        if (st) return st;
+        CUDA_TRY(cudaMemcpyAsync(stage, &p.ws->result, sizeof(cudapre_extremes_t),
+                                 cudaMemcpyDeviceToHost, strm));
+        CUDA_TRY(cudaStreamSynchronize(strm));
+        std::memcpy(h_out, stage, sizeof(cudapre_extremes_t));
+    }
+    if (h_rep) {
+        float ms = 0.f;
+        CUDA_TRY(cudaEventSynchronize(ev[1]));
+        CUDA_TRY(cudaEventElapsedTime(&ms, ev[0], ev[1]));
+        h_rep->n = n_local;
+        h_rep->ms_extremes_kernels = ms;
+        h_rep->launches = launches;
+    }
+    if (h_out && h_out->nonfinite)
+        return fail(CUDAPRE_ERR_NONFINITE_INPUT, "non-finite coordinate in the input");
+    return CUDAPRE_OK;
+}
+
+cudapre_status cudapre_extremes_merge(const cudapre_extremes_t* h_parts, int32_t count,
+                                      cudapre_extremes_t* h_out) {
+    g_err.clear();
+    if (!h_parts || count < 1 || !h_out)
+        return fail(CUDAPRE_ERR_INVALID_ARGUMENT, "need >= 1 part and an output");
+    for (int p = 1; p < count; ++p)
+        if (h_parts[p].nang != h_parts[0].nang)
+            return fail(CUDAPRE_ERR_INVALID_ARGUMENT, "parts use different angle lists");
+    merge_extremes(h_parts, count, h_out);
+    if (h_out->n == 0) return fail(CUDAPRE_ERR_EMPTY_INPUT, "empty input (all parts empty)");
+    if (h_out->nonfinite) return fail(CUDAPRE_ERR_NONFINITE_INPUT, "non-finite coordinate in the input");
+    return CUDAPRE_OK;
+}
+
+cudapre_status cudapre_polygon(const cudapre_extremes_t* h_ext, cudapre_polygon_t* h_poly) {
+    g_err.clear();
+    if (!h_ext || !h_poly) return fail(CUDAPRE_ERR_INVALID_ARGUMENT, "NULL argument");
+    if (h_ext->n <= 0) return fail(CUDAPRE_ERR_EMPTY_INPUT, "empty input");
+    if (h_ext->nang < 1 || h_ext->nang > CUDAPRE_MAX_ANGLES)
+        return fail(CUDAPRE_ERR_INVALID_ARGUMENT, "bad nang in extremes");
+    build_polygon(*h_ext, h_poly, nullptr);
+    return CUDAPRE_OK;
+}
+
+cudapre_status cudapre_filter(const cudapre_pt* d_pts, int64_t n_local, int64_t index_base,
+                              const cudapre_extremes_t* h_ext, int64_t* d_surv_idx,
+                              cudapre_pt* d_surv_pts, int64_t capacity, void* d_ws, size_t ws_bytes,
+                              void* stream, int64_t* h_count, cudapre_polygon_t* h_poly,
+                              cudapre_report_t* h_rep) {
+    g_err.clear();
+    cudapre_status st = check_points(d_pts, n_local);
+    if (st) return st;
+    if (!h_ext || !h_count) return fail(CUDAPRE_ERR_INVALID_ARGUMENT, "h_ext and h_count are required");
+    if (capacity < 0) return fail(CUDAPRE_ERR_INVALID_ARGUMENT, "capacity < 0");
+    if (n_local > 0 && !d_surv_idx) return fail(CUDAPRE_ERR_INVALID_ARGUMENT, "d_surv_idx is NULL");
+    if (h_ext->nonfinite) return fail(CUDAPRE_ERR_NONFINITE_INPUT, "non-finite coordinate in the input");
+    if (h_ext->n <= 0) return fail(CUDAPRE_ERR_EMPTY_INPUT, "empty input");
+    if (h_ext->nang < 1 || h_ext->nang > CUDAPRE_MAX_ANGLES)
+        return fail(CUDAPRE_ERR_INVALID_ARGUMENT, "bad nang in extremes");
+    if (h_rep) std::memset(h_rep, 0, sizeof(*h_rep));
+
+    K2Params p;
+    std::memset(&p, 0, sizeof(p));
+    cudapre_polygon_t poly;
+    const auto t0 = std::chrono::steady_clock::now();
+    build_polygon(*h_ext, &poly, &p);
+    const auto t1 = std::chrono::steady_clock::now();
+    if (h_poly) *h_poly = poly;
+    if (h_rep) {
+        h_rep->n = n_local;
+        h_rep->ms_polygon_host = std::chrono::duration<double, std::milli>(t1 - t0).count();
+    }
+    *h_count = 0;
+    if (n_local == 0) return CUDAPRE_OK;
+    st = check_ws(d_ws, ws_bytes, n_local);
+    if (st) return st;
+
+    cudaStream_t strm = (cudaStream_t)stream;
+    p.pts = reinterpret_cast<const float*>(d_pts);
+    p.n = (unsigned)n_local;
+    p.base = index_base;
+    p.out_idx = reinterpret_cast<long long*>(d_surv_idx);
+    p.out_pts = reinterpret_cast<float*>(d_surv_pts);
+    p.capacity = (unsigned long long)capacity;
+    p.ws = ws_header(d_ws);
+    p.status = ws_status(d_ws);
+    p.num_tiles = (unsigned)ws_tiles(n_local);
+    const int vec16 = (((uintptr_t)d_pts & 15u) == 0);
+
+    cudaEvent_t* ev = nullptr;
+    if (h_rep) {
+        st = events(&ev);
+        if (st) return st;
+        CUDA_TRY(cudaEventRecord(ev[2], strm));
+    }
+    int launches = 0;
+    CUDA_TRY(launch_filter(p, vec16, stream, &launches));
+    if (h_rep) CUDA_TRY(cudaEventRecord(ev[3], strm));
+    void* stage = nullptr;
+    st = staging(&stage);
+    if (st) return st;
+    CUDA_TRY(cudaMemcpyAsync(stage, &p.ws->count, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                             strm));
+    CUDA_TRY(cudaStreamSynchronize(strm));
+    const int64_t count = (int64_t) * reinterpret_cast<unsigned long long*>(stage);
+    *h_count = count;
+    if (h_rep) {
+        float ms = 0.f;
+        CUDA_TRY(cudaEventElapsedTime(&ms, ev[2], ev[3]));
+        h_rep->ms_filter_kernel = ms;
+        h_rep->survivors = count;
+        h_rep->launches = launches;
+    }
+    if (count > capacity)
+        return fail(CUDAPRE_ERR_CAPACITY, "%lld survivors > capacity %lld", (long long)count,
+                    (long long)capacity);
+    return CUDAPRE_OK;
+}
+
+cudapre_status cudapre_hull(const cudapre_pt* h_pts, const int64_t* h_ids, int64_t n,
+                            int64_t* h_ring, int64_t* h_ring_len) {
+    g_err.clear();
+    if (n < 0 || !h_ring_len || (n > 0 && (!h_pts || !h_ring)))
+        return fail(CUDAPRE_ERR_INVALID_ARGUMENT, "bad hull arguments");
+    *h_ring_len = n == 0 ? 0 : hull_ring(h_pts, h_ids, n, h_ring);
+    return CUDAPRE_OK;
+}
+
+cudapre_status cudapre_run_host(const cudapre_pt* h_pts, int64_t n, int32_t nang, const double* c,
+                                const double* s, cudapre_pt* d_pts, void* d_ws, size_t ws_bytes,
+                                int64_t* d_surv_idx, int64_t* h_surv_idx, int64_t capacity,
+                                void* stream, int64_t* h_count, cudapre_report_t* h_rep) {
+    g_err.clear();
+    if (n < 0 || (n > 0 && (!h_pts || !d_pts || !h_surv_idx || !d_surv_idx)) || !h_count)
+        return fail(CUDAPRE_ERR_INVALID_ARGUMENT, "bad run_host arguments");
+    cudaStream_t strm = (cudaStream_t)stream;
+    if (n > 0)
+        CUDA_TRY(cudaMemcpyAsync(d_pts, h_pts, (size_t)n * sizeof(cudapre_pt), cudaMemcpyHostToDevice,
+                                 strm));
+    cudapre_extremes_t ext;
+    cudapre_report_t r1, r2;
+    cudapre_status st = cudapre_extremes(d_pts, n, 0, nang, c, s, d_ws, ws_bytes, stream, nullptr, &ext,
+                                         h_rep ? &r1 : nullptr);
+    if (st) return st;
+    st = cudapre_filter(d_pts, n, 0, &ext, d_surv_idx, nullptr, capacity, d_ws, ws_bytes, stream,
+                        h_count, nullptr, h_rep ? &r2 : nullptr);
+    if (st && st != CUDAPRE_ERR_CAPACITY) return st;
+    const int64_t m = *h_count < capacity ? *h_count : capacity;
+    if (m > 0)
+        CUDA_TRY(cudaMemcpyAsync(h_surv_idx, d_surv_idx, (size_t)m * sizeof(int64_t),
+                                 cudaMemcpyDeviceToHost, strm));
+    CUDA_TRY(cudaStreamSynchronize(strm));
+    if (h_rep) {
+        *h_rep = r2;
+        h_rep->ms_extremes_kernels = r1.ms_extremes_kernels;
+        h_rep->launches = r1.launches + r2.launches;
+    }
+    return st;
+}
+
+}  // extern "C"

@@ -1,0 +1,264 @@
+// host_geom.cpp — host side of the CudaPre pipeline:
+//   * Step 2: Andrew's monotone chain of the <= 16 extreme
+//     points with the exact orientation predicate (A10, A11), and the
+//     parameters the Step-3 kernel needs (per-edge float line coefficients with
+//     rigorous error bounds, an inner box) — DESIGN.md §6.2.
+//   * the final hull of the survivors, canonical ring (A17).
+//   * the cross-shard merge of Step-1 results.
+// Compiled with -ffp-contract=off (no FMA contraction anywhere in this file).
+#include <algorithm>
+#include <cfloat>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "exact.cuh"
+#include "internal.h"
+
+namespace cudapre {
+
+int orient_exact(float ax, float ay, float bx, float by, float cx, float cy) {
+    return orient_sign_f(ax, ay, bx, by, cx, cy);
+}
+
+namespace {
+
+struct CP {
+    float x, y;
+    int64_t id;
+};
+
+bool lex_less(const CP& a, const CP& b) {
+    if (a.x < b.x) return true;
+    if (a.x > b.x) return false;
+    if (a.y < b.y) return true;
+    if (a.y > b.y) return false;
+    return a.id < b.id;
+}
+
+int turn(const CP& a, const CP& b, const CP& c) { return orient_exact(a.x, a.y, b.x, b.y, c.x, c.y); }
+
+// Andrew's monotone chain over P (sorted in place).  Writes ring ids, returns length.
+int64_t chain(std::vector<CP>& P, int64_t* ring) {
+    const int64_t m = (int64_t)P.size();
+    if (m == 0) return 0;
+    std::sort(P.begin(), P.end(), lex_less);
+    // distinct coordinates: first of each run has the lowest id (-0 == +0)
+    int64_t u = 1;
+    for (int64_t j = 1; j < m; ++j)
+        if (P[j].x != P[u - 1].x || P[j].y != P[u - 1].y) P[u++] = P[j];
+    if (u == 1) {
+        ring[0] = P[0].id;
+        return 1;
+    }
+    std::vector<CP> H((size_t)(2 * u + 1));
+    int64_t k = 0;
+    for (int64_t j = 0; j < u; ++j) {   // lower chain, pop while not a strict left turn
+        while (k >= 2 && turn(H[k - 2], H[k - 1], P[j]) <= 0) --k;
+        H[k++] = P[j];
+    }
+    const int64_t lower = k;
+    for (int64_t j = u - 2; j >= 0; --j) {   // upper chain
+        while (k > lower && turn(H[k - 2], H[k - 1], P[j]) <= 0) --k;
+        H[k++] = P[j];
+    }
+    --k;   // the last point repeats the first
+    for (int64_t j = 0; j < k; ++j) ring[j] = H[j].id;
+    return k;
+}
+
+// float nearest-below / nearest-above of a double (directed conversion)
+float f_down(double d) {
+    float f = (float)d;
+    if ((double)f > d) f = std::nextafter(f, -INFINITY);
+    return f;
+}
+float f_up(double d) {
+    float f = (float)d;
+    if ((double)f < d) f = std::nextafter(f, INFINITY);
+    return f;
+}
+
+bool strictly_inside_ring(const cudapre_pt* v, int nv, float px, float py) {
+    for (int j = 0; j < nv; ++j) {
+        const cudapre_pt& a = v[j];
+        const cudapre_pt& b = v[(j + 1) % nv];
+        if (orient_exact(a.x, a.y, b.x, b.y, px, py) <= 0) return false;
+    }
+    return true;
+}
+
+}  // namespace
+
+int64_t hull_ring(const cudapre_pt* pts, const int64_t* ids, int64_t n, int64_t* ring) {
+    std::vector<CP> P((size_t)n);
+    for (int64_t j = 0; j < n; ++j) {
+        const int64_t id = ids ? ids[j] : j;
+        P[j] = CP{pts[id].x, pts[id].y, id};
+    }
+    return chain(P, ring);
+}
+
+void merge_extremes(const cudapre_extremes_t* parts, int count, cudapre_extremes_t* out) {
+    cudapre_extremes_t r = parts[0];
+    r.n = 0;
+    r.nonfinite = 0;
+    const int slots = 4 * r.nang;
+    for (int s = 0; s < slots; ++s) r.idx[s] = -1;
+    for (int p = 0; p < count; ++p) {
+        const cudapre_extremes_t& q = parts[p];
+        r.n += q.n;
+        r.nonfinite |= q.nonfinite;
+        for (int s = 0; s < slots; ++s) {
+            if (q.idx[s] < 0) continue;
+            const bool is_max = (s & 1) != 0;
+            bool better;
+            if (r.idx[s] < 0) {
+                better = true;
+            } else if (q.key[s] == r.key[s]) {
+                better = q.idx[s] < r.idx[s];   // lowest global index on equal keys (A7)
+            } else {
+                better = is_max ? (q.key[s] > r.key[s]) : (q.key[s] < r.key[s]);
+            }
+            if (better) {
+                r.idx[s] = q.idx[s];
+                r.key[s] = q.key[s];
+                r.pt[s] = q.pt[s];
+            }
+        }
+    }
+    *out = r;
+}
+
+void build_polygon(const cudapre_extremes_t& ext, cudapre_polygon_t* poly, K2Params* kp) {
+    std::memset(poly, 0, sizeof(*poly));
+    const int slots = 4 * ext.nang;
+    // ---- Step 2: distinct picks -> monotone chain (A9, A10)
+    std::vector<CP> P;
+    std::vector<cudapre_pt> byid;
+    for (int s = 0; s < slots; ++s)
+        if (ext.idx[s] >= 0) P.push_back(CP{ext.pt[s].x, ext.pt[s].y, ext.idx[s]});
+    {
+        std::vector<CP> Q = P;
+        std::sort(Q.begin(), Q.end(), lex_less);
+        int d = Q.empty() ? 0 : 1;
+        for (size_t j = 1; j < Q.size(); ++j)
+            if (Q[j].x != Q[j - 1].x || Q[j].y != Q[j - 1].y) ++d;
+        poly->n_distinct = d;
+    }
+    int64_t ring[CUDAPRE_MAX_SLOTS];
+    std::vector<CP> Pc = P;
+    const int nv = (int)chain(Pc, ring);
+    poly->nv = nv;
+    for (int j = 0; j < nv; ++j) {
+        poly->vidx[j] = ring[j];
+        for (const CP& c : P)
+            if (c.id == ring[j]) { poly->v[j] = cudapre_pt{c.x, c.y}; break; }
+    }
+    poly->degenerate = nv < 3;
+    poly->box[0] = 1.0f;
+    poly->box[1] = 0.0f;   // empty box
+    poly->box[2] = 1.0f;
+    poly->box[3] = 0.0f;
+    if (kp) {
+        kp->nv = nv;
+        kp->mode = poly->degenerate ? 1 : 0;
+        kp->bx0 = 1.0f; kp->bx1 = 0.0f; kp->by0 = 1.0f; kp->by1 = 0.0f;
+        kp->e2max = 0.0f;
+        for (int j = 0; j <= nv && j <= CUDAPRE_MAX_SLOTS; ++j) {
+            kp->vx[j] = poly->v[j % (nv ? nv : 1)].x;
+            kp->vy[j] = poly->v[j % (nv ? nv : 1)].y;
+        }
+    }
+    if (poly->degenerate) return;
+
+    // ---- exact data bounding box: the angle-0 picks (slots 0..3 = min x, max x,
+    //      min y, max y of the whole point set; c0 = 1, s0 = 0).
+    const double xmin = ext.pt[0].x, xmax = ext.pt[1].x, ymin = ext.pt[2].y, ymax = ext.pt[3].y;
+    const double Mx = std::max(std::fabs(xmin), std::fabs(xmax));
+    const double My = std::max(std::fabs(ymin), std::fabs(ymax));
+
+    // ---- per-edge float line g_j(p) = A px + B py + C'.
+    // orient(a, b, p) = A p.x + B p.y + C with A = ay-by, B = bx-ax, C = ax*by-ay*bx.
+    // E_j bounds |float evaluation - exact orient| over the bbox with a factor
+    // >= 2.6 of slack: coefficient rounding <= 2^-23 S, the two fma roundings
+    // <= 2^-23 S', subnormal / absolute terms <= 2^-140 (Mx+My+1) + 2^-126.
+    bool exact_only = false;
+    float emax = 0.0f;
+    for (int j = 0; j < nv; ++j) {
+        const double ax = poly->v[j].x, ay = poly->v[j].y;
+        const double bx = poly->v[(j + 1) % nv].x, by = poly->v[(j + 1) % nv].y;
+        const double A = ay - by, B = bx - ax, C = ax * by - ay * bx;
+        const double S = std::fabs(A) * Mx + std::fabs(B) * My + std::fabs(C);
+        const double Ed = S * 0x1p-20 + (Mx + My + 1.0) * 0x1p-140 + 0x1p-126;
+        const float E = f_up(Ed);
+        const float Cl = f_down(C - (double)E);
+        const float Af = (float)A, Bf = (float)B;
+        if (!(S < 1e36) || !std::isfinite(E) || !std::isfinite(Cl) || !std::isfinite(Af) ||
+            !std::isfinite(Bf))
+            exact_only = true;
+        emax = std::max(emax, E);
+        poly->A[j] = Af;
+        poly->B[j] = Bf;
+        poly->C[j] = Cl;
+        poly->E[j] = E;
+        if (kp) {
+            kp->A[j] = Af;
+            kp->B[j] = Bf;
+            kp->C[j] = Cl;
+        }
+    }
+    if (!(emax < 1e37f)) exact_only = true;
+    poly->err_max = emax;
+    poly->exact_only = exact_only;
+
+    // ---- inner box: centred at the vertex mean, the largest scale (binary
+    //      search) whose 4 float corners are strictly inside every edge,
+    //      checked with the exact predicate.  Convexity => the closed box is
+    //      strictly inside.
+    double ox = 0, oy = 0, pxmin = poly->v[0].x, pxmax = pxmin, pymin = poly->v[0].y, pymax = pymin;
+    for (int j = 0; j < nv; ++j) {
+        ox += poly->v[j].x;
+        oy += poly->v[j].y;
+        pxmin = std::min(pxmin, (double)poly->v[j].x);
+        pxmax = std::max(pxmax, (double)poly->v[j].x);
+        pymin = std::min(pymin, (double)poly->v[j].y);
+        pymax = std::max(pymax, (double)poly->v[j].y);
+    }
+    ox /= nv;
+    oy /= nv;
+    const double hw = 0.5 * (pxmax - pxmin), hh = 0.5 * (pymax - pymin);
+    double lo = 0.0, hi = 1.0;
+    bool have = false;
+    float best[4] = {1.0f, 0.0f, 1.0f, 0.0f};
+    if (std::isfinite(ox) && std::isfinite(oy) && std::isfinite(hw) && std::isfinite(hh)) {
+        for (int it = 0; it < 40; ++it) {
+            const double t = (it == 0) ? 1.0 : 0.5 * (lo + hi);
+            const float x0 = f_up(ox - t * hw), x1 = f_down(ox + t * hw);
+            const float y0 = f_up(oy - t * hh), y1 = f_down(oy + t * hh);
+            bool ok = x0 <= x1 && y0 <= y1 && strictly_inside_ring(poly->v, nv, x0, y0) &&
+                      strictly_inside_ring(poly->v, nv, x1, y0) &&
+                      strictly_inside_ring(poly->v, nv, x1, y1) &&
+                      strictly_inside_ring(poly->v, nv, x0, y1);
+            if (ok) {
+                have = true;
+                best[0] = x0; best[1] = x1; best[2] = y0; best[3] = y1;
+                lo = t;
+                if (it == 0) break;
+            } else {
+                hi = t;
+            }
+        }
+    }
+    if (have) std::memcpy(poly->box, best, sizeof(best));
+    if (kp) {
+        kp->mode = exact_only ? 2 : 0;
+        kp->e2max = 2.0f * emax;
+        kp->bx0 = poly->box[0];
+        kp->bx1 = poly->box[1];
+        kp->by0 = poly->box[2];
+        kp->by1 = poly->box[3];
+    }
+}
+
+}  // namespace cudapre

@@ -1,0 +1,101 @@
+// internal.h — shared declarations of the CudaPre B200 library (not part of the ABI).
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+
+#include "../../include/cudapre.h"
+
+namespace cudapre {
+
+// ---------------------------------------------------------------- launch shape
+constexpr int kK1Threads = 256;        // K1 block
+constexpr int kK1Unroll = 4;           // float4 (= 2 points) per thread per iteration
+constexpr int kSeedThreads = 128;      // seed block; one chunk = 128 float4 = 256 points
+constexpr int kK2Threads = 256;        // K2 block
+constexpr int kK2Items = 4;            // float4 per thread per tile
+constexpr int kK2TilePairs = kK2Threads * kK2Items;   // 1024 pairs
+constexpr int kK2TilePts = 2 * kK2TilePairs;          // 2048 points per tile
+constexpr int kMaxK1Blocks = 148 * 16;
+
+// ---------------------------------------------------------------- workspace
+// Device workspace layout (caller-owned, zero-filled once):
+//   [WsHeader, padded to 4 KiB][K1Partial x kMaxK1Blocks x 32][tile status x ntiles]
+// Every kernel leaves the counters it uses back at their reset values, so the
+// workspace stays valid from call to call.
+struct alignas(16) WsHeader {
+    unsigned int k1_ticket;      // K1 blocks finished (last-block finalize)
+    unsigned int k1_nonfinite;   // set by K1's exact path on NaN/Inf input
+    unsigned int k2_ticket;      // K2 dynamic tile counter
+    unsigned int k2_done;        // K2 blocks finished
+    unsigned int epoch;          // K2 tile-status epoch (never 0 after the first call)
+    unsigned int pad0[3];
+    unsigned long long count;    // K2 survivors (written by the last tile)
+    unsigned long long pad1;
+    unsigned int seed[CUDAPRE_MAX_SLOTS];   // seed thresholds, order-preserving encoding, 0 = none
+    cudapre_extremes_t result;   // K1 final result
+};
+static_assert(sizeof(WsHeader) <= 4096, "header too large");
+
+struct K1Partial {
+    double key;
+    unsigned int idx;   // local index, 0xffffffff = none
+    unsigned int pad;
+};
+
+constexpr size_t kWsHeaderBytes = 4096;
+constexpr size_t kWsPartialBytes = sizeof(K1Partial) * kMaxK1Blocks * CUDAPRE_MAX_SLOTS;
+
+inline size_t ws_tiles(int64_t n) { return (size_t)((n + kK2TilePts - 1) / kK2TilePts); }
+inline size_t ws_bytes_for(int64_t n) {
+    return kWsHeaderBytes + kWsPartialBytes + 8 * (ws_tiles(n) + 1);
+}
+
+// ---------------------------------------------------------------- kernel params
+struct K1Params {
+    const float* pts;         // n points, x y interleaved
+    unsigned int n;
+    int nang;
+    long long base;           // global index of pts[0]
+    float cf[CUDAPRE_MAX_ANGLES], sf[CUDAPRE_MAX_ANGLES], nsf[CUDAPRE_MAX_ANGLES];
+    double c[CUDAPRE_MAX_ANGLES], s[CUDAPRE_MAX_ANGLES];
+    WsHeader* ws;
+    K1Partial* partials;
+    cudapre_extremes_t* d_out;   // nullable extra copy of the result
+    unsigned int seed_chunks;    // number of 256-point sample chunks (0 = no seed)
+};
+
+struct K2Params {
+    const float* pts;
+    unsigned int n;
+    int nv;                   // ring length
+    long long base;
+    long long* out_idx;
+    float* out_pts;           // nullable, float2 per survivor
+    unsigned long long capacity;
+    WsHeader* ws;
+    unsigned long long* status;   // ntiles tile-status words
+    unsigned int num_tiles;
+    int mode;                 // 0 = filter, 1 = keep everything (degenerate), 2 = exact only
+    float bx0, bx1, by0, by1; // inner box (closed), strictly inside the ring
+    float e2max;              // 2 * max_j E_j
+    float A[CUDAPRE_MAX_SLOTS], B[CUDAPRE_MAX_SLOTS], C[CUDAPRE_MAX_SLOTS];   // C already lowered by E_j
+    float vx[CUDAPRE_MAX_SLOTS + 1], vy[CUDAPRE_MAX_SLOTS + 1];               // ring, v[nv] = v[0]
+};
+
+// ---------------------------------------------------------------- launchers (.cu)
+// All return a cudaError_t as int (0 = success).
+int launch_extremes(const K1Params& p, int vec16, void* stream, int* launches);
+int launch_filter(const K2Params& p, int vec16, void* stream, int* launches);
+int device_sm_count();
+
+// ---------------------------------------------------------------- host geometry (host_geom.cpp)
+int orient_exact(float ax, float ay, float bx, float by, float cx, float cy);
+// Build the polygon + K2 coefficients from global extremes.  Fills poly and,
+// if kp != nullptr, the geometric fields of kp (nv, mode, box, A/B/C, e2max, v).
+void build_polygon(const cudapre_extremes_t& ext, cudapre_polygon_t* poly, K2Params* kp);
+// Canonical monotone-chain ring of pts[ids[j]] (ids nullptr = identity).
+int64_t hull_ring(const cudapre_pt* pts, const int64_t* ids, int64_t n, int64_t* ring);
+void merge_extremes(const cudapre_extremes_t* parts, int count, cudapre_extremes_t* out);
+
+}  // namespace cudapre

@@ -1,0 +1,239 @@
+"""C-ABI and host-logic tests (no GPU needed).
+
+* libcudapre.so loads and exports every function include/cudapre.h declares;
+* the host-side pieces of the product (Step 2 polygon + kernel parameters,
+  final hull, shard merge, angle presets) agree with the oracle / closed forms;
+* the Step-3 kernel's float fast path (inner box, per-edge bounds E_j) is
+  emulated EXACTLY here (fractions, correctly rounded float32 fma) on points
+  hugging the polygon's edges, proving its decisions agree with the exact
+  predicate before any GPU run.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+from decimal import Decimal, getcontext
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+import paper_1405_3454_b200 as cp
+import synth
+from tests import brute
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def L():
+    from paper_1405_3454_b200 import build
+
+    build.build()
+    return cp.lib()
+
+
+def test_exports_every_declared_symbol(L):
+    hdr = open(os.path.join(ROOT, "include", "cudapre.h")).read()
+    declared = set(re.findall(r"^\s*(?:const\s+)?[\w\s\*]+?\b(cudapre_\w+)\s*\(", hdr, re.M))
+    assert len(declared) >= 11
+    for name in declared:
+        assert hasattr(L, name), name
+    assert set(cp.SYMBOLS) == declared
+    assert b"sm_100a" in L.cudapre_version()
+
+
+def test_struct_sizes_match_header(L):
+    # offsets derived from the C layout rules of include/cudapre.h
+    assert ctypes.sizeof(cp.ExtremesT) == 8 + 8 + 32 * 8 + 32 * 8 + 32 * 8 + 8 * 8 + 8 * 8
+    assert ctypes.sizeof(cp.PolygonT) == 16 + 32 * 8 + 32 * 8 + 16 + 8 + 4 * 32 * 4
+    assert ctypes.sizeof(cp.ReportT) == 48
+
+
+def test_angle_presets_correctly_rounded(L):
+    """Reading A5, independently of the oracle: decimal closed forms."""
+    getcontext().prec = 80
+    s2, s3 = Decimal(2).sqrt(), Decimal(3).sqrt()
+    want = {
+        "A": [(1, 0), (s3 / 2, Decimal(1) / 2), (s2 / 2, s2 / 2), (Decimal(1) / 2, s3 / 2)],
+        "B": [(1, 0), (s3 / 2, Decimal(1) / 2), (s2 / 2, s2 / 2), (s2 / 2, s2 / 2)],
+        "AT": [(1, 0)],
+        "C": [(1, 0), ((2 + s2).sqrt() / 2, (2 - s2).sqrt() / 2), (s2 / 2, s2 / 2),
+              ((2 - s2).sqrt() / 2, (2 + s2).sqrt() / 2)],
+    }
+    for name, cs in want.items():
+        n, c, s = cp.angles(name)
+        assert n == len(cs)
+        for k, (cc, ss) in enumerate(cs):
+            assert c[k] == float(Decimal(cc)) and s[k] == float(Decimal(ss)), (name, k)
+
+
+def test_empty_and_bad_args_without_gpu(L):
+    """Argument errors are reported before any CUDA call."""
+    st = L.cudapre_extremes(None, -1, 0, 4, None, None, None, 0, None, None, None, None)
+    assert st == cp.ERR_ARG
+    assert b"out of range" in L.cudapre_last_error()
+    bad = np.zeros(8)
+    bad[0] = 0.5
+    st = L.cudapre_extremes(None, 5, 0, 4, bad.ctypes.data_as(ctypes.c_void_p),
+                            np.zeros(8).ctypes.data_as(ctypes.c_void_p), None, 0, None, None,
+                            None, None)
+    assert st == cp.ERR_ARG
+    assert L.cudapre_workspace_bytes(10 ** 9) > 8 * (10 ** 9 // 2048)
+
+
+# ------------------------------------------------------------ host-side pieces
+def _ext_from_oracle(oracle, xy, angles="A", base=0, lo=0, hi=None):
+    """A cudapre_extremes_t for xy[lo:hi] built from the ORACLE's Step 1."""
+    hi = len(xy) if hi is None else hi
+    r = cp.ExtremesT()
+    nang, c, s = cp.angles(angles)
+    r.nang = nang
+    r.n = hi - lo
+    for k in range(32):
+        r.idx[k] = -1
+    for k in range(8):
+        r.c[k], r.s[k] = c[k], s[k]
+    if hi > lo:
+        idx, key = oracle.extremes(xy[lo:hi], angles, with_keys=True)
+        for k in range(4 * nang):
+            r.idx[k] = int(idx[k]) + base + lo
+            r.key[k] = float(key[k])
+            r.pt[k].x, r.pt[k].y = map(float, xy[lo + idx[k]])
+    return r
+
+
+@pytest.mark.parametrize("family", ["square", "disk", "gauss", "circle"])
+def test_hull_matches_oracle(L, oracle_lib, family):
+    for n in (1, 2, 3, 17, 1000, 50_000):
+        xy = synth.generate(family, n, seed=n)
+        assert cp.hull(xy).tolist() == oracle_lib.hull(xy).tolist()
+    grid = np.random.default_rng(0).integers(-3, 4, (500, 2)).astype(np.float32)
+    assert cp.hull(grid).tolist() == oracle_lib.hull(grid).tolist()
+    a11 = np.array([[2.0 ** -60, 0.0], [1.0, 1.0], [1 + 2.0 ** -23, 1 + 2.0 ** -23]], np.float32)
+    assert cp.hull(a11).tolist() == oracle_lib.hull(a11).tolist() == [0, 2, 1]
+
+
+def test_product_orient_vs_fractions(L, oracle_lib):
+    """The product's exact predicate (expansions) on the oracle's hard cases,
+    through the hull of 3 points (orientation sign decides the ring)."""
+    rng = np.random.default_rng(11)
+    from tests.test_oracle_pins import _float_triples
+
+    for a, b, c in _float_triples(rng, 3000):
+        pts = np.array([a, b, c], np.float32)
+        ring = cp.hull(pts)
+        assert ring.tolist() == brute.gift_wrap(pts), pts
+
+
+@pytest.mark.parametrize("family", ["square", "disk", "gauss", "circle"])
+@pytest.mark.parametrize("angles", ["A", "B", "C", "AT"])
+def test_polygon_matches_oracle(L, oracle_lib, family, angles):
+    xy = synth.generate(family, 20_000, seed=5)
+    ext = cp.Extremes(_ext_from_oracle(oracle_lib, xy, angles))
+    poly = cp.polygon(ext)
+    want = oracle_lib.polygon(xy, oracle_lib.extremes(xy, angles))
+    assert poly.vidx.tolist() == want.tolist()
+    assert poly.degenerate == (len(want) < 3)
+    x0, x1, y0, y1 = poly.box
+    if not poly.degenerate and x0 <= x1:
+        ring = xy[want]
+        for corner in ((x0, y0), (x1, y0), (x1, y1), (x0, y1)):
+            assert brute.strictly_inside_frac(ring, corner)
+
+
+def test_merge_equals_single_shard(L, oracle_lib):
+    """any sharding merges to the single-set result (incl. empty shards
+    and ties across shard borders)."""
+    xy = np.round(synth.generate("disk", 30_001, seed=8) * 16).astype(np.float32)  # heavy ties
+    whole = _ext_from_oracle(oracle_lib, xy)
+    rng = np.random.default_rng(1)
+    for _ in range(20):
+        cuts = sorted(rng.integers(0, len(xy), rng.integers(1, 6)).tolist())
+        bounds = [0, *cuts, len(xy)]
+        parts = [_ext_from_oracle(oracle_lib, xy, lo=a, hi=b) for a, b in zip(bounds, bounds[1:])]
+        m = cp.merge(parts)
+        assert m.idx.tolist() == list(whole.idx[:16])
+        assert m.n == len(xy)
+    with pytest.raises(cp.CudaPreError):
+        cp.merge([_ext_from_oracle(oracle_lib, xy, lo=0, hi=0)])
+
+
+# ------------------------------------------------------------ K2 float path, emulated exactly
+def _rn32(q: Fraction) -> np.float32:
+    """Correctly rounded (nearest-even) float32 of an exact rational."""
+    f = np.float32(float(q))
+    best = f
+    for g in (np.nextafter(f, np.float32(-np.inf)), np.nextafter(f, np.float32(np.inf))):
+        if not np.isfinite(g):
+            continue
+        db, dg = abs(Fraction(float(best)) - q), abs(Fraction(float(g)) - q)
+        if dg < db or (dg == db and (int(g.view(np.uint32)) & 1) == 0):
+            best = g
+    return best
+
+
+def _fma32(a, b, c) -> np.float32:
+    return _rn32(Fraction(float(a)) * Fraction(float(b)) + Fraction(float(c)))
+
+
+def test_k2_float_decisions_are_conservative(L, oracle_lib):
+    """with the library's A, B, C', E, inner box, the kernel's
+    decisions (box -> discard; min g > 0 -> discard; RN(min g + 2Emax) < 0 ->
+    keep) never contradict the exact predicate, on points within a few ulp of
+    the polygon's edges and vertices."""
+    lib = cp.lib()
+    xy = synth.generate("disk", 50_000, seed=13)
+    ext = _ext_from_oracle(oracle_lib, xy)
+    poly = cp.PolygonT()
+    assert lib.cudapre_polygon(ctypes.byref(ext), ctypes.byref(poly)) == 0
+    nv = poly.nv
+    V = np.array([[poly.v[j].x, poly.v[j].y] for j in range(nv)], np.float32)
+    coef = [(np.float32(poly.A[j]), np.float32(poly.B[j]), np.float32(poly.C[j]), np.float32(poly.E[j]))
+            for j in range(nv)]
+    # E_j really bounds the float error of the kernel's expression over the bbox
+    Mx = max(abs(float(xy[:, 0].min())), abs(float(xy[:, 0].max())))
+    My = max(abs(float(xy[:, 1].min())), abs(float(xy[:, 1].max())))
+    for j in range(nv):
+        ax, ay = map(Fraction, map(float, V[j]))
+        bx, by = map(Fraction, map(float, V[(j + 1) % nv]))
+        A, B, C = ay - by, bx - ax, ax * by - ay * bx
+        S = abs(A) * Fraction(Mx) + abs(B) * Fraction(My) + abs(C)
+        assert Fraction(float(coef[j][3])) >= S * Fraction(1, 2 ** 20)
+    e2max = np.float32(2 * max(c[3] for c in coef))
+    assert float(e2max) == 2 * poly.err_max
+    rng = np.random.default_rng(4)
+    checked = decided = 0
+    for j in range(nv):
+        a, b = V[j].astype(np.float64), V[(j + 1) % nv].astype(np.float64)
+        nrm = np.array([a[1] - b[1], b[0] - a[0]])   # inward normal (CCW ring)
+        nrm /= np.hypot(*nrm)
+        for t in rng.uniform(-0.05, 1.05, 40):
+            base = a + t * (b - a)
+            pts = []
+            for d in (-3, -1, 0, 1, 3):          # within a few ulp of the edge line
+                p = base.astype(np.float32)
+                if d:
+                    p = np.array([np.nextafter(p[0], np.float32(np.sign(d) * np.inf)), p[1]], np.float32)
+                    for _ in range(abs(d) - 1):
+                        p[1] = np.nextafter(p[1], np.float32(np.sign(d) * np.inf))
+                pts.append(p)
+            for off in (-1e-3, -1e-5, -1e-6, 1e-6, 1e-5, 1e-3):   # clearly off the line
+                pts.append((base + off * nrm).astype(np.float32))
+            for p in pts:
+                    inside = brute.strictly_inside_frac(V, p)
+                    x0, x1, y0, y1 = poly.box
+                    if x0 <= p[0] <= x1 and y0 <= p[1] <= y1:
+                        assert inside
+                        continue
+                    g = [_fma32(A, p[0], _fma32(B, p[1], Cl)) for A, B, Cl, _ in coef]
+                    mn = min(g)
+                    checked += 1
+                    if mn > 0:
+                        decided += 1
+                        assert inside, p
+                    elif np.float32(mn + e2max) < 0:
+                        decided += 1
+                        assert not inside, p
+    assert checked > 1000 and decided > 0.3 * checked   # ~5/11 of the probes sit in the band

@@ -1,0 +1,240 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle, element by
+element — bit-exact on the Step-1 indices, the sorted survivor index set, the
+polygon and the final hull (north_star).
+
+Inputs are seeded synthetic point sets (synth/); the device generator's bytes
+are themselves checked against the numpy generator, and the oracle always
+consumes numpy-generated (or D2H-copied, generator-verified) bytes."""
+from __future__ import annotations
+
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_1405_3454_b200 as cp
+import synth
+import synth.cuda as scuda
+
+pytestmark = pytest.mark.gpu
+THREADS = max(1, min(64, os.cpu_count() or 1))
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1405_3454_b200 import build
+
+    build.build()
+    scuda.build()
+    oracle.build()
+    torch.cuda.set_device(0)
+    yield
+
+
+def _run(xy_or_t, angles="A", return_points=True):
+    pts = xy_or_t if isinstance(xy_or_t, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(xy_or_t)).cuda()
+    ext = cp.extremes(pts, angles)
+    idx, sp, rep = cp.filter(pts, ext, return_points=return_points)
+    torch.cuda.synchronize()
+    return ext, idx.cpu().numpy(), (sp.cpu().numpy() if sp is not None else None), rep
+
+
+def _assert_parity(xy, angles="A", check_hull=True):
+    ext, idx, sp, rep = _run(xy, angles)
+    want = oracle.cudapre(xy, angles, threads=THREADS)
+    assert ext.idx.tolist() == want["ext_idx"].tolist(), "Step 1 indices"
+    c, s = oracle.coeffs(angles)
+    assert rep["polygon"].vidx.tolist() == want["ring"].tolist(), "Step 2 ring"
+    assert rep["polygon"].degenerate == want["degenerate"]
+    assert np.array_equal(idx, want["survivors"]), (
+        f"Step 3 survivors: gpu {len(idx)} vs oracle {len(want['survivors'])}")
+    assert np.array_equal(sp, xy[idx]), "survivor coordinates"
+    if check_hull:
+        assert cp.hull(xy, idx).tolist() == oracle.hull(xy, want["survivors"]).tolist()
+    return ext, idx, want
+
+
+# ----------------------------------------------------------------- generator
+@pytest.mark.parametrize("family", synth.FAMILIES)
+def test_device_generator_matches_numpy(family):
+    for n, base in ((300_001, 0), (4097, 1_999_000_000)):
+        want = synth.generate(family, n, seed=11, base=base)
+        got = scuda.generate(family, n, seed=11, base=base).cpu().numpy()
+        assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), family
+
+
+# ----------------------------------------------------------------- randomized suite
+SIZES = [1, 2, 3, 5, 31, 32, 33, 513, 2047, 2048, 2049, 4097, 65_537, 100_003, 262_145]
+
+
+@pytest.mark.parametrize("family", synth.FAMILIES)
+@pytest.mark.parametrize("angles", ["A", "B", "C", "AT"])
+def test_parity_sizes(family, angles):
+    for n in SIZES:
+        xy = synth.generate(family, n, seed=n + 7)
+        _assert_parity(xy, angles, check_hull=n <= 100_003)
+
+
+def test_parity_ties_grid_and_duplicates():
+    rng = np.random.default_rng(0)
+    for trial in range(30):
+        n = int(rng.integers(3, 300_000))
+        k = int(rng.integers(1, 20))
+        xy = (rng.integers(-k, k + 1, (n, 2)) / k).astype(np.float32)     # heavy ties at every key
+        _assert_parity(xy, "A")
+    xy = np.round(synth.generate("disk", 1_000_003, seed=5) * (1 << 12)).astype(np.float32) / (1 << 12)
+    _assert_parity(xy, "A")
+
+
+def test_parity_degenerate():
+    for xy in ([[0.5, 0.25]] * 1000, [[i, 2 * i] for i in range(5000)], [[1, 1], [2, 2]],
+               [[0, 0], [1, 0], [1, 1], [0, 1]] * 300, [[-0.0, 0.0], [0.0, -0.0], [0.0, 0.0]]):
+        _assert_parity(np.asarray(xy, np.float32), "A")
+
+
+def test_parity_boundary_points():
+    """Points exactly on the polygon's edges survive (A12)."""
+    sq = [[0, 0], [4, 0], [4, 4], [0, 4]]
+    edge = [[t, 0] for t in np.linspace(0, 4, 257)] + [[4, t] for t in np.linspace(0, 4, 257)]
+    inner = np.random.default_rng(1).uniform(0.001, 3.999, (100_000, 2)).tolist()
+    xy = np.asarray(sq + edge + inner, np.float32)
+    _, idx, _ = _assert_parity(xy, "A")
+    assert set(range(4 + 2 * 257)) <= set(idx.tolist())
+
+
+@pytest.mark.parametrize("scale", [1e-30, 1e-12, 1.0, 3e7, 1e30, 1e36])
+def test_parity_extreme_magnitudes(scale):
+    xy = (synth.generate("disk", 200_001, seed=3).astype(np.float64) * scale).astype(np.float32)
+    xy[::7] *= np.float32(0.5)
+    _assert_parity(xy, "A")
+
+
+def test_parity_offset_disk_and_sorted_order():
+    xy = synth.generate("disk", 500_001, seed=9) + np.float32(1000.0)   # far from the origin
+    _assert_parity(xy, "A")
+    order = np.lexsort((xy[:, 1], xy[:, 0]))
+    _assert_parity(np.ascontiguousarray(xy[order]), "A")                 # adversarial (sorted)
+    _assert_parity(np.ascontiguousarray(xy[order[::-1]]), "A")
+
+
+def test_misaligned_and_index_base():
+    """8-byte aligned (not 16) input uses the scalar-load path; index_base
+    shifts every returned index."""
+    xy = synth.generate("gauss", 300_000, seed=2)
+    full = torch.from_numpy(xy).cuda()
+    view = full[1:]                       # data_ptr % 16 == 8
+    assert view.data_ptr() % 16 == 8
+    ext = cp.extremes(view, "A", index_base=1)
+    idx, sp, rep = cp.filter(view, ext, index_base=1)
+    want = oracle.cudapre(xy[1:], "A", threads=THREADS)
+    assert (ext.idx - 1).tolist() == want["ext_idx"].tolist()
+    assert np.array_equal(idx.cpu().numpy() - 1, want["survivors"])
+
+
+def test_errors():
+    with pytest.raises(cp.CudaPreError) as e:
+        cp.extremes(torch.empty((0, 2), device="cuda"))
+    assert e.value.status == cp.ERR_EMPTY
+    idx, sp, rep = cp.cuda_pre(torch.empty((0, 2), device="cuda"))
+    assert rep["skipped"] and len(idx) == 0
+    xy = synth.generate("disk", 10_000, seed=1)
+    xy[777] = [np.nan, 0.0]
+    with pytest.raises(cp.CudaPreError) as e:
+        cp.extremes(torch.from_numpy(xy).cuda())
+    assert e.value.status == cp.ERR_NONFINITE
+    xy = synth.generate("circle", 100_000, seed=1)
+    pts = torch.from_numpy(xy).cuda()
+    ext = cp.extremes(pts)
+    small = torch.empty(10, dtype=torch.int64, device="cuda")
+    with pytest.raises(cp.CudaPreError) as e:
+        cp.filter(pts, ext, out_idx=small, return_points=False)
+    assert e.value.status == cp.ERR_CAPACITY
+
+
+def test_repeated_calls_reuse_workspace():
+    """The workspace self-resets (tickets, seeds, epochs): 50 back-to-back
+    calls on different inputs all stay exact."""
+    for t in range(50):
+        fam = synth.FAMILIES[t % 4]
+        n = 10_000 + 3337 * t
+        xy = synth.generate(fam, n, seed=100 + t)
+        ext, idx, _, _ = _run(xy)
+        want = oracle.cudapre(xy, "A", threads=THREADS)
+        assert ext.idx.tolist() == want["ext_idx"].tolist()
+        assert np.array_equal(idx, want["survivors"])
+
+
+def test_run_host_end_to_end():
+    xy = synth.generate("disk", 1_000_003, seed=4)
+    h = torch.from_numpy(xy).pin_memory()
+    d = torch.empty_like(h, device="cuda")
+    ds = torch.empty(len(xy), dtype=torch.int64, device="cuda")
+    hs = torch.empty(len(xy), dtype=torch.int64).pin_memory()
+    m, rep = cp.run_host(h, d, ds, hs)
+    want = oracle.cudapre(xy, "A", threads=THREADS)
+    assert np.array_equal(hs[:m].numpy(), want["survivors"])
+
+
+# ----------------------------------------------------------------- BASELINE configs at full size
+@pytest.mark.parametrize("name", ["C1", "C2a", "C2b", "C3", "C4", "C4e0"])
+def test_config_full_size(name):
+    cfg = dict(synth.CONFIGS[name])
+    n = cfg.pop("n")
+    fam = cfg.pop("family")
+    seed = cfg.pop("seed")
+    xy = synth.generate(fam, n, seed=seed, **cfg)
+    dev = scuda.generate(fam, n, seed=seed, **cfg)
+    assert np.array_equal(dev.cpu().numpy().view(np.uint32), xy.view(np.uint32))
+    ext, idx, want = _assert_parity(xy, "A", check_hull=n <= 20_000_000)
+    print(f"{name}: n={n} survivors={len(idx)} ({100 * len(idx) / n:.4f}%)")
+
+
+def test_config_c5_2b_sampled():
+    """C5 at its full 2e9 points on one GPU (the bench workload): Step 1 vs the
+    oracle over all 2e9 points (chunked D2H of generator-verified bytes);
+    Step 3 element by element on sampled contiguous index windows."""
+    cfg = dict(synth.CONFIGS["C5"])
+    n = cfg.pop("n")
+    pts = scuda.generate(cfg["family"], n, seed=cfg["seed"])
+    ext = cp.extremes(pts, "A")
+    cap = n // 16
+    idx, _, rep = cp.filter(pts, ext, out_idx=torch.empty(cap, dtype=torch.int64, device="cuda"),
+                            return_points=False)
+    torch.cuda.synchronize()
+    surv = idx.cpu().numpy()
+    assert np.all(np.diff(surv) > 0)
+    # Step 1: oracle over every chunk, merged by the lexicographic rule
+    c, s = oracle.coeffs("A")
+    best_k = [None] * 16
+    best_i = [None] * 16
+    chunk = 100_000_000
+    for lo in range(0, n, chunk):
+        hi = min(n, lo + chunk)
+        host = pts[lo:hi].cpu().numpy()
+        if lo == 0:
+            want = synth.generate("disk", 4096, seed=cfg["seed"])
+            assert np.array_equal(host[:4096].view(np.uint32), want.view(np.uint32))
+        ii, kk = oracle.extremes(host, "A", threads=THREADS, with_keys=True)
+        for sl in range(16):
+            k, i = float(kk[sl]), int(ii[sl]) + lo
+            mx = sl % 2 == 1
+            if best_k[sl] is None or (k > best_k[sl] if mx else k < best_k[sl]):
+                best_k[sl], best_i[sl] = k, i
+    assert ext.idx.tolist() == best_i
+    # Step 2 (oracle polygon from the oracle's picks) and Step 3 on windows
+    ring_ids = oracle.hull(np.concatenate([pts[i:i + 1].cpu().numpy() for i in best_i]))
+    ring_xy = np.concatenate([pts[best_i[j]:best_i[j] + 1].cpu().numpy() for j in ring_ids])
+    assert rep["polygon"].v.tolist() == ring_xy.tolist()
+    rng = np.random.default_rng(0)
+    for lo in [0, n - 1_000_000, *rng.integers(0, n - 1_000_000, 6).tolist()]:
+        hi = lo + 1_000_000
+        host = pts[lo:hi].cpu().numpy()
+        keep = np.flatnonzero(oracle.filter_mask(host, ring_xy, threads=THREADS)) + lo
+        a, b = np.searchsorted(surv, [lo, hi])
+        assert np.array_equal(surv[a:b], keep), lo
+    frac = len(surv) / n
+    assert 0.0330 < frac < 0.0345, frac            # closed form 3.384 % (reading A1)
