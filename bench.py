@@ -199,8 +199,11 @@ def main():
     out_pts = torch.empty((cap, 2), dtype=torch.float32, device="cuda")
     torch.cuda.synchronize()
 
+    exact_pts = [0]
+
     def step(rep1):
         ext = cp.extremes(pts, args.angles, index_base=base, group=group, ws=ws, report=rep1)
+        exact_pts[0] = ext.raw.exact_points
         idx, sp, rep2 = cp.filter(pts, ext, index_base=base, ws=ws, out_idx=out_idx, out_pts=out_pts)
         return idx.shape[0], rep2
 
@@ -336,6 +339,7 @@ def main():
             "remaining_pct": round(100 * surv_total / n_total, 4),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": clocks.result(),
+            "k1_exact_path_points_per_step": int(exact_pts[0]),
         }
         print(json.dumps(line), flush=True)
     if group is not None:

@@ -77,6 +77,8 @@ typedef struct {
     cudapre_pt pt[CUDAPRE_MAX_SLOTS];    /* coordinates of each pick */
     double c[CUDAPRE_MAX_ANGLES];        /* cos of each angle used (correctly rounded, A5) */
     double s[CUDAPRE_MAX_ANGLES];        /* sin of each angle used */
+    int64_t exact_points;                /* diagnostic: points that took the exact binary64 path
+                                          * (passed the float screen), summed over merged parts */
 } cudapre_extremes_t;
 
 /* Step 2 result: the filter polygon and the parameters the Step-3 kernel
@@ -91,6 +93,8 @@ typedef struct {
     int64_t vidx[CUDAPRE_MAX_SLOTS];     /* global index of each ring vertex */
     cudapre_pt v[CUDAPRE_MAX_SLOTS];     /* ring vertex coordinates */
     float box[4];                        /* inner box x0,x1,y0,y1 strictly inside the ring (x0>x1: none) */
+    float circle[4];                     /* inner disk: centre x, y; r2 with RN32((x-cx)^2+(y-cy)^2)
+                                          * < r2 => strictly inside (r2 < 0: none); pad */
     float err_max;                       /* largest per-edge float error bound E_j */
     int32_t pad;
     /* Step-3 kernel line tests, edge j = v[j] -> v[j+1]:  g_j(p) = fma(A_j, p.x,

@@ -50,14 +50,15 @@ class ExtremesT(ctypes.Structure):
     _fields_ = [("nang", ctypes.c_int32), ("nonfinite", ctypes.c_int32), ("n", ctypes.c_int64),
                 ("idx", ctypes.c_int64 * MAX_SLOTS), ("key", ctypes.c_double * MAX_SLOTS),
                 ("pt", Pt * MAX_SLOTS), ("c", ctypes.c_double * MAX_ANGLES),
-                ("s", ctypes.c_double * MAX_ANGLES)]
+                ("s", ctypes.c_double * MAX_ANGLES), ("exact_points", ctypes.c_int64)]
 
 
 class PolygonT(ctypes.Structure):
     _fields_ = [("nv", ctypes.c_int32), ("degenerate", ctypes.c_int32),
                 ("n_distinct", ctypes.c_int32), ("exact_only", ctypes.c_int32),
                 ("vidx", ctypes.c_int64 * MAX_SLOTS), ("v", Pt * MAX_SLOTS),
-                ("box", ctypes.c_float * 4), ("err_max", ctypes.c_float), ("pad", ctypes.c_int32),
+                ("box", ctypes.c_float * 4), ("circle", ctypes.c_float * 4),
+                ("err_max", ctypes.c_float), ("pad", ctypes.c_int32),
                 ("A", ctypes.c_float * MAX_SLOTS), ("B", ctypes.c_float * MAX_SLOTS),
                 ("C", ctypes.c_float * MAX_SLOTS), ("E", ctypes.c_float * MAX_SLOTS)]
 
@@ -227,6 +228,10 @@ class Polygon:
     @property
     def box(self):
         return tuple(self.raw.box)
+
+    @property
+    def circle(self):
+        return tuple(self.raw.circle[:3])
 
 
 def _angle_arrays(angle_set):

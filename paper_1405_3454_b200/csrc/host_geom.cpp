@@ -103,12 +103,14 @@ void merge_extremes(const cudapre_extremes_t* parts, int count, cudapre_extremes
     cudapre_extremes_t r = parts[0];
     r.n = 0;
     r.nonfinite = 0;
+    r.exact_points = 0;
     const int slots = 4 * r.nang;
     for (int s = 0; s < slots; ++s) r.idx[s] = -1;
     for (int p = 0; p < count; ++p) {
         const cudapre_extremes_t& q = parts[p];
         r.n += q.n;
         r.nonfinite |= q.nonfinite;
+        r.exact_points += q.exact_points;
         for (int s = 0; s < slots; ++s) {
             if (q.idx[s] < 0) continue;
             const bool is_max = (s & 1) != 0;
@@ -160,11 +162,14 @@ void build_polygon(const cudapre_extremes_t& ext, cudapre_polygon_t* poly, K2Par
     poly->box[1] = 0.0f;   // empty box
     poly->box[2] = 1.0f;
     poly->box[3] = 0.0f;
+    poly->circle[2] = -1.0f;
     if (kp) {
         kp->nv = nv;
         kp->mode = poly->degenerate ? 1 : 0;
         kp->bx0 = 1.0f; kp->bx1 = 0.0f; kp->by0 = 1.0f; kp->by1 = 0.0f;
         kp->e2max = 0.0f;
+        kp->ox = kp->oy = 0.0f;
+        kp->r2 = -1.0f;
         for (int j = 0; j <= nv && j <= CUDAPRE_MAX_SLOTS; ++j) {
             kp->vx[j] = poly->v[j % (nv ? nv : 1)].x;
             kp->vy[j] = poly->v[j % (nv ? nv : 1)].y;
@@ -208,6 +213,12 @@ void build_polygon(const cudapre_extremes_t& ext, cudapre_polygon_t* poly, K2Par
             kp->C[j] = Cl;
         }
     }
+    if (kp)   // padding edges for the kernel's fixed-length loop: g = +inf, never the minimum
+        for (int j = nv; j < CUDAPRE_MAX_SLOTS; ++j) {
+            kp->A[j] = 0.0f;
+            kp->B[j] = 0.0f;
+            kp->C[j] = INFINITY;
+        }
     if (!(emax < 1e37f)) exact_only = true;
     poly->err_max = emax;
     poly->exact_only = exact_only;
@@ -251,7 +262,49 @@ void build_polygon(const cudapre_extremes_t& ext, cudapre_polygon_t* poly, K2Par
         }
     }
     if (have) std::memcpy(poly->box, best, sizeof(best));
+
+    // ---- inner disk: centre O (box centre, else vertex mean,
+    //      rounded to float and checked strictly inside exactly), radius^2 =
+    //      (1 - 2^-16) * (a rigorous LOWER bound of min_j dist(O, edge line j))^2.
+    //      Kernel test RN32(fma(dx, dx, RN32(dy*dy))) < r2 with dx = RN32(x - ox):
+    //      the float value is >= true d^2 (1 - 4u), so acceptance implies true
+    //      d^2 < R^2 (1 - 2^-16) / (1 - 4u) < R^2.  Disabled outside [2^-100, 2^100].
+    poly->circle[0] = 0.0f;
+    poly->circle[1] = 0.0f;
+    poly->circle[2] = -1.0f;
+    {
+        const float cx = have ? 0.5f * (best[0] + best[1]) : (float)ox;
+        const float cy = have ? 0.5f * (best[2] + best[3]) : (float)oy;
+        if (std::isfinite(cx) && std::isfinite(cy) && strictly_inside_ring(poly->v, nv, cx, cy)) {
+            double rmin = INFINITY;
+            bool ok = true;
+            for (int j = 0; j < nv && ok; ++j) {
+                const double ax = poly->v[j].x, ay = poly->v[j].y;
+                const double bx = poly->v[(j + 1) % nv].x, by = poly->v[(j + 1) % nv].y;
+                const double ex = bx - ax, ey = by - ay, px = cx - ax, py = cy - ay;
+                const double t1 = ex * py, t2 = ey * px;
+                const double num = t1 - t2;
+                // each of ex, ey, px, py, t1, t2, num carries <= 1 rounding (2^-53 rel.)
+                const double err = (std::fabs(t1) + std::fabs(t2)) * 0x1p-49;
+                const double len = std::sqrt(ex * ex + ey * ey) * (1.0 + 0x1p-48);
+                if (!(num - err > 0.0) || !(len > 0.0) || !std::isfinite(len)) {
+                    ok = false;
+                    break;
+                }
+                rmin = std::min(rmin, (num - err) / len * (1.0 - 0x1p-50));
+            }
+            const double r2 = rmin * rmin * (1.0 - 0x1p-16);
+            if (ok && r2 >= 0x1p-100 && r2 <= 0x1p100) {
+                poly->circle[0] = cx;
+                poly->circle[1] = cy;
+                poly->circle[2] = f_down(r2);
+            }
+        }
+    }
     if (kp) {
+        kp->ox = poly->circle[0];
+        kp->oy = poly->circle[1];
+        kp->r2 = poly->circle[2];
         kp->mode = exact_only ? 2 : 0;
         kp->e2max = 2.0f * emax;
         kp->bx0 = poly->box[0];

@@ -13,9 +13,11 @@ constexpr int kK1Threads = 256;        // K1 block
 constexpr int kK1Unroll = 4;           // float4 (= 2 points) per thread per iteration
 constexpr int kSeedThreads = 128;      // seed block; one chunk = 128 float4 = 256 points
 constexpr int kK2Threads = 256;        // K2 block
-constexpr int kK2Items = 4;            // float4 per thread per tile
-constexpr int kK2TilePairs = kK2Threads * kK2Items;   // 1024 pairs
-constexpr int kK2TilePts = 2 * kK2TilePairs;          // 2048 points per tile
+constexpr int kK2Items = 4;            // float4 per thread per sub-tile
+constexpr int kK2SubPairs = kK2Threads * kK2Items;    // 1024 pairs = 2048 points per sub-tile
+constexpr int kK2Sub = 8;              // sub-tiles per super-tile (one look-back each)
+constexpr int kK2TilePairs = kK2Sub * kK2SubPairs;    // 8192 pairs
+constexpr int kK2TilePts = 2 * kK2TilePairs;          // 16384 points = 128 KiB per super-tile
 constexpr int kMaxK1Blocks = 148 * 16;
 
 // ---------------------------------------------------------------- workspace
@@ -26,10 +28,11 @@ constexpr int kMaxK1Blocks = 148 * 16;
 struct alignas(16) WsHeader {
     unsigned int k1_ticket;      // K1 blocks finished (last-block finalize)
     unsigned int k1_nonfinite;   // set by K1's exact path on NaN/Inf input
+    unsigned int k1_exact;       // points that took K1's exact path (diagnostic)
     unsigned int k2_ticket;      // K2 dynamic tile counter
     unsigned int k2_done;        // K2 blocks finished
     unsigned int epoch;          // K2 tile-status epoch (never 0 after the first call)
-    unsigned int pad0[3];
+    unsigned int pad0[2];
     unsigned long long count;    // K2 survivors (written by the last tile)
     unsigned long long pad1;
     unsigned int seed[CUDAPRE_MAX_SLOTS];   // seed thresholds, order-preserving encoding, 0 = none
@@ -78,6 +81,7 @@ struct K2Params {
     unsigned int num_tiles;
     int mode;                 // 0 = filter, 1 = keep everything (degenerate), 2 = exact only
     float bx0, bx1, by0, by1; // inner box (closed), strictly inside the ring
+    float ox, oy, r2;         // inner disk: RN(fma(dx,dx,RN(dy*dy))) < r2 => strictly inside (r2 < 0: off)
     float e2max;              // 2 * max_j E_j
     float A[CUDAPRE_MAX_SLOTS], B[CUDAPRE_MAX_SLOTS], C[CUDAPRE_MAX_SLOTS];   // C already lowered by E_j
     float vx[CUDAPRE_MAX_SLOTS + 1], vy[CUDAPRE_MAX_SLOTS + 1];               // ring, v[nv] = v[0]

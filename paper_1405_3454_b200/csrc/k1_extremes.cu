@@ -176,14 +176,19 @@ __device__ __forceinline__ bool screen2(const float4 v, const float (&T)[4 * NAN
 template <int NANG>
 __device__ __forceinline__ void exact_staged(WarpState<NANG>& st, const float (&T)[4 * NANG],
                                              const K1Params& p) {
+    unsigned hits = 0;
 #pragma unroll 1
     for (int j = 0; j < 2 * kK1Unroll; ++j) {
         const float4 v = st.stage[j >> 1];
         const unsigned i = 2u * st.stage_q[j >> 1] + (unsigned)(j & 1);
         const float x = (j & 1) ? v.z : v.x;
         const float y = (j & 1) ? v.w : v.y;
-        if (i < p.n && screen1<NANG>(x, y, T, p)) exact_update<NANG>(st, x, y, i, p);
+        if (i < p.n && screen1<NANG>(x, y, T, p)) {
+            exact_update<NANG>(st, x, y, i, p);
+            ++hits;
+        }
     }
+    atomicAdd(&p.ws->k1_exact, hits);
 }
 
 // thresholds <- the warp state (rounded to the safe side) and the seed
@@ -269,7 +274,7 @@ __global__ void __launch_bounds__(kSeedThreads) k1_seed(const K1Params p) {
 
 // ---------------------------------------------------------------- main kernel
 template <int NANG, bool VEC>
-__global__ void __launch_bounds__(kK1Threads) k1_extremes(const K1Params p) {
+__global__ void __launch_bounds__(kK1Threads, 2) k1_extremes(const K1Params p) {
     constexpr int NS = 4 * NANG;
     constexpr int kWarps = kK1Threads / 32;
     __shared__ WarpState<NANG> sst[kWarps];
@@ -298,37 +303,55 @@ __global__ void __launch_bounds__(kK1Threads) k1_extremes(const K1Params p) {
     unsigned q0 = blockIdx.x * (kK1Threads * kK1Unroll) + threadIdx.x;
     // full iterations: every pair valid (2q+1 < n  <=>  q < n/2)
     const unsigned full_pairs = p.n / 2u;
-    // loop conditions use the warp's lane-0 pair so all lanes agree (warp votes below)
-    for (; (q0 - lane) + 31u + (kK1Unroll - 1) * kK1Threads < full_pairs; q0 += stride) {
-        float4 v[kK1Unroll];
+    // Full iterations (every pair valid), software-pipelined: the next
+    // iteration's 4 x 128-bit loads are issued before this one is screened.
+    // Loop conditions use the warp's lane-0 pair so all lanes agree.
+    auto full = [&](unsigned q) {
+        return (q - lane) + 31u + (kK1Unroll - 1) * kK1Threads < full_pairs;
+    };
+    auto load_full = [&](float4 (&dst)[kK1Unroll], unsigned q) {
 #pragma unroll
         for (int u = 0; u < kK1Unroll; ++u) {
-            if (VEC)
-                v[u] = ld_stream(reinterpret_cast<const float4*>(p.pts) + q0 + u * kK1Threads);
-            else {
+            if (VEC) {
+                dst[u] = ld_stream(reinterpret_cast<const float4*>(p.pts) + q + u * kK1Threads);
+            } else {
                 bool a, b;
-                v[u] = load_pair<false>(p.pts, q0 + u * kK1Threads, p.n, a, b);
+                dst[u] = load_pair<false>(p.pts, q + u * kK1Threads, p.n, a, b);
             }
         }
-        bool cand = false;
+    };
+    if (full(q0)) {
+        float4 v[kK1Unroll];
+        load_full(v, q0);
+        while (true) {
+            const unsigned qn = q0 + stride;
+            const bool more = full(qn);
+            float4 vn[kK1Unroll];
+            if (more) load_full(vn, qn);
+            bool cand = false;
 #pragma unroll
-        for (int u = 0; u < kK1Unroll; ++u) cand |= screen2<NANG>(v[u], T, p);
-        if (__any_sync(kFull, cand)) {
-            unsigned mask = __ballot_sync(kFull, cand);
-            while (mask) {
-                const unsigned l = __ffs(mask) - 1;
-                mask &= mask - 1;
-                if (lane == l) {
+            for (int u = 0; u < kK1Unroll; ++u) cand |= screen2<NANG>(v[u], T, p);
+            if (__any_sync(kFull, cand)) {
+                unsigned mask = __ballot_sync(kFull, cand);
+                while (mask) {
+                    const unsigned l = __ffs(mask) - 1;
+                    mask &= mask - 1;
+                    if (lane == l) {
 #pragma unroll
-                    for (int u = 0; u < kK1Unroll; ++u) {
-                        st.stage[u] = v[u];
-                        st.stage_q[u] = q0 + u * kK1Threads;
+                        for (int u = 0; u < kK1Unroll; ++u) {
+                            st.stage[u] = v[u];
+                            st.stage_q[u] = q0 + u * kK1Threads;
+                        }
+                        exact_staged<NANG>(st, T, p);
                     }
-                    exact_staged<NANG>(st, T, p);
+                    __syncwarp();
                 }
-                __syncwarp();
+                refresh_thresholds<NANG>(T, st);
             }
-            refresh_thresholds<NANG>(T, st);
+            q0 = qn;
+            if (!more) break;
+#pragma unroll
+            for (int u = 0; u < kK1Unroll; ++u) v[u] = vn[u];
         }
     }
     // remainder (guarded)
@@ -446,6 +469,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_extremes(const K1Params p) {
                 outs[o]->nang = p.nang;
                 outs[o]->nonfinite = nf ? 1 : 0;
                 outs[o]->n = (long long)p.n;
+                outs[o]->exact_points = (long long)__ldcg(&p.ws->k1_exact);
             }
         }
         __syncwarp();
@@ -453,6 +477,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_extremes(const K1Params p) {
         if (threadIdx.x == 0) {
             p.ws->k1_ticket = 0u;
             p.ws->k1_nonfinite = 0u;
+            p.ws->k1_exact = 0u;
         }
     }
 }

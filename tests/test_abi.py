@@ -46,8 +46,8 @@ def test_exports_every_declared_symbol(L):
 
 def test_struct_sizes_match_header(L):
     # offsets derived from the C layout rules of include/cudapre.h
-    assert ctypes.sizeof(cp.ExtremesT) == 8 + 8 + 32 * 8 + 32 * 8 + 32 * 8 + 8 * 8 + 8 * 8
-    assert ctypes.sizeof(cp.PolygonT) == 16 + 32 * 8 + 32 * 8 + 16 + 8 + 4 * 32 * 4
+    assert ctypes.sizeof(cp.ExtremesT) == 8 + 8 + 32 * 8 + 32 * 8 + 32 * 8 + 8 * 8 + 8 * 8 + 8
+    assert ctypes.sizeof(cp.PolygonT) == 16 + 32 * 8 + 32 * 8 + 16 + 16 + 8 + 4 * 32 * 4
     assert ctypes.sizeof(cp.ReportT) == 48
 
 
@@ -80,7 +80,7 @@ def test_empty_and_bad_args_without_gpu(L):
                             np.zeros(8).ctypes.data_as(ctypes.c_void_p), None, 0, None, None,
                             None, None)
     assert st == cp.ERR_ARG
-    assert L.cudapre_workspace_bytes(10 ** 9) > 8 * (10 ** 9 // 2048)
+    assert L.cudapre_workspace_bytes(10 ** 9) > 8 * (10 ** 9 // 16384)   # one status word per super-tile
 
 
 # ------------------------------------------------------------ host-side pieces
@@ -237,3 +237,31 @@ def test_k2_float_decisions_are_conservative(L, oracle_lib):
                         decided += 1
                         assert not inside, p
     assert checked > 1000 and decided > 0.3 * checked   # ~5/11 of the probes sit in the band
+
+
+def test_k2_inner_disk_is_conservative(L, oracle_lib):
+    """every point the kernel's disk test accepts
+    (RN32(fma(dx, dx, RN32(dy*dy))) < r2, dx = RN32(x - ox)) is strictly inside
+    the ring by the exact predicate — probed on and around the disk boundary."""
+    for family, seed in (("disk", 13), ("square", 2), ("gauss", 4), ("circle", 5)):
+        xy = synth.generate(family, 50_000, seed=seed)
+        ext = _ext_from_oracle(oracle_lib, xy)
+        poly = cp.polygon(cp.Extremes(ext))
+        ox, oy, r2 = poly.circle
+        if r2 < 0:
+            assert family == "circle" or poly.degenerate
+            continue
+        V = poly.v
+        r = float(np.sqrt(np.float64(r2)))
+        rng = np.random.default_rng(seed)
+        accepted = 0
+        for th in rng.uniform(0, 2 * np.pi, 400):
+            for f in (0.999, 0.99999, 1.0, 1.000001, 1.00001):
+                p = np.array([ox + f * r * np.cos(th), oy + f * r * np.sin(th)], np.float32)
+                dx = np.float32(p[0] - np.float32(ox))
+                dy = np.float32(p[1] - np.float32(oy))
+                d2 = _fma32(dx, dx, np.float32(dy * dy))
+                if d2 < np.float32(r2):
+                    accepted += 1
+                    assert brute.strictly_inside_frac(V, p), (family, p)
+        assert accepted > 400
