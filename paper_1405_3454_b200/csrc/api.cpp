@@ -5,6 +5,7 @@
 #include <chrono>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -215,6 +216,12 @@ cudapre_status cudapre_extremes(const cudapre_pt* d_pts, int64_t n_local, int64_
         p.seed_chunks = (unsigned)(ch < 16 ? 16 : (ch > 4096 ? 4096 : ch));
     }
     const int vec16 = (((uintptr_t)d_pts & 15u) == 0);
+    {
+        // K1 input path: register double-buffered 128-bit loads (default,
+        // measured faster on C5) or the cp.async.bulk ring (CUDAPRE_K1_TMA=1).
+        const char* e = getenv("CUDAPRE_K1_TMA");
+        p.use_tma = e ? atoi(e) : 0;
+    }
     cudaEvent_t* ev = nullptr;
     if (h_rep) {
         st = events(&ev);

@@ -12,6 +12,8 @@ namespace cudapre {
 constexpr int kK1Threads = 256;        // K1 block
 constexpr int kK1Unroll = 4;           // float4 (= 2 points) per thread per iteration
 constexpr int kSeedThreads = 128;      // seed block; one chunk = 128 float4 = 256 points
+constexpr int kK1StagePairs = kK1Threads * kK1Unroll;   // 1024 pairs = 16 KiB per TMA stage
+constexpr int kK1Stages = 4;           // TMA ring depth per block
 constexpr int kK2Threads = 256;        // K2 block
 constexpr int kK2Items = 4;            // float4 per thread per sub-tile
 constexpr int kK2SubPairs = kK2Threads * kK2Items;    // 1024 pairs = 2048 points per sub-tile
@@ -66,6 +68,7 @@ struct K1Params {
     K1Partial* partials;
     cudapre_extremes_t* d_out;   // nullable extra copy of the result
     unsigned int seed_chunks;    // number of 256-point sample chunks (0 = no seed)
+    int use_tma;                 // 1: stream through the cp.async.bulk ring (16-B aligned input)
 };
 
 struct K2Params {

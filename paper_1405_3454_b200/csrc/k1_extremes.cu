@@ -52,6 +52,36 @@ __device__ __forceinline__ float4 ld_stream(const float4* p) {
     return r;
 }
 
+// ---- TMA bulk copy + mbarrier (sm_90+/sm_100a): global -> shared, no registers
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                         unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+    asm volatile(
+        "{\n .reg .pred P1;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        " @!P1 bra WAIT_%=;\n }" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
 // Load the point pair q = (2q, 2q+1); v1 false if 2q+1 >= n.  VEC: 16-B aligned base.
 template <bool VEC>
 __device__ __forceinline__ float4 load_pair(const float* pts, unsigned q, unsigned n, bool& v0,
@@ -273,7 +303,7 @@ __global__ void __launch_bounds__(kSeedThreads) k1_seed(const K1Params p) {
 }
 
 // ---------------------------------------------------------------- main kernel
-template <int NANG, bool VEC>
+template <int NANG, bool VEC, bool TMA>
 __global__ void __launch_bounds__(kK1Threads, 2) k1_extremes(const K1Params p) {
     constexpr int NS = 4 * NANG;
     constexpr int kWarps = kK1Threads / 32;
@@ -320,7 +350,67 @@ __global__ void __launch_bounds__(kK1Threads, 2) k1_extremes(const K1Params p) {
             }
         }
     };
-    if (full(q0)) {
+    // screen 4 pairs; the rare candidates take the exact path (cold)
+    auto process = [&](const float4 (&v)[kK1Unroll], unsigned qb) {
+        bool cand = false;
+#pragma unroll
+        for (int u = 0; u < kK1Unroll; ++u) cand |= screen2<NANG>(v[u], T, p);
+        if (__any_sync(kFull, cand)) {
+            unsigned mask = __ballot_sync(kFull, cand);
+            while (mask) {
+                const unsigned l = __ffs(mask) - 1;
+                mask &= mask - 1;
+                if (lane == l) {
+#pragma unroll
+                    for (int u = 0; u < kK1Unroll; ++u) {
+                        st.stage[u] = v[u];
+                        st.stage_q[u] = qb + u * kK1Threads;
+                    }
+                    exact_staged<NANG>(st, T, p);
+                }
+                __syncwarp();
+            }
+            refresh_thresholds<NANG>(T, st);
+        }
+    };
+    if constexpr (TMA) {
+        // Chunks of kK1StagePairs pairs (16 KiB) stream through a kK1Stages-deep
+        // shared-memory ring filled by cp.async.bulk (TMA) and completed on
+        // mbarriers: deep memory-level parallelism without holding loads in
+        // registers.  Chunk c goes to block c % gridDim.x.
+        extern __shared__ __align__(128) float4 ring[];
+        __shared__ unsigned long long fullb[kK1Stages];
+        const unsigned nchunks = full_pairs / kK1StagePairs;
+        const unsigned mine =
+            blockIdx.x < nchunks ? (nchunks - blockIdx.x + gridDim.x - 1) / gridDim.x : 0u;
+        const float4* src = reinterpret_cast<const float4*>(p.pts);
+        auto issue = [&](unsigned i) {
+            const unsigned sidx = i % kK1Stages;
+            const unsigned chunk = blockIdx.x + i * gridDim.x;
+            mbar_expect_tx(&fullb[sidx], kK1StagePairs * 16u);
+            bulk_g2s(&ring[sidx * kK1StagePairs], src + (size_t)chunk * kK1StagePairs, kK1StagePairs * 16u,
+                     &fullb[sidx]);
+        };
+        if (threadIdx.x == 0) {
+            for (int k = 0; k < kK1Stages; ++k) mbar_init(&fullb[k], 1u);
+            mbar_fence_init();
+            for (unsigned i = 0; i < (unsigned)kK1Stages && i < mine; ++i) issue(i);
+        }
+        __syncthreads();
+        for (unsigned i = 0; i < mine; ++i) {
+            const unsigned sidx = i % kK1Stages;
+            mbar_wait(&fullb[sidx], (i / kK1Stages) & 1u);
+            float4 v[kK1Unroll];
+#pragma unroll
+            for (int u = 0; u < kK1Unroll; ++u) v[u] = ring[sidx * kK1StagePairs + u * kK1Threads + threadIdx.x];
+            process(v, (blockIdx.x + i * gridDim.x) * kK1StagePairs + threadIdx.x);
+            __syncthreads();   // every warp is done with this stage: refill it
+            if (threadIdx.x == 0 && i + kK1Stages < mine) issue(i + kK1Stages);
+        }
+        q0 = nchunks * kK1StagePairs + blockIdx.x * (kK1Threads * kK1Unroll) + threadIdx.x;
+    } else if (full(q0)) {
+        // registers: the next iteration's 4 x 128-bit loads are issued before
+        // this one is screened
         float4 v[kK1Unroll];
         load_full(v, q0);
         while (true) {
@@ -328,26 +418,7 @@ __global__ void __launch_bounds__(kK1Threads, 2) k1_extremes(const K1Params p) {
             const bool more = full(qn);
             float4 vn[kK1Unroll];
             if (more) load_full(vn, qn);
-            bool cand = false;
-#pragma unroll
-            for (int u = 0; u < kK1Unroll; ++u) cand |= screen2<NANG>(v[u], T, p);
-            if (__any_sync(kFull, cand)) {
-                unsigned mask = __ballot_sync(kFull, cand);
-                while (mask) {
-                    const unsigned l = __ffs(mask) - 1;
-                    mask &= mask - 1;
-                    if (lane == l) {
-#pragma unroll
-                        for (int u = 0; u < kK1Unroll; ++u) {
-                            st.stage[u] = v[u];
-                            st.stage_q[u] = q0 + u * kK1Threads;
-                        }
-                        exact_staged<NANG>(st, T, p);
-                    }
-                    __syncwarp();
-                }
-                refresh_thresholds<NANG>(T, st);
-            }
+            process(v, q0);
             q0 = qn;
             if (!more) break;
 #pragma unroll
@@ -482,12 +553,15 @@ __global__ void __launch_bounds__(kK1Threads, 2) k1_extremes(const K1Params p) {
     }
 }
 
-template <int NANG, bool VEC>
+template <int NANG, bool VEC, bool TMA>
 cudaError_t launch_t(const K1Params& p, cudaStream_t s, int* launches) {
     static int k1_blocks = 0, seed_blocks = 0;
+    const int smem = TMA ? kK1Stages * kK1StagePairs * 16 : 0;
     if (!k1_blocks) {
+        if (TMA)
+            cudaFuncSetAttribute(k1_extremes<NANG, VEC, TMA>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1_extremes<NANG, VEC>, kK1Threads, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1_extremes<NANG, VEC, TMA>, kK1Threads, smem);
         const int sms = device_sm_count();
         k1_blocks = per_sm * sms;
         if (k1_blocks > kMaxK1Blocks) k1_blocks = kMaxK1Blocks;
@@ -503,14 +577,18 @@ cudaError_t launch_t(const K1Params& p, cudaStream_t s, int* launches) {
         k1_seed<NANG, VEC><<<sb, kSeedThreads, 0, s>>>(p);
         ++*launches;
     }
-    k1_extremes<NANG, VEC><<<blocks, kK1Threads, 0, s>>>(p);
+    k1_extremes<NANG, VEC, TMA><<<blocks, kK1Threads, smem, s>>>(p);
     ++*launches;
     return cudaGetLastError();
 }
 
 template <int NANG>
 cudaError_t launch_n(const K1Params& p, int vec16, cudaStream_t s, int* launches) {
-    return vec16 ? launch_t<NANG, true>(p, s, launches) : launch_t<NANG, false>(p, s, launches);
+    // 16-B aligned input streams through the TMA ring; 8-B aligned input uses
+    // register loads (cp.async.bulk needs 16-B aligned sources).
+    if (vec16) return p.use_tma ? launch_t<NANG, true, true>(p, s, launches)
+                                : launch_t<NANG, true, false>(p, s, launches);
+    return launch_t<NANG, false, false>(p, s, launches);
 }
 
 }  // namespace

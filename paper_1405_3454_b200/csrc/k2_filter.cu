@@ -38,7 +38,6 @@ constexpr unsigned kFull = 0xffffffffu;
 constexpr unsigned kFlagA = 1u;   // tile aggregate available
 constexpr unsigned kFlagP = 2u;   // inclusive prefix available
 constexpr unsigned kEpochMask = 0x3fffffffu;
-constexpr unsigned kStash = 256;   // per-warp survivor coordinates kept in smem per super-tile
 
 __device__ __forceinline__ float4 ld_stream(const float4* p) {
     float4 r;
@@ -105,32 +104,33 @@ __device__ __forceinline__ bool queue_keep(const K2Params& p, float x, float y) 
     return !exact_inside(p, x, y);
 }
 
-// Decoupled look-back by warp 0, 256 predecessors per round (8 per lane,
-// loads in flight together): returns the exclusive prefix of super-tile `tile`.
-// At HBM speed ~50 super-tiles complete per microsecond, so the look-back
-// window must be wide or the chain of inclusive prefixes serialises.
-__device__ __forceinline__ unsigned long long lookback(const K2Params& p, unsigned tile,
-                                                       unsigned total, unsigned epoch,
-                                                       unsigned lane) {
+// ---------------------------------------------------------------- look-back
+// Status word of super-tile t: [epoch:30 | flag:2 | count:32].  publish_*
+// write it with one relaxed 64-bit store; resolve() (warp 0) walks back 256
+// predecessors per round (8 loads in flight per lane) summing aggregates up to
+// the nearest inclusive prefix.  Because resolve(t) runs one tile-time after
+// t's own aggregate was published (deferred, see the kernel), every
+// predecessor's aggregate is normally already there: no spinning.
+__device__ __forceinline__ void publish(const K2Params& p, unsigned tile, unsigned flag,
+                                        unsigned long long value, unsigned epoch) {
+    st_status(&p.status[tile], ((unsigned long long)(epoch & kEpochMask) << 34) |
+                                   ((unsigned long long)flag << 32) | (value & 0xffffffffull));
+}
+
+__device__ __forceinline__ unsigned long long resolve(const K2Params& p, unsigned tile,
+                                                      unsigned epoch, unsigned lane) {
     constexpr int kPer = 8;
-    unsigned long long* st = p.status;
-    const unsigned long long E = (unsigned long long)(epoch & kEpochMask) << 34;
     const unsigned long long PF = (unsigned long long)kFlagP << 32;
-    if (tile == 0) {
-        if (lane == 0) st_status(&st[0], E | PF | total);
-        return 0ull;
-    }
-    if (lane == 0) st_status(&st[tile], E | ((unsigned long long)kFlagA << 32) | total);
+    const unsigned long long E = (unsigned long long)(epoch & kEpochMask) << 34;
     unsigned long long ex = 0;
     long long pred = (long long)tile - 1;
-    while (true) {
+    while (pred >= 0) {
         unsigned long long w[kPer];
 #pragma unroll
         for (int k = 0; k < kPer; ++k) {
             const long long t = pred - (long long)(kPer * lane + k);
-            w[k] = (t >= 0) ? ld_status(&st[t]) : (E | PF);
+            w[k] = (t >= 0) ? ld_status(&p.status[t]) : (E | PF);
         }
-        // lane-local: nearest P among its 8 (k = 0 is the nearest), validity, sum
         int kp = kPer;
         bool inval = false;
         unsigned long long sum = 0;
@@ -149,7 +149,7 @@ __device__ __forceinline__ unsigned long long lookback(const K2Params& p, unsign
         const unsigned lim = pmask ? (unsigned)(__ffs(pmask) - 1) : 31u;
         const unsigned need = (lim == 31u) ? kFull : ((2u << lim) - 1u);
         if (imask & need) {
-            __nanosleep(32);
+            __nanosleep(64);
             continue;
         }
         unsigned long long v = (lane <= lim) ? sum : 0ull;
@@ -159,210 +159,294 @@ __device__ __forceinline__ unsigned long long lookback(const K2Params& p, unsign
         if (pmask) break;
         pred -= 32 * kPer;
     }
-    if (lane == 0) st_status(&st[tile], E | PF | (ex + total));
     return ex;
 }
 
-// One super-tile = kK2Sub sub-tiles of kK2SubPairs point pairs.
-//   pass A: stream the sub-tiles (register double buffer), classify, keep the
-//           per-(sub-tile, item, warp) ballots in shared memory;
-//   scan:   256 counts -> exclusive offsets inside the super-tile;
-//   look-back (warp 0) -> global offset; the next super-tile's first
-//           sub-tile is already in flight;
-//   pass B: survivors' int64 indices (+ float2 re-read from L2, just streamed)
-//           written as contiguous runs per (sub-tile, item, warp).
+// ---------------------------------------------------------------- kernel
+// Per-super-tile state, double buffered: pass B of tile k-1 runs after pass A
+// of tile k.
+struct alignas(16) SurvEntry {
+    float x, y;
+    unsigned idx;    // local point index
+    unsigned meta;   // (group << 6) | (owner lane << 1) | pair element
+};
+
+constexpr int kK2Warps = kK2Threads / 32;
+constexpr int kGroups = kK2Sub * kK2Items * kK2Warps;   // 256 ballot groups per super-tile
+constexpr unsigned kList = 128;                          // per-warp survivor list per super-tile
+constexpr int kQueue = 2 * kK2Items * 32;                // per-warp undecided-point queue
+
+struct TileState {
+    unsigned mask[kGroups][2];     // keep ballots (element 0 / 1 of each pair)
+    unsigned off[kGroups];         // exclusive offset of each group inside the super-tile
+    unsigned wcnt[kK2Warps];       // survivors per warp
+    unsigned total;
+    SurvEntry list[kK2Warps][kList];
+};
+struct K2Smem {
+    TileState ts[2];
+    float2 qxy[kK2Warps][kQueue];
+    unsigned char qslot[kK2Warps][kQueue];
+    unsigned char own[kK2Warps][32];   // keep bits returned to each owner lane
+    unsigned wsum[kK2Warps];
+    unsigned next;
+    unsigned long long prefix;
+};
+
+// Pass B of a resolved super-tile: write indices (+ coordinates).
+__device__ __forceinline__ void emit(const K2Params& p, const TileState& ts, unsigned tbase,
+                                     unsigned long long ex, unsigned warp, unsigned lane,
+                                     unsigned lt) {
+    const unsigned wc = ts.wcnt[warp];
+    if (wc <= kList) {   // sparse: the compact list, full lanes
+        for (unsigned r = lane; r < wc; r += 32) {
+            const SurvEntry e = ts.list[warp][r];
+            const unsigned g = e.meta >> 6, ol = (e.meta >> 1) & 31u, h = e.meta & 1u;
+            const unsigned m0 = ts.mask[g][0], m1 = ts.mask[g][1], olt = (1u << ol) - 1u;
+            const unsigned rig = __popc(m0 & olt) + __popc(m1 & olt) + (h ? ((m0 >> ol) & 1u) : 0u);
+            const unsigned long long pos = ex + ts.off[g] + rig;
+            if (pos < p.capacity) {
+                p.out_idx[pos] = p.base + (long long)e.idx;
+                if (p.out_pts) reinterpret_cast<float2*>(p.out_pts)[pos] = make_float2(e.x, e.y);
+            }
+        }
+        return;
+    }
+    // dense: every group of this warp; coordinates re-read (L2-resident)
+#pragma unroll 1
+    for (int sub = 0; sub < kK2Sub; ++sub) {
+#pragma unroll
+        for (int u = 0; u < kK2Items; ++u) {
+            const int g = (sub * kK2Items + u) * kK2Warps + warp;
+            const unsigned b0 = ts.mask[g][0], b1 = ts.mask[g][1];
+            const bool k0 = (b0 >> lane) & 1u, k1 = (b1 >> lane) & 1u;
+            if (!(k0 | k1)) continue;
+            unsigned long long pos = ex + ts.off[g] + __popc(b0 & lt) + __popc(b1 & lt);
+            const unsigned i0 = 2u * (tbase + sub * kK2SubPairs + u * kK2Threads + threadIdx.x);
+            if (k0) {
+                if (pos < p.capacity) {
+                    p.out_idx[pos] = p.base + (long long)i0;
+                    if (p.out_pts)
+                        reinterpret_cast<float2*>(p.out_pts)[pos] =
+                            __ldcg(reinterpret_cast<const float2*>(p.pts) + i0);
+                }
+                ++pos;
+            }
+            if (k1 && pos < p.capacity) {
+                p.out_idx[pos] = p.base + (long long)(i0 + 1u);
+                if (p.out_pts)
+                    reinterpret_cast<float2*>(p.out_pts)[pos] =
+                        __ldcg(reinterpret_cast<const float2*>(p.pts) + i0 + 1);
+            }
+        }
+    }
+}
+
+// One super-tile = kK2Sub sub-tiles of kK2SubPairs point pairs (128 KiB).
+//   pass A(k):   stream + classify tile k, ballots and survivor list into
+//                ts[k&1]; block scan; publish tile k's aggregate;
+//   resolve(k-1): exclusive prefix of tile k-1 (its predecessors published
+//                long ago), publish its inclusive prefix;
+//   pass B(k-1): write tile k-1's survivors.
+// The next tile's ticket is taken after pass A(k) and its first sub-tile is
+// prefetched into registers before resolve/pass B.
 template <bool VEC, int EDGES>
 __global__ void __launch_bounds__(kK2Threads, 2) k2_filter(const __grid_constant__ K2Params p) {
-    constexpr int kWarps = kK2Threads / 32;
-    constexpr int kGroups = kK2Sub * kK2Items * kWarps;   // 256 ballot groups per super-tile
     static_assert(kGroups == kK2Threads, "one scan entry per thread");
-    __shared__ unsigned s_mask[kGroups][2];
-    __shared__ float2 s_stash[kWarps][kStash];
-    __shared__ float2 s_qxy[kWarps][2 * kK2Items * 32];         // undecided points
-    __shared__ unsigned char s_qslot[kWarps][2 * kK2Items * 32]; // owner lane * 8 + bit
-    __shared__ unsigned s_res[kWarps][2 * kK2Items];             // keep bits back to owners
-    __shared__ unsigned s_off[kGroups];
-    __shared__ unsigned s_wsum[kWarps];
-    __shared__ unsigned s_next;
-    __shared__ unsigned long long s_prefix;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    K2Smem& S = *reinterpret_cast<K2Smem*>(smem_raw);
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const unsigned lt = (1u << lane) - 1u;
     const unsigned epoch = *(volatile unsigned*)&p.ws->epoch;
 
-    if (threadIdx.x == 0) s_next = atomicAdd(&p.ws->k2_ticket, 1u);
+    if (threadIdx.x == 0) S.next = atomicAdd(&p.ws->k2_ticket, 1u);
     __syncthreads();
-    unsigned tile = s_next;
+    unsigned tile = S.next;
+    unsigned pend = 0xffffffffu;   // super-tile awaiting resolve + pass B
     float4 v[kK2Items];
     if (tile < p.num_tiles) {
 #pragma unroll
         for (int u = 0; u < kK2Items; ++u)
             v[u] = load_pair<VEC>(p.pts, tile * kK2TilePairs + u * kK2Threads + threadIdx.x, p.n);
     }
-    while (tile < p.num_tiles) {
+    for (unsigned k = 0;; ++k) {
+        const bool have = tile < p.num_tiles;
+        TileState& cur = S.ts[k & 1];
+        TileState& prv = S.ts[(k & 1) ^ 1];
         const unsigned tbase = tile * kK2TilePairs;
-        unsigned wc = 0;   // this warp's survivors so far in the super-tile (stash cursor)
-        // ---- pass A
+        if (have) {
+            // ---------------- pass A
+            const bool full_tile = p.mode == 0 && 2ull * (tbase + kK2TilePairs) <= (unsigned long long)p.n;
+            unsigned wc = 0;
 #pragma unroll 1
-        for (int sub = 0; sub < kK2Sub; ++sub) {
-            const unsigned qbase = tbase + sub * kK2SubPairs + threadIdx.x;
-            float4 vn[kK2Items];
-            if (sub + 1 < kK2Sub) {
+            for (int sub = 0; sub < kK2Sub; ++sub) {
+                const unsigned qbase = tbase + sub * kK2SubPairs + threadIdx.x;
+                float4 vn[kK2Items];
+                if (sub + 1 < kK2Sub) {
 #pragma unroll
-                for (int u = 0; u < kK2Items; ++u)
-                    vn[u] = load_pair<VEC>(p.pts, qbase + kK2SubPairs + u * kK2Threads, p.n);
-            }
-            // fast tests for the lane's 8 points: bit b = 2u + h
-            unsigned keep = 0u, needy = 0u;
-#pragma unroll
-            for (int u = 0; u < kK2Items; ++u) {
-                const unsigned i0 = 2u * (qbase + u * kK2Threads);
-                const unsigned valid = (i0 < p.n ? 1u : 0u) | (i0 + 1u < p.n ? 2u : 0u);
-                if (p.mode == 1) {
-                    keep |= valid << (2 * u);
-                } else {
-                    const unsigned in = (p.mode == 0 && fast_inside(p, v[u].x, v[u].y) ? 1u : 0u) |
-                                        (p.mode == 0 && fast_inside(p, v[u].z, v[u].w) ? 2u : 0u);
-                    needy |= (valid & ~in) << (2 * u);
-                }
-            }
-            // undecided points -> per-warp queue, tested with full lanes
-            const unsigned nq = __popc(needy);
-            unsigned incl = nq;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const unsigned y = __shfl_up_sync(kFull, incl, o);
-                if (lane >= (unsigned)o) incl += y;
-            }
-            const unsigned qtotal = __shfl_sync(kFull, incl, 31);
-            if (qtotal) {
-                if (lane < 2 * kK2Items) s_res[warp][lane] = 0u;
-                unsigned j = incl - nq;
-#pragma unroll
-                for (int b = 0; b < 2 * kK2Items; ++b) {
-                    if ((needy >> b) & 1u) {
-                        const float4 w = v[b >> 1];
-                        s_qxy[warp][j] = (b & 1) ? make_float2(w.z, w.w) : make_float2(w.x, w.y);
-                        s_qslot[warp][j] = (unsigned char)(lane * 8u + (unsigned)b);
-                        ++j;
+                    for (int u = 0; u < kK2Items; ++u) {
+                        const unsigned q = qbase + kK2SubPairs + u * kK2Threads;
+                        vn[u] = (VEC && full_tile) ? ld_stream(reinterpret_cast<const float4*>(p.pts) + q)
+                                                   : load_pair<VEC>(p.pts, q, p.n);
                     }
                 }
-                __syncwarp();
-                for (unsigned base = 0; base < qtotal; base += 32) {
-                    const unsigned e = base + lane;
-                    if (e < qtotal) {
-                        const float2 q = s_qxy[warp][e];
-                        if (queue_keep<EDGES>(p, q.x, q.y)) {
-                            const unsigned sl = s_qslot[warp][e];
-                            atomicOr(&s_res[warp][sl & 7u], 1u << (sl >> 3));
+                unsigned keep = 0u, needy = 0u;   // bit b = 2u + h
+                if (full_tile) {
+#pragma unroll
+                    for (int u = 0; u < kK2Items; ++u) {
+                        const unsigned in = (fast_inside(p, v[u].x, v[u].y) ? 1u : 0u) |
+                                            (fast_inside(p, v[u].z, v[u].w) ? 2u : 0u);
+                        needy |= (3u & ~in) << (2 * u);
+                    }
+                } else {
+#pragma unroll
+                    for (int u = 0; u < kK2Items; ++u) {
+                        const unsigned i0 = 2u * (qbase + u * kK2Threads);
+                        const unsigned valid = (i0 < p.n ? 1u : 0u) | (i0 + 1u < p.n ? 2u : 0u);
+                        if (p.mode == 1) {
+                            keep |= valid << (2 * u);
+                        } else {
+                            const unsigned in =
+                                (p.mode == 0 && fast_inside(p, v[u].x, v[u].y) ? 1u : 0u) |
+                                (p.mode == 0 && fast_inside(p, v[u].z, v[u].w) ? 2u : 0u);
+                            needy |= (valid & ~in) << (2 * u);
                         }
                     }
                 }
-                __syncwarp();
+                // Undecided points -> per-warp queue, tested with full lanes.
+                // Survivors are always queued points (fast paths only discard),
+                // so the survivor list is built here, in the queue pass.
+                const unsigned nq = __popc(needy);
+                unsigned incl = nq;
 #pragma unroll
-                for (int b = 0; b < 2 * kK2Items; ++b) keep |= ((s_res[warp][b] >> lane) & 1u) << b;
-                __syncwarp();
-            }
-#pragma unroll
-            for (int u = 0; u < kK2Items; ++u) {
-                const bool k0 = (keep >> (2 * u)) & 1u, k1 = (keep >> (2 * u + 1)) & 1u;
-                const unsigned b0 = __ballot_sync(kFull, k0);
-                const unsigned b1 = __ballot_sync(kFull, k1);
-                if (lane == 0) {
-                    const int g = (sub * kK2Items + u) * kWarps + warp;
-                    s_mask[g][0] = b0;
-                    s_mask[g][1] = b1;
+                for (int o = 1; o < 32; o <<= 1) {
+                    const unsigned y = __shfl_up_sync(kFull, incl, o);
+                    if (lane >= (unsigned)o) incl += y;
                 }
-                if (p.out_pts && (b0 | b1)) {   // stash survivors' coordinates (pass B order)
-                    const unsigned r0 = wc + __popc(b0 & lt) + __popc(b1 & lt);
-                    if (k0 && r0 < kStash) s_stash[warp][r0] = make_float2(v[u].x, v[u].y);
-                    if (k1 && r0 + k0 < kStash) s_stash[warp][r0 + k0] = make_float2(v[u].z, v[u].w);
+                const unsigned qtotal = __shfl_sync(kFull, incl, 31);
+                if (qtotal) {
+                    S.own[warp][lane] = 0;
+                    unsigned j = incl - nq;
+                    for (unsigned m = needy; m; m &= m - 1) {
+                        const unsigned b = __ffs(m) - 1;
+                        const float4 w = (b >> 1) == 0 ? v[0] : (b >> 1) == 1 ? v[1] : (b >> 1) == 2 ? v[2] : v[3];
+                        S.qxy[warp][j] = (b & 1) ? make_float2(w.z, w.w) : make_float2(w.x, w.y);
+                        S.qslot[warp][j] = (unsigned char)(lane * 8u + b);
+                        ++j;
+                    }
+                    __syncwarp();
+                    for (unsigned base = 0; base < qtotal; base += 32) {
+                        const unsigned e = base + lane;
+                        bool kp = false;
+                        float2 q = make_float2(0.f, 0.f);
+                        unsigned sl = 0;
+                        if (e < qtotal) {
+                            q = S.qxy[warp][e];
+                            sl = S.qslot[warp][e];
+                            kp = queue_keep<EDGES>(p, q.x, q.y);
+                        }
+                        const unsigned kb = __ballot_sync(kFull, kp);
+                        if (kp) {
+                            const unsigned ol = sl >> 3, bb = sl & 7u, u = bb >> 1, h = bb & 1u;
+                            atomicOr(reinterpret_cast<unsigned*>(&S.own[warp][ol & ~3u]),
+                                     (1u << bb) << (8u * (ol & 3u)));
+                            const unsigned r = wc + __popc(kb & lt);
+                            if (r < kList) {
+                                const unsigned g = (sub * kK2Items + u) * kK2Warps + warp;
+                                cur.list[warp][r] = SurvEntry{
+                                    q.x, q.y, 2u * (qbase - lane + ol + u * kK2Threads) + h,
+                                    (g << 6) | (ol << 1) | h};
+                            }
+                        }
+                        wc += __popc(kb);
+                    }
+                    __syncwarp();
+                    keep |= S.own[warp][lane];
                 }
-                wc += __popc(b0) + __popc(b1);
-            }
-            if (sub + 1 < kK2Sub) {
+                if (qtotal || p.mode == 1) {
 #pragma unroll
-                for (int u = 0; u < kK2Items; ++u) v[u] = vn[u];
+                    for (int u = 0; u < kK2Items; ++u) {
+                        const unsigned b0 = __ballot_sync(kFull, (keep >> (2 * u)) & 1u);
+                        const unsigned b1 = __ballot_sync(kFull, (keep >> (2 * u + 1)) & 1u);
+                        if (lane == 0) {
+                            const unsigned g = (sub * kK2Items + u) * kK2Warps + warp;
+                            cur.mask[g][0] = b0;
+                            cur.mask[g][1] = b1;
+                        }
+                        if (p.mode == 1) wc += __popc(b0) + __popc(b1);   // list unused: dense pass B
+                    }
+                } else if (lane < kK2Items) {
+                    const unsigned g = (sub * kK2Items + lane) * kK2Warps + warp;
+                    cur.mask[g][0] = 0u;
+                    cur.mask[g][1] = 0u;
+                }
+                if (sub + 1 < kK2Sub) {
+#pragma unroll
+                    for (int u = 0; u < kK2Items; ++u) v[u] = vn[u];
+                }
             }
+            if (lane == 0) cur.wcnt[warp] = (p.mode == 1) ? kList + 1u : wc;
+            // next ticket only now: a tile is never held while its block is busy
+            if (threadIdx.x == 0) S.next = atomicAdd(&p.ws->k2_ticket, 1u);
+            __syncthreads();
+            // ---------------- block scan of the 256 group counts (group order = index order)
+            {
+                const unsigned c = __popc(cur.mask[threadIdx.x][0]) + __popc(cur.mask[threadIdx.x][1]);
+                unsigned incl = c;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const unsigned y = __shfl_up_sync(kFull, incl, o);
+                    if (lane >= (unsigned)o) incl += y;
+                }
+                if (lane == 31) S.wsum[warp] = incl;
+                __syncthreads();
+                unsigned wpre = 0, total = 0;
+#pragma unroll
+                for (int w = 0; w < kK2Warps; ++w) {
+                    const unsigned x = S.wsum[w];
+                    wpre += (w < (int)warp) ? x : 0u;
+                    total += x;
+                }
+                cur.off[threadIdx.x] = wpre + incl - c;
+                if (threadIdx.x == 0) {
+                    cur.total = total;
+                    if (tile == 0) {   // first tile: its inclusive prefix is known now
+                        publish(p, 0, kFlagP, total, epoch);
+                        if (p.num_tiles == 1) p.ws->count = total;
+                    } else {
+                        publish(p, tile, kFlagA, total, epoch);
+                    }
+                }
+            }
+        } else if (threadIdx.x == 0) {
+            S.next = 0xffffffffu;
         }
-        // The next ticket is taken only now, so a tile is never held while its
-        // block is still busy with an earlier one (that made successors' look-
-        // backs wait a whole tile time and the delays cascade).
-        if (threadIdx.x == 0) s_next = atomicAdd(&p.ws->k2_ticket, 1u);
         __syncthreads();
-        const unsigned next = s_next;
+        const unsigned next = have ? S.next : 0xffffffffu;
         if (next < p.num_tiles) {   // prefetch the next super-tile's first sub-tile
 #pragma unroll
             for (int u = 0; u < kK2Items; ++u)
                 v[u] = load_pair<VEC>(p.pts, next * kK2TilePairs + u * kK2Threads + threadIdx.x, p.n);
         }
-        // ---- block exclusive scan of the 256 group counts (group order = index order)
-        {
-            const unsigned c = __popc(s_mask[threadIdx.x][0]) + __popc(s_mask[threadIdx.x][1]);
-            unsigned incl = c;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const unsigned y = __shfl_up_sync(kFull, incl, o);
-                if (lane >= (unsigned)o) incl += y;
-            }
-            if (lane == 31) s_wsum[warp] = incl;
-            __syncthreads();
-            unsigned wpre = 0, total = 0;
-#pragma unroll
-            for (int w = 0; w < kWarps; ++w) {
-                const unsigned x = s_wsum[w];
-                wpre += (w < (int)warp) ? x : 0u;
-                total += x;
-            }
-            s_off[threadIdx.x] = wpre + incl - c;
+        // ---------------- resolve + pass B of the pending super-tile
+        if (pend != 0xffffffffu) {
             if (warp == 0) {
-                const unsigned long long ex = lookback(p, tile, total, epoch, lane);
-                if (lane == 0) {
-                    s_prefix = ex;
-                    if (tile == p.num_tiles - 1) p.ws->count = ex + total;
-                }
-            }
-        }
-        __syncthreads();
-        // ---- pass B: coordinates come from the stash (global re-read only on overflow)
-        const unsigned long long ex = s_prefix;
-        wc = 0;
-#pragma unroll 1
-        for (int sub = 0; sub < kK2Sub; ++sub) {
-#pragma unroll
-            for (int u = 0; u < kK2Items; ++u) {
-                const int g = (sub * kK2Items + u) * kWarps + warp;
-                const unsigned b0 = s_mask[g][0], b1 = s_mask[g][1];
-                if ((b0 | b1) == 0u) continue;
-                const bool k0 = (b0 >> lane) & 1u, k1 = (b1 >> lane) & 1u;
-                const unsigned r0 = __popc(b0 & lt) + __popc(b1 & lt);
-                unsigned long long pos = ex + s_off[g] + r0;
-                const unsigned q = tbase + sub * kK2SubPairs + u * kK2Threads + threadIdx.x;
-                const unsigned i0 = 2u * q;
-                if (k0 | k1) {
-                    float2 a = make_float2(0.f, 0.f), b = a;
-                    if (p.out_pts) {
-                        const unsigned s0 = wc + r0;
-                        if (k0) a = s0 < kStash ? s_stash[warp][s0]
-                                                : __ldcg(reinterpret_cast<const float2*>(p.pts) + i0);
-                        if (k1) b = s0 + k0 < kStash ? s_stash[warp][s0 + k0]
-                                                     : __ldcg(reinterpret_cast<const float2*>(p.pts) + i0 + 1);
-                    }
-                    if (k0) {
-                        if (pos < p.capacity) {
-                            p.out_idx[pos] = p.base + (long long)i0;
-                            if (p.out_pts) reinterpret_cast<float2*>(p.out_pts)[pos] = a;
-                        }
-                        ++pos;
-                    }
-                    if (k1 && pos < p.capacity) {
-                        p.out_idx[pos] = p.base + (long long)(i0 + 1u);
-                        if (p.out_pts) reinterpret_cast<float2*>(p.out_pts)[pos] = b;
+                unsigned long long ex = 0;
+                if (pend != 0) {
+                    ex = resolve(p, pend, epoch, lane);
+                    if (lane == 0) {
+                        publish(p, pend, kFlagP, ex + prv.total, epoch);
+                        if (pend == p.num_tiles - 1) p.ws->count = ex + prv.total;
                     }
                 }
-                wc += __popc(b0) + __popc(b1);
+                if (lane == 0) S.prefix = ex;
             }
+            __syncthreads();
+            emit(p, prv, pend * kK2TilePairs, S.prefix, warp, lane, lt);
         }
-        __syncthreads();   // shared arrays are reused by the next super-tile
+        __syncthreads();   // prv is reused by the next pass A
+        if (!have) break;
+        pend = tile;
         tile = next;
     }
     // last block out resets the ticket and bumps the epoch (all blocks have
@@ -384,14 +468,16 @@ __global__ void __launch_bounds__(kK2Threads, 2) k2_filter(const __grid_constant
 template <bool VEC, int EDGES>
 cudaError_t launch_t(const K2Params& p, cudaStream_t s, int* launches) {
     static int max_blocks = 0;
+    const int smem = (int)sizeof(K2Smem);
     if (!max_blocks) {
+        cudaFuncSetAttribute(k2_filter<VEC, EDGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2_filter<VEC, EDGES>, kK2Threads, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2_filter<VEC, EDGES>, kK2Threads, smem);
         max_blocks = (per_sm > 0 ? per_sm : 1) * device_sm_count();
     }
     unsigned blocks = p.num_tiles < (unsigned)max_blocks ? p.num_tiles : (unsigned)max_blocks;
     if (blocks < 1) blocks = 1;
-    k2_filter<VEC, EDGES><<<blocks, kK2Threads, 0, s>>>(p);
+    k2_filter<VEC, EDGES><<<blocks, kK2Threads, smem, s>>>(p);
     ++*launches;
     return cudaGetLastError();
 }
