@@ -93,7 +93,7 @@ typedef struct {
     int64_t vidx[CUDAPRE_MAX_SLOTS];     /* global index of each ring vertex */
     cudapre_pt v[CUDAPRE_MAX_SLOTS];     /* ring vertex coordinates */
     float box[4];                        /* inner box x0,x1,y0,y1 strictly inside the ring (x0>x1: none) */
-    float circle[4];                     /* inner disk: centre x, y; r2 with RN32((x-cx)^2+(y-cy)^2)
+    float circle[4];                     /* inner disk: centre x, y; r2 with RN32(RN32(dx^2)+RN32(dy^2)), d = RN32(p - c),
                                           * < r2 => strictly inside (r2 < 0: none); pad */
     float err_max;                       /* largest per-edge float error bound E_j */
     int32_t pad;

@@ -16,8 +16,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libcudapre.so")
 BUILD = os.path.join(HERE, "_build")
-SOURCES = ["api.cpp", "host_geom.cpp", "k1_extremes.cu", "k2_filter.cu"]
-HEADERS = ["internal.h", "exact.cuh", os.path.join("..", "..", "include", "cudapre.h")]
+SOURCES = ["api.cpp", "host_geom.cpp", "k1_extremes.cu", "k2_filter.cu", "k2_filter_tma.cu"]
+HEADERS = ["internal.h", "exact.cuh", "k2_common.cuh", "tma.cuh", os.path.join("..", "..", "include", "cudapre.h")]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-ffp-contract=off,-O2",
               "--expt-relaxed-constexpr"]

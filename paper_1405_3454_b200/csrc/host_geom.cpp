@@ -266,7 +266,7 @@ void build_polygon(const cudapre_extremes_t& ext, cudapre_polygon_t* poly, K2Par
     // ---- inner disk: centre O (box centre, else vertex mean,
     //      rounded to float and checked strictly inside exactly), radius^2 =
     //      (1 - 2^-16) * (a rigorous LOWER bound of min_j dist(O, edge line j))^2.
-    //      Kernel test RN32(fma(dx, dx, RN32(dy*dy))) < r2 with dx = RN32(x - ox):
+    //      Kernel test RN32(RN32(dx*dx) + RN32(dy*dy)) < r2 with dx = RN32(x - ox):
     //      the float value is >= true d^2 (1 - 4u), so acceptance implies true
     //      d^2 < R^2 (1 - 2^-16) / (1 - 4u) < R^2.  Disabled outside [2^-100, 2^100].
     poly->circle[0] = 0.0f;

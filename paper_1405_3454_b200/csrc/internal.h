@@ -14,6 +14,7 @@ constexpr int kK1Unroll = 4;           // float4 (= 2 points) per thread per ite
 constexpr int kSeedThreads = 128;      // seed block; one chunk = 128 float4 = 256 points
 constexpr int kK1StagePairs = kK1Threads * kK1Unroll;   // 1024 pairs = 16 KiB per TMA stage
 constexpr int kK1Stages = 4;           // TMA ring depth per block
+constexpr int kK1Queue = 32 + 2 * kK1Unroll * 32;   // per-warp pre-screen queue: 31 carried + one iteration (256)
 constexpr int kK2Threads = 256;        // K2 block
 constexpr int kK2Items = 4;            // float4 per thread per sub-tile
 constexpr int kK2SubPairs = kK2Threads * kK2Items;    // 1024 pairs = 2048 points per sub-tile
@@ -84,7 +85,7 @@ struct K2Params {
     unsigned int num_tiles;
     int mode;                 // 0 = filter, 1 = keep everything (degenerate), 2 = exact only
     float bx0, bx1, by0, by1; // inner box (closed), strictly inside the ring
-    float ox, oy, r2;         // inner disk: RN(fma(dx,dx,RN(dy*dy))) < r2 => strictly inside (r2 < 0: off)
+    float ox, oy, r2;         // inner disk: RN(RN(dx^2)+RN(dy^2)) < r2 => strictly inside (r2 < 0: off)
     float e2max;              // 2 * max_j E_j
     float A[CUDAPRE_MAX_SLOTS], B[CUDAPRE_MAX_SLOTS], C[CUDAPRE_MAX_SLOTS];   // C already lowered by E_j
     float vx[CUDAPRE_MAX_SLOTS + 1], vy[CUDAPRE_MAX_SLOTS + 1];               // ring, v[nv] = v[0]
@@ -94,6 +95,8 @@ struct K2Params {
 // All return a cudaError_t as int (0 = success).
 int launch_extremes(const K1Params& p, int vec16, void* stream, int* launches);
 int launch_filter(const K2Params& p, int vec16, void* stream, int* launches);
+int launch_filter_tma(const K2Params& p, void* stream, int* launches);   // vec16, mode 0
+int k2_use_tma();   // CUDAPRE_K2_TMA (default 1)
 int device_sm_count();
 
 // ---------------------------------------------------------------- host geometry (host_geom.cpp)

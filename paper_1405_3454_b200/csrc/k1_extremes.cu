@@ -37,6 +37,7 @@
 #include <cstdint>
 
 #include "internal.h"
+#include "tma.cuh"
 
 namespace cudapre {
 namespace {
@@ -50,36 +51,6 @@ __device__ __forceinline__ float4 ld_stream(const float4* p) {
                  : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
                  : "l"(p));
     return r;
-}
-
-// ---- TMA bulk copy + mbarrier (sm_90+/sm_100a): global -> shared, no registers
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-    return static_cast<unsigned>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_fence_init() {
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
-                                         unsigned long long* bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
-    asm volatile(
-        "{\n .reg .pred P1;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-        " @!P1 bra WAIT_%=;\n }" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
 }
 
 // Load the point pair q = (2q, 2q+1); v1 false if 2q+1 >= n.  VEC: 16-B aligned base.
@@ -234,6 +205,39 @@ __device__ __forceinline__ void refresh_thresholds(float (&T)[4 * NANG], const W
     }
 }
 
+// Pre-screen disk: with c = centre of the angle-0 thresholds
+// and slack_s = T_s - key_s(c) (max slots) / key_s(c) - T_s (min slots), a
+// point with |p - c| < rho = min_s slack_s (1 - 2^-10) - (|cx|+|cy|) 2^-17
+// - 2^-100 cannot pass the float screen of any slot (the screen margin m,
+// the binary64 key rounding and ulp(T_s) are all absorbed by the two
+// relative terms).  The kernel tests d2 = RN(RN(dx^2)+RN(dy^2)) < rho2 with
+// (dx, dy) = RN(p - c); d2 >= |p-c|^2 (1 - 4u) and rho2 <= rho^2 (1 - 2^-16).
+// rho2 = -1 disables the pre-screen (no seed yet, or no positive slack).
+template <int NANG>
+__device__ __forceinline__ void prescreen_params(const float (&T)[4 * NANG], const K1Params& p,
+                                                 float& cx, float& cy, float& rho2) {
+    cx = __fmul_rn(__fadd_rn(T[0], T[1]), 0.5f);
+    cy = __fmul_rn(__fadd_rn(T[2], T[3]), 0.5f);
+    rho2 = -1.0f;
+    if (!isfinite(cx) || !isfinite(cy)) return;
+    double smin = INFINITY;
+#pragma unroll
+    for (int k = 0; k < NANG; ++k) {
+        const double px = __dadd_rn(__dmul_rn((double)cx, p.c[k]), __dmul_rn((double)cy, p.s[k]));
+        const double py = __dsub_rn(__dmul_rn((double)cy, p.c[k]), __dmul_rn((double)cx, p.s[k]));
+        smin = fmin(smin, __dsub_rn(px, (double)T[4 * k + 0]));
+        smin = fmin(smin, __dsub_rn((double)T[4 * k + 1], px));
+        smin = fmin(smin, __dsub_rn(py, (double)T[4 * k + 2]));
+        smin = fmin(smin, __dsub_rn((double)T[4 * k + 3], py));
+    }
+    const double ac = __dadd_rn(fabs((double)cx), fabs((double)cy));
+    const double rho = __dsub_rn(__dsub_rn(__dmul_rn(smin, 1.0 - 0x1p-10), __dmul_rn(ac, 0x1p-17)), 0x1p-100);
+    if (!(rho > 0.0) || !isfinite(rho)) return;
+    const double r2 = fmin(__dmul_rn(__dmul_rn(rho, rho), 1.0 - 0x1p-16), 0x1p126);
+    if (r2 < 0x1p-100) return;
+    rho2 = __double2float_rd(r2);
+}
+
 // ---------------------------------------------------------------- seed kernel
 // Float-only bounds over sample chunks spread evenly over the input:
 //   max slot: a float <= the exact key of some sampled point  (RD(Xf - m))
@@ -308,6 +312,8 @@ __global__ void __launch_bounds__(kK1Threads, 2) k1_extremes(const K1Params p) {
     constexpr int NS = 4 * NANG;
     constexpr int kWarps = kK1Threads / 32;
     __shared__ WarpState<NANG> sst[kWarps];
+    __shared__ float sqx[kWarps][kK1Queue], sqy[kWarps][kK1Queue];
+    __shared__ unsigned sqi[kWarps][kK1Queue];
     __shared__ bool s_last;
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     WarpState<NANG>& st = sst[warp];
@@ -327,6 +333,9 @@ __global__ void __launch_bounds__(kK1Threads, 2) k1_extremes(const K1Params p) {
         st.idx[lane] = kNoIdx;
     }
     __syncwarp();
+    float pcx, pcy, prho2;
+    prescreen_params<NANG>(T, p, pcx, pcy, prho2);
+    unsigned qcount = 0;   // this warp's queued points (uniform)
 
     const unsigned npairs = (p.n + 1u) / 2u;
     const unsigned stride = gridDim.x * kK1Threads * kK1Unroll;
@@ -350,27 +359,86 @@ __global__ void __launch_bounds__(kK1Threads, 2) k1_extremes(const K1Params p) {
             }
         }
     };
-    // screen 4 pairs; the rare candidates take the exact path (cold)
-    auto process = [&](const float4 (&v)[kK1Unroll], unsigned qb) {
-        bool cand = false;
-#pragma unroll
-        for (int u = 0; u < kK1Unroll; ++u) cand |= screen2<NANG>(v[u], T, p);
-        if (__any_sync(kFull, cand)) {
-            unsigned mask = __ballot_sync(kFull, cand);
-            while (mask) {
-                const unsigned l = __ffs(mask) - 1;
-                mask &= mask - 1;
-                if (lane == l) {
-#pragma unroll
-                    for (int u = 0; u < kK1Unroll; ++u) {
-                        st.stage[u] = v[u];
-                        st.stage_q[u] = qb + u * kK1Threads;
-                    }
-                    exact_staged<NANG>(st, T, p);
-                }
-                __syncwarp();
+    // Screen queued points in full 32-lane batches (all of them if `all`):
+    // float screen, then the rare candidates' exact binary64 update (cold).
+    auto drain = [&](bool all) {
+        const unsigned nb = all ? qcount : (qcount & ~31u);
+        for (unsigned base = 0; base < nb; base += 32) {
+            const unsigned e = base + lane;
+            bool cand = false;
+            float x = 0.f, y = 0.f;
+            unsigned i = 0;
+            if (e < nb) {
+                x = sqx[warp][e];
+                y = sqy[warp][e];
+                i = sqi[warp][e];
+                cand = screen1<NANG>(x, y, T, p);
             }
-            refresh_thresholds<NANG>(T, st);
+            unsigned mask = __ballot_sync(kFull, cand);
+            if (mask) {
+                const unsigned hits = __popc(mask);
+                while (mask) {
+                    const unsigned l = __ffs(mask) - 1;
+                    mask &= mask - 1;
+                    if (lane == l) exact_update<NANG>(st, x, y, i, p);
+                    __syncwarp();
+                }
+                if (lane == 0) atomicAdd(&p.ws->k1_exact, hits);
+                refresh_thresholds<NANG>(T, st);
+                prescreen_params<NANG>(T, p, pcx, pcy, prho2);
+            }
+        }
+        const unsigned rem = qcount - nb;   // < 32: move to the front
+        float rx = 0.f, ry = 0.f;
+        unsigned ri = 0;
+        if (lane < rem) {
+            rx = sqx[warp][nb + lane];
+            ry = sqy[warp][nb + lane];
+            ri = sqi[warp][nb + lane];
+        }
+        __syncwarp();
+        if (lane < rem) {
+            sqx[warp][lane] = rx;
+            sqy[warp][lane] = ry;
+            sqi[warp][lane] = ri;
+        }
+        __syncwarp();
+        qcount = rem;
+    };
+    // Pre-screen 4 pairs against the warp's disk; queue the rest.
+    auto process = [&](const float4 (&v)[kK1Unroll], unsigned qb) {
+        unsigned needy = 0u;   // bit b = 2u + h
+        const float2 nc = make_float2(-pcx, -pcy);
+#pragma unroll
+        for (int u = 0; u < kK1Unroll; ++u) {
+            const float2 d0 = __fmul2_rn(__fadd2_rn(make_float2(v[u].x, v[u].y), nc), __fadd2_rn(make_float2(v[u].x, v[u].y), nc));
+            const float2 d1 = __fmul2_rn(__fadd2_rn(make_float2(v[u].z, v[u].w), nc), __fadd2_rn(make_float2(v[u].z, v[u].w), nc));
+            needy |= ((__fadd_rn(d0.x, d0.y) < prho2) ? 0u : 1u) << (2 * u);
+            needy |= ((__fadd_rn(d1.x, d1.y) < prho2) ? 0u : 2u) << (2 * u);
+        }
+        const unsigned nq = __popc(needy);
+        unsigned incl = nq;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned t = __shfl_up_sync(kFull, incl, o);
+            if (lane >= (unsigned)o) incl += t;
+        }
+        const unsigned qtotal = __shfl_sync(kFull, incl, 31);
+        if (qtotal) {
+            unsigned j = qcount + incl - nq;
+#pragma unroll
+            for (int b = 0; b < 2 * kK1Unroll; ++b) {
+                if ((needy >> b) & 1u) {
+                    const float4 w = v[b >> 1];
+                    sqx[warp][j] = (b & 1) ? w.z : w.x;
+                    sqy[warp][j] = (b & 1) ? w.w : w.y;
+                    sqi[warp][j] = 2u * (qb + (b >> 1) * kK1Threads) + (unsigned)(b & 1);
+                }
+                j += (needy >> b) & 1u;
+            }
+            qcount += qtotal;
+            __syncwarp();
+            if (qcount >= 32u) drain(false);
         }
     };
     if constexpr (TMA) {
@@ -425,6 +493,7 @@ __global__ void __launch_bounds__(kK1Threads, 2) k1_extremes(const K1Params p) {
             for (int u = 0; u < kK1Unroll; ++u) v[u] = vn[u];
         }
     }
+    drain(true);
     // remainder (guarded)
     for (; q0 - lane < npairs; q0 += stride) {
         float4 v[kK1Unroll];

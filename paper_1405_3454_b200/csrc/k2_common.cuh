@@ -1,0 +1,147 @@
+// k2_common.cuh — device helpers shared by the two Step-3 kernels
+// (k2_filter.cu: register path; k2_filter_tma.cu: TMA-ring path).  Internal
+// linkage: each translation unit gets its own copy.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "exact.cuh"
+#include "internal.h"
+
+namespace cudapre {
+namespace {
+
+constexpr unsigned kFull = 0xffffffffu;
+constexpr unsigned kFlagA = 1u;   // tile aggregate available
+constexpr unsigned kFlagP = 2u;   // inclusive prefix available
+constexpr unsigned kEpochMask = 0x3fffffffu;
+
+__device__ __forceinline__ float4 ld_stream(const float4* p) {
+    float4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+                 : "l"(p));
+    return r;
+}
+
+__device__ __forceinline__ void st_status(unsigned long long* a, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(a), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_status(const unsigned long long* a) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(a) : "memory");
+    return v;
+}
+
+template <bool VEC>
+__device__ __forceinline__ float4 load_pair(const float* pts, unsigned q, unsigned n) {
+    const unsigned i0 = 2u * q;
+    float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (i0 + 1u < n) {
+        if (VEC) {
+            r = ld_stream(reinterpret_cast<const float4*>(pts) + q);
+        } else {
+            const float2 a = __ldg(reinterpret_cast<const float2*>(pts) + i0);
+            const float2 b = __ldg(reinterpret_cast<const float2*>(pts) + i0 + 1);
+            r = make_float4(a.x, a.y, b.x, b.y);
+        }
+    } else if (i0 < n) {
+        const float2 a = __ldg(reinterpret_cast<const float2*>(pts) + i0);
+        r = make_float4(a.x, a.y, 0.f, 0.f);
+    }
+    return r;
+}
+
+__device__ __noinline__ bool exact_inside(const K2Params& p, float x, float y) {
+    for (int j = 0; j < p.nv; ++j)
+        if (orient_sign_f(p.vx[j], p.vy[j], p.vx[j + 1], p.vy[j + 1], x, y) <= 0) return false;
+    return true;
+}
+
+// Certainly strictly inside (inner box or inner disk; both proven on the host).
+// Disk: (dx, dy) = RN((x, y) - (ox, oy)) in one FADD2, squares in one FMUL2,
+// d2 = RN(dx^2 + dy^2) >= true d^2 (1 - 4u) — the bound DESIGN.md §6.2 uses.
+// Bitwise (not short-circuit) logic: no branches.
+__device__ __forceinline__ bool fast_inside(const K2Params& p, float x, float y) {
+    const float2 d = __fadd2_rn(make_float2(x, y), make_float2(-p.ox, -p.oy));
+    const float2 d2 = __fmul2_rn(d, d);
+    const bool in_disk = __fadd_rn(d2.x, d2.y) < p.r2;
+    const bool in_box = (x >= p.bx0) & (x <= p.bx1) & (y >= p.by0) & (y <= p.by1);
+    return in_disk | in_box;
+}
+
+// Survivor test for a point the fast tests could not decide (true = keep).
+// EDGES: compile-time edge count; the host pads edges nv..EDGES-1 with
+// A = B = 0, C = +inf (never the minimum), so the loop fully unrolls and the
+// coefficients are constant-bank operands of the FFMAs.
+template <int EDGES>
+__device__ __forceinline__ bool queue_keep(const K2Params& p, float x, float y) {
+    if (p.mode == 2) return !exact_inside(p, x, y);
+    float mn = INFINITY;
+#pragma unroll
+    for (int j = 0; j < EDGES; ++j) mn = fminf(mn, __fmaf_rn(p.A[j], x, __fmaf_rn(p.B[j], y, p.C[j])));
+    if (mn > 0.0f) return false;
+    if (__fadd_rn(mn, p.e2max) < 0.0f) return true;
+    return !exact_inside(p, x, y);
+}
+
+// ---------------------------------------------------------------- look-back
+// Status word of super-tile t: [epoch:30 | flag:2 | count:32].  publish_*
+// write it with one relaxed 64-bit store; resolve() (warp 0) walks back 256
+// predecessors per round (8 loads in flight per lane) summing aggregates up to
+// the nearest inclusive prefix.  Because resolve(t) runs one tile-time after
+// t's own aggregate was published (deferred, see the kernel), every
+// predecessor's aggregate is normally already there: no spinning.
+__device__ __forceinline__ void publish(const K2Params& p, unsigned tile, unsigned flag,
+                                        unsigned long long value, unsigned epoch) {
+    st_status(&p.status[tile], ((unsigned long long)(epoch & kEpochMask) << 34) |
+                                   ((unsigned long long)flag << 32) | (value & 0xffffffffull));
+}
+
+__device__ __forceinline__ unsigned long long resolve(const K2Params& p, unsigned tile,
+                                                      unsigned epoch, unsigned lane) {
+    constexpr int kPer = 8;
+    const unsigned long long PF = (unsigned long long)kFlagP << 32;
+    const unsigned long long E = (unsigned long long)(epoch & kEpochMask) << 34;
+    unsigned long long ex = 0;
+    long long pred = (long long)tile - 1;
+    while (pred >= 0) {
+        unsigned long long w[kPer];
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) {
+            const long long t = pred - (long long)(kPer * lane + k);
+            w[k] = (t >= 0) ? ld_status(&p.status[t]) : (E | PF);
+        }
+        int kp = kPer;
+        bool inval = false;
+        unsigned long long sum = 0;
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) {
+            const unsigned flag =
+                ((unsigned)(w[k] >> 34) == (epoch & kEpochMask)) ? (unsigned)((w[k] >> 32) & 3u) : 0u;
+            if (kp == kPer) {
+                if (flag == 0u) inval = true;
+                sum += w[k] & 0xffffffffull;
+                if (flag == kFlagP) kp = k;
+            }
+        }
+        const unsigned pmask = __ballot_sync(kFull, kp < kPer);
+        const unsigned imask = __ballot_sync(kFull, inval);
+        const unsigned lim = pmask ? (unsigned)(__ffs(pmask) - 1) : 31u;
+        const unsigned need = (lim == 31u) ? kFull : ((2u << lim) - 1u);
+        if (imask & need) {
+            __nanosleep(64);
+            continue;
+        }
+        unsigned long long v = (lane <= lim) ? sum : 0ull;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+        ex += v;
+        if (pmask) break;
+        pred -= 32 * kPer;
+    }
+    return ex;
+}
+
+}  // namespace
+}  // namespace cudapre

@@ -241,7 +241,7 @@ def test_k2_float_decisions_are_conservative(L, oracle_lib):
 
 def test_k2_inner_disk_is_conservative(L, oracle_lib):
     """every point the kernel's disk test accepts
-    (RN32(fma(dx, dx, RN32(dy*dy))) < r2, dx = RN32(x - ox)) is strictly inside
+    (RN32(RN32(dx*dx) + RN32(dy*dy)) < r2, dx = RN32(x - ox)) is strictly inside
     the ring by the exact predicate — probed on and around the disk boundary."""
     for family, seed in (("disk", 13), ("square", 2), ("gauss", 4), ("circle", 5)):
         xy = synth.generate(family, 50_000, seed=seed)
@@ -260,7 +260,7 @@ def test_k2_inner_disk_is_conservative(L, oracle_lib):
                 p = np.array([ox + f * r * np.cos(th), oy + f * r * np.sin(th)], np.float32)
                 dx = np.float32(p[0] - np.float32(ox))
                 dy = np.float32(p[1] - np.float32(oy))
-                d2 = _fma32(dx, dx, np.float32(dy * dy))
+                d2 = np.float32(np.float32(dx * dx) + np.float32(dy * dy))   # kernel: FADD2, FMUL2, FADD
                 if d2 < np.float32(r2):
                     accepted += 1
                     assert brute.strictly_inside_frac(V, p), (family, p)
