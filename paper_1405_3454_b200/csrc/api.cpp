@@ -319,7 +319,7 @@ cudapre_status cudapre_filter(const cudapre_pt* d_pts, int64_t n_local, int64_t 
     p.capacity = (unsigned long long)capacity;
     p.ws = ws_header(d_ws);
     p.status = ws_status(d_ws);
-    p.num_tiles = (unsigned)ws_tiles(n_local);
+    p.num_tiles = (unsigned)((n_local + kK2TilePts - 1) / kK2TilePts);   // the TMA launcher re-derives its own
     const int vec16 = (((uintptr_t)d_pts & 15u) == 0);
 
     cudaEvent_t* ev = nullptr;

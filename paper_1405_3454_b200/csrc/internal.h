@@ -52,7 +52,9 @@ struct K1Partial {
 constexpr size_t kWsHeaderBytes = 4096;
 constexpr size_t kWsPartialBytes = sizeof(K1Partial) * kMaxK1Blocks * CUDAPRE_MAX_SLOTS;
 
-inline size_t ws_tiles(int64_t n) { return (size_t)((n + kK2TilePts - 1) / kK2TilePts); }
+// tile-status words are sized for the smallest super-tile any K2 kernel uses
+constexpr int kStatusTilePts = 14336;   // warp-specialised K2: 7168 pairs
+inline size_t ws_tiles(int64_t n) { return (size_t)((n + kStatusTilePts - 1) / kStatusTilePts); }
 inline size_t ws_bytes_for(int64_t n) {
     return kWsHeaderBytes + kWsPartialBytes + 8 * (ws_tiles(n) + 1);
 }

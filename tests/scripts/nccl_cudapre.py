@@ -1,0 +1,42 @@
+"""Run under torchrun: each rank filters its contiguous shard through the
+public API with group=WORLD (NCCL all-gather of the per-rank Step-1 structs),
+then rank 0 gathers the survivors and checks them against the oracle."""
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
+import oracle  # noqa: E402
+import paper_1405_3454_b200 as cp  # noqa: E402
+import synth  # noqa: E402
+
+N = int(os.environ.get("NCCL_TEST_N", "3000017"))
+
+
+def main():
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+    dist.init_process_group("nccl", device_id=torch.device("cuda", torch.cuda.current_device()))
+    n_local = N // world + (1 if rank < N % world else 0)
+    base = rank * (N // world) + min(rank, N % world)
+    xy = synth.generate("disk", n_local, seed=6, base=base)
+    pts = torch.from_numpy(xy).cuda()
+    idx, sp, rep = cp.cuda_pre(pts, "A", group=dist.group.WORLD, index_base=base)
+    counts = [None] * world
+    dist.all_gather_object(counts, idx.cpu().numpy())
+    if rank == 0:
+        got = np.concatenate(counts)
+        full = synth.generate("disk", N, seed=6)
+        want = oracle.cudapre(full, "A", threads=os.cpu_count())
+        assert rep["extremes"].idx.tolist() == want["ext_idx"].tolist(), "Step 1"
+        assert np.array_equal(got, want["survivors"]), "Step 3"
+        print(f"nccl ok world={world} survivors={len(got)}")
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

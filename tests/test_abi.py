@@ -265,3 +265,62 @@ def test_k2_inner_disk_is_conservative(L, oracle_lib):
                     accepted += 1
                     assert brute.strictly_inside_frac(V, p), (family, p)
         assert accepted > 400
+
+
+def _prescreen_params(T, c, s):
+    """Python mirror of k1_extremes.cu:prescreen_params (float32/float64 IEEE ops)."""
+    f32 = np.float32
+    cx = f32(f32(f32(T[0]) + f32(T[1])) * f32(0.5))
+    cy = f32(f32(f32(T[2]) + f32(T[3])) * f32(0.5))
+    smin = np.inf
+    for k in range(len(c)):
+        px = float(cx) * c[k] + float(cy) * s[k]
+        py = float(cy) * c[k] - float(cx) * s[k]
+        smin = min(smin, px - float(T[4 * k]), float(T[4 * k + 1]) - px,
+                   py - float(T[4 * k + 2]), float(T[4 * k + 3]) - py)
+    ac = abs(float(cx)) + abs(float(cy))
+    rho = smin * (1.0 - 2.0 ** -10) - ac * 2.0 ** -17 - 2.0 ** -100
+    if not rho > 0:
+        return cx, cy, np.float32(-1.0)
+    r2 = min(rho * rho * (1.0 - 2.0 ** -16), 2.0 ** 126)
+    f = np.float32(r2)
+    if float(f) > r2:
+        f = np.nextafter(f, np.float32(0))
+    return cx, cy, f
+
+
+@pytest.mark.parametrize("family", ["disk", "square", "gauss", "circle"])
+def test_k1_prescreen_is_conservative(L, oracle_lib, family):
+    """with thresholds T that are safe float roundings of real
+    extreme keys, every point the pre-screen rejects (float d2 < rho2) has
+    exact binary64 keys strictly worse than every threshold, so it can never be
+    an extreme.  Probed on points straddling the pre-screen circle."""
+    xy = synth.generate(family, 40_000, seed=17)
+    c, s = oracle_lib.coeffs("A")
+    _, keys = oracle_lib.extremes(xy, "A", with_keys=True)
+    # thresholds as the kernel holds them: max slots RD32, min slots RU32 of real keys
+    T = []
+    for k, v in enumerate(keys):
+        f = np.float32(v)
+        if k % 2 == 1 and float(f) > v:
+            f = np.nextafter(f, np.float32(-np.inf))
+        if k % 2 == 0 and float(f) < v:
+            f = np.nextafter(f, np.float32(np.inf))
+        T.append(f)
+    cx, cy, rho2 = _prescreen_params(T, c, s)
+    assert rho2 > 0
+    r = float(np.sqrt(np.float64(rho2)))
+    rng = np.random.default_rng(3)
+    th = rng.uniform(0, 2 * np.pi, 20_000)
+    f = rng.uniform(0.999, 1.001, 20_000)
+    pts = np.stack([float(cx) + f * r * np.cos(th), float(cy) + f * r * np.sin(th)], 1).astype(np.float32)
+    d = (pts - np.array([cx, cy], np.float32)).astype(np.float32)
+    d2 = (d[:, 0] * d[:, 0]).astype(np.float32) + (d[:, 1] * d[:, 1]).astype(np.float32)
+    rejected = pts[d2.astype(np.float32) < rho2]
+    assert len(rejected) > 1000
+    P = rejected.astype(np.float64)
+    for k in range(4):
+        X = P[:, 0] * c[k] + P[:, 1] * s[k]
+        Y = P[:, 1] * c[k] - P[:, 0] * s[k]
+        assert (X > float(T[4 * k])).all() and (X < float(T[4 * k + 1])).all()
+        assert (Y > float(T[4 * k + 2])).all() and (Y < float(T[4 * k + 3])).all()

@@ -238,3 +238,44 @@ def test_config_c5_2b_sampled():
         assert np.array_equal(surv[a:b], keep), lo
     frac = len(surv) / n
     assert 0.0330 < frac < 0.0345, frac            # closed form 3.384 % (reading A1)
+
+
+def test_nccl_group_path_under_torchrun():
+    """The multi-rank path of the public API (NCCL all-gather of the per-rank
+    Step-1 structs + host merge) on the GPUs this box has (torchrun, one
+    process per GPU), against the oracle on the whole set."""
+    import socket
+    import subprocess
+    import sys
+
+    ngpu = torch.cuda.device_count()
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    script = os.path.join(os.path.dirname(__file__), "scripts", "nccl_cudapre.py")
+    res = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                          f"--nproc-per-node={ngpu}", "--master-addr=127.0.0.1",
+                          f"--master-port={port}", script], capture_output=True, text=True,
+                         timeout=600)
+    assert res.returncode == 0, res.stdout[-2000:] + res.stderr[-4000:]
+    assert "nccl ok" in res.stdout
+
+
+def test_register_k2_fallback_matches():
+    """CUDAPRE_K2_TMA=0 routes 16-B aligned input through the register K2
+    kernel; it must give the same bytes (separate process: the switch is read
+    once per process)."""
+    import subprocess
+    import sys
+
+    code = ("import numpy as np, torch, oracle, synth, paper_1405_3454_b200 as cp\n"
+            "for fam, n in (('disk', 1000003), ('square', 400001), ('circle', 300007)):\n"
+            "    xy = synth.generate(fam, n, seed=3)\n"
+            "    idx, sp, rep = cp.cuda_pre(torch.from_numpy(xy).cuda())\n"
+            "    want = oracle.cudapre(xy, 'A', threads=8)\n"
+            "    assert np.array_equal(idx.cpu().numpy(), want['survivors']), fam\n"
+            "print('reg ok')\n")
+    env = dict(os.environ, CUDAPRE_K2_TMA="0")
+    res = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600,
+                         env=env, cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert res.returncode == 0 and "reg ok" in res.stdout, res.stderr[-3000:]
