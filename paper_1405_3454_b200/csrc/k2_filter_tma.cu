@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "k2_common.cuh"
 #include "tma.cuh"
@@ -28,9 +29,7 @@ namespace cudapre {
 namespace {
 
 constexpr int kW = kK2Threads / 32;                  // 8 warps
-constexpr int kNst = 4;                              // ring stages
 constexpr int kG = kK2Sub * kK2Items * kW;           // 256 ballot groups per super-tile
-constexpr unsigned kL = 128;                         // survivor list per warp per super-tile
 constexpr unsigned kNone = 0xffffffffu;
 constexpr unsigned kProd = kK2Threads - 32;          // producer thread: lane 0 of the last warp
 
@@ -39,6 +38,7 @@ struct SurvT {
     unsigned meta;   // (group << 6) | (owner lane << 1) | pair element
 };
 
+template <unsigned kL>
 struct TileT {
     unsigned mask[kG][2];   // keep ballots, group g = (sub*kK2Items + u)*kW + warp
     unsigned off[kG];       // exclusive offset of each group inside the super-tile
@@ -47,11 +47,12 @@ struct TileT {
     SurvT list[kW][kL];
 };
 
+template <int kNst, unsigned kL>
 struct SmemT {
     float4 ring[kNst][kK2SubPairs];
     unsigned long long full[kNst];
     unsigned long long empty[kNst];
-    TileT ts[2];
+    TileT<kL> ts[2];
     unsigned char qslot[kW][2 * kK2Items * 32];
     unsigned char own[kW][32];
     unsigned wsum[kW];
@@ -66,7 +67,8 @@ __device__ __forceinline__ unsigned entry_index(unsigned tbase, unsigned meta) {
     return 2u * q + h;
 }
 
-__device__ __forceinline__ void emit_t(const K2Params& p, const TileT& ts, unsigned tbase,
+template <unsigned kL>
+__device__ __forceinline__ void emit_t(const K2Params& p, const TileT<kL>& ts, unsigned tbase,
                                        unsigned long long ex, unsigned warp, unsigned lane,
                                        unsigned lt) {
     const unsigned wc = ts.wcnt[warp];
@@ -122,11 +124,19 @@ __device__ __forceinline__ unsigned sub_bytes(unsigned tile, unsigned sub, unsig
     return (np >= (unsigned)kK2SubPairs ? (unsigned)kK2SubPairs : np) * 16u;
 }
 
-template <int EDGES>
-__global__ void __launch_bounds__(kK2Threads, 2) k2_filter_tma(const __grid_constant__ K2Params p) {
+// CFG 0: 4-stage ring, 128-entry lists, 2 blocks/SM (default);
+// CFG 1: 3-stage ring, 64-entry lists, 3 blocks/SM (<= 85 registers).
+template <int CFG> struct K2Cfg;
+template <> struct K2Cfg<0> { static constexpr int kNst = 4; static constexpr unsigned kL = 128; static constexpr int kMinB = 2; };
+template <> struct K2Cfg<1> { static constexpr int kNst = 3; static constexpr unsigned kL = 64; static constexpr int kMinB = 3; };
+
+template <int EDGES, int CFG>
+__global__ void __launch_bounds__(kK2Threads, K2Cfg<CFG>::kMinB) k2_filter_tma(const __grid_constant__ K2Params p) {
     static_assert(kG == kK2Threads, "one scan entry per thread");
+    constexpr int kNst = K2Cfg<CFG>::kNst;
+    constexpr unsigned kL = K2Cfg<CFG>::kL;
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    SmemT& S = *reinterpret_cast<SmemT*>(smem_raw);
+    SmemT<kNst, kL>& S = *reinterpret_cast<SmemT<kNst, kL>*>(smem_raw);
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const unsigned lt = (1u << lane) - 1u;
     const unsigned epoch = *(volatile unsigned*)&p.ws->epoch;
@@ -176,22 +186,9 @@ __global__ void __launch_bounds__(kK2Threads, 2) k2_filter_tma(const __grid_cons
     unsigned pend = kNone;
     for (unsigned k = 0;; ++k) {
         const bool have = tile < p.num_tiles;
-        TileT& cur = S.ts[k & 1];
-        TileT& prv = S.ts[(k & 1) ^ 1];
+        TileT<kL>& cur = S.ts[k & 1];
+        TileT<kL>& prv = S.ts[(k & 1) ^ 1];
         const unsigned tbase = tile * kK2TilePairs;
-        // ---------------- resolve the pending super-tile (warp 0), overlapping
-        // the other warps' pass A (they run ahead up to the ring depth)
-        if (pend != kNone && warp == 0) {
-            unsigned long long ex = 0;
-            if (pend != 0) {
-                ex = resolve(p, pend, epoch, lane);
-                if (lane == 0) {
-                    publish(p, pend, kFlagP, ex + prv.total, epoch);
-                    if (pend == p.num_tiles - 1) p.ws->count = ex + prv.total;
-                }
-            }
-            if (lane == 0) S.prefix = ex;
-        }
         if (have) {
             // ---------------- pass A
             unsigned wc = 0;
@@ -305,10 +302,10 @@ __global__ void __launch_bounds__(kK2Threads, 2) k2_filter_tma(const __grid_cons
                 S.next = pnext;
             }
         }
-        __syncthreads();   // pass A done everywhere; S.prefix of the pending tile visible
+        __syncthreads();   // pass A done everywhere
         const unsigned next = have ? S.next : kNone;
         unsigned c = 0, inc = 0;
-        if (have) {   // block scan of the 256 group counts, phase 1
+        if (have) {   // block scan of the 256 group counts (group order = index order)
             c = __popc(cur.mask[threadIdx.x][0]) + __popc(cur.mask[threadIdx.x][1]);
             inc = c;
 #pragma unroll
@@ -318,10 +315,8 @@ __global__ void __launch_bounds__(kK2Threads, 2) k2_filter_tma(const __grid_cons
             }
             if (lane == 31) S.wsum[warp] = inc;
         }
-        // ---------------- pass B of the pending super-tile
-        if (pend != kNone) emit_t(p, prv, pend * kK2TilePairs, S.prefix, warp, lane, lt);
-        __syncthreads();   // prv free for the next pass A; wsum complete
-        if (have) {   // scan phase 2 + publish this tile's aggregate
+        __syncthreads();
+        if (have) {   // offsets + publish this tile's aggregate (tile 0: its prefix)
             unsigned wpre = 0, total = 0;
 #pragma unroll
             for (int w = 0; w < kW; ++w) {
@@ -340,6 +335,26 @@ __global__ void __launch_bounds__(kK2Threads, 2) k2_filter_tma(const __grid_cons
                 }
             }
         }
+        // ---------------- resolve + pass B of the pending super-tile: one
+        // tile-time after its aggregate was published, so its predecessors
+        // have published theirs (no spinning); the next super-tile's first
+        // sub-tiles are already in flight in the ring.
+        if (pend != kNone) {
+            if (warp == 0) {
+                unsigned long long ex = 0;
+                if (pend != 0) {
+                    ex = resolve(p, pend, epoch, lane);
+                    if (lane == 0) {
+                        publish(p, pend, kFlagP, ex + prv.total, epoch);
+                        if (pend == p.num_tiles - 1) p.ws->count = ex + prv.total;
+                    }
+                }
+                if (lane == 0) S.prefix = ex;
+            }
+            __syncthreads();
+            emit_t(p, prv, pend * kK2TilePairs, S.prefix, warp, lane, lt);
+        }
+        __syncthreads();   // prv is reused by the next pass A
         if (!have) break;
         pend = tile;
         tile = next;
@@ -363,28 +378,40 @@ __global__ void __launch_bounds__(kK2Threads, 2) k2_filter_tma(const __grid_cons
     }
 }
 
-template <int EDGES>
+template <int EDGES, int CFG>
 cudaError_t launch_tma_t(const K2Params& p, cudaStream_t s, int* launches) {
     static int max_blocks = 0;
-    const int smem = (int)sizeof(SmemT);
+    const int smem = (int)sizeof(SmemT<K2Cfg<CFG>::kNst, K2Cfg<CFG>::kL>);
     if (!max_blocks) {
-        cudaFuncSetAttribute(k2_filter_tma<EDGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(k2_filter_tma<EDGES, CFG>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2_filter_tma<EDGES>, kK2Threads, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2_filter_tma<EDGES, CFG>, kK2Threads, smem);
         max_blocks = (per_sm > 0 ? per_sm : 1) * device_sm_count();
     }
     unsigned blocks = p.num_tiles < (unsigned)max_blocks ? p.num_tiles : (unsigned)max_blocks;
     if (blocks < 1) blocks = 1;
-    k2_filter_tma<EDGES><<<blocks, kK2Threads, smem, s>>>(p);
+    k2_filter_tma<EDGES, CFG><<<blocks, kK2Threads, smem, s>>>(p);
     ++*launches;
     return cudaGetLastError();
+}
+
+int k2_cfg() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("CUDAPRE_K2_CFG");
+        v = e ? atoi(e) : 0;
+        if (v < 0 || v > 1) v = 0;
+    }
+    return v;
 }
 
 }  // namespace
 
 int launch_filter_tma(const K2Params& p, void* stream, int* launches) {
     cudaStream_t s = (cudaStream_t)stream;
-    return p.nv <= 16 ? (int)launch_tma_t<16>(p, s, launches) : (int)launch_tma_t<32>(p, s, launches);
+    if (k2_cfg() == 1)
+        return p.nv <= 16 ? (int)launch_tma_t<16, 1>(p, s, launches) : (int)launch_tma_t<32, 1>(p, s, launches);
+    return p.nv <= 16 ? (int)launch_tma_t<16, 0>(p, s, launches) : (int)launch_tma_t<32, 0>(p, s, launches);
 }
 
 }  // namespace cudapre
