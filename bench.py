@@ -210,7 +210,7 @@ def main():
     rep1 = cp.ReportT()
     for _ in range(args.warmup):
         step(rep1)
-    k1_ms, k2_ms, launches = [], [], 0
+    k1_ms, k2_ms, poly_ms, launches = [], [], [], 0
     surv = 0
     clocks = ClockSampler(torch.cuda.current_device())
     if group is not None:
@@ -223,6 +223,7 @@ def main():
             surv, rep2 = step(rep1)
             k1_ms.append(rep1.ms_extremes_kernels)
             k2_ms.append(rep2["ms_filter_kernel"])
+            poly_ms.append(rep2["ms_polygon_host"])
             launches += rep1.launches + rep2["launches"]
         end.record()
         torch.cuda.synchronize()
@@ -340,6 +341,7 @@ def main():
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": clocks.result(),
             "k1_exact_path_points_per_step": int(exact_pts[0]),
+            "host_step2_ms": round(statistics.median(poly_ms), 4),
         }
         print(json.dumps(line), flush=True)
     if group is not None:

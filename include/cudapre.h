@@ -50,6 +50,7 @@ extern "C" {
 
 #define CUDAPRE_MAX_ANGLES 8
 #define CUDAPRE_MAX_SLOTS (4 * CUDAPRE_MAX_ANGLES)
+#define CUDAPRE_SECTORS 1024   /* Step-3 sector buckets: pseudo-angle [0,4] x 256 */
 
 typedef enum {
     CUDAPRE_OK = 0,
@@ -102,6 +103,12 @@ typedef struct {
      * |float evaluation - exact orient(v_j, v_j+1, p)| over the exact data
      * bounding box.                                        */
     float A[CUDAPRE_MAX_SLOTS], B[CUDAPRE_MAX_SLOTS], C[CUDAPRE_MAX_SLOTS], E[CUDAPRE_MAX_SLOTS];
+    /* Step-3 sector test around the centre (circle[0], circle[1]): with
+     * (dx, dy) = RN32(p - c), t = dy / (|dx| + |dy|) and the pseudo-angle
+     * pa = t + 1 (dx >= 0) or 3 - t (dx < 0) in [0, 4], bucket
+     * b = round(256 pa); RN32(RN32(dx^2) + RN32(dy^2)) < sector_r2[b] implies p
+     * strictly inside the ring.  -1 = bucket disabled.      */
+    float sector_r2[CUDAPRE_SECTORS + 1];
 } cudapre_polygon_t;
 
 /* Per-call report (S:118-123 FilterReport; per-phase timings S:189). */

@@ -29,6 +29,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libcudapre.so")
 MAX_ANGLES = 8
 MAX_SLOTS = 32
+SECTORS = 1024
 
 OK, ERR_EMPTY, ERR_ARG, ERR_NONFINITE, ERR_CUDA, ERR_CAPACITY, ERR_WORKSPACE = range(7)
 _STATUS = {1: "EMPTY_INPUT", 2: "INVALID_ARGUMENT", 3: "NONFINITE_INPUT", 4: "CUDA",
@@ -60,7 +61,8 @@ class PolygonT(ctypes.Structure):
                 ("box", ctypes.c_float * 4), ("circle", ctypes.c_float * 4),
                 ("err_max", ctypes.c_float), ("pad", ctypes.c_int32),
                 ("A", ctypes.c_float * MAX_SLOTS), ("B", ctypes.c_float * MAX_SLOTS),
-                ("C", ctypes.c_float * MAX_SLOTS), ("E", ctypes.c_float * MAX_SLOTS)]
+                ("C", ctypes.c_float * MAX_SLOTS), ("E", ctypes.c_float * MAX_SLOTS),
+                ("sector_r2", ctypes.c_float * (SECTORS + 1))]
 
 
 class ReportT(ctypes.Structure):

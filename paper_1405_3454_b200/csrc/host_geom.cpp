@@ -88,6 +88,49 @@ bool strictly_inside_ring(const cudapre_pt* v, int nv, float px, float py) {
     return true;
 }
 
+// direction (unnormalised) of pseudo-angle pa (wrapped into [0, 4)):
+// pa in [0,2]: t = pa-1, (1-|t|, t);  pa in [2,4]: t = 3-pa, (-(1-|t|), t)
+void pa_dir(double pa, double& ux, double& uy) {   // pa in [-4, 8)
+    if (pa < 0.0) pa += 4.0;
+    if (pa >= 4.0) pa -= 4.0;
+    if (pa <= 2.0) {
+        const double t = pa - 1.0;
+        ux = 1.0 - std::fabs(t);
+        uy = t;
+    } else {
+        const double t = 3.0 - pa;
+        ux = -(1.0 - std::fabs(t));
+        uy = t;
+    }
+}
+double pa_of(double ux, double uy) {
+    const double t = uy / (std::fabs(ux) + std::fabs(uy));
+    return ux >= 0.0 ? t + 1.0 : 3.0 - t;
+}
+
+// The sector sample rays are fixed: pseudo-angles (k - 0.5 -+ 1/64)/256,
+// k = 0..1025 (wrapped into [0, 4)), with their unnormalised directions and
+// lengths; built once per process.
+struct SectorSamples {
+    static constexpr int kS = 2 * (CUDAPRE_SECTORS + 2);
+    double pa[kS], ux[kS], uy[kS], ul[kS];
+    SectorSamples() {
+        const double g = 1.0 / 64.0;
+        for (int i = 0; i < kS; ++i) {
+            double pw = ((double)(i >> 1) - 0.5 + ((i & 1) ? g : -g)) / 256.0;
+            if (pw < 0.0) pw += 4.0;
+            if (pw >= 4.0) pw -= 4.0;
+            pa[i] = pw;
+            pa_dir(pw, ux[i], uy[i]);
+            ul[i] = std::sqrt(ux[i] * ux[i] + uy[i] * uy[i]);
+        }
+    }
+};
+const SectorSamples& sector_samples() {
+    static const SectorSamples s;
+    return s;
+}
+
 }  // namespace
 
 int64_t hull_ring(const cudapre_pt* pts, const int64_t* ids, int64_t n, int64_t* ring) {
@@ -163,6 +206,7 @@ void build_polygon(const cudapre_extremes_t& ext, cudapre_polygon_t* poly, K2Par
     poly->box[2] = 1.0f;
     poly->box[3] = 0.0f;
     poly->circle[2] = -1.0f;
+    for (int b = 0; b <= CUDAPRE_SECTORS; ++b) poly->sector_r2[b] = -1.0f;
     if (kp) {
         kp->nv = nv;
         kp->mode = poly->degenerate ? 1 : 0;
@@ -170,6 +214,7 @@ void build_polygon(const cudapre_extremes_t& ext, cudapre_polygon_t* poly, K2Par
         kp->e2max = 0.0f;
         kp->ox = kp->oy = 0.0f;
         kp->r2 = -1.0f;
+        for (int b = 0; b <= CUDAPRE_SECTORS; ++b) kp->sr2[b] = -1.0f;
         for (int j = 0; j <= nv && j <= CUDAPRE_MAX_SLOTS; ++j) {
             kp->vx[j] = poly->v[j % (nv ? nv : 1)].x;
             kp->vy[j] = poly->v[j % (nv ? nv : 1)].y;
@@ -243,7 +288,7 @@ void build_polygon(const cudapre_extremes_t& ext, cudapre_polygon_t* poly, K2Par
     bool have = false;
     float best[4] = {1.0f, 0.0f, 1.0f, 0.0f};
     if (std::isfinite(ox) && std::isfinite(oy) && std::isfinite(hw) && std::isfinite(hh)) {
-        for (int it = 0; it < 40; ++it) {
+        for (int it = 0; it < 16; ++it) {
             const double t = (it == 0) ? 1.0 : 0.5 * (lo + hi);
             const float x0 = f_up(ox - t * hw), x1 = f_down(ox + t * hw);
             const float y0 = f_up(oy - t * hh), y1 = f_down(oy + t * hh);
@@ -294,14 +339,110 @@ void build_polygon(const cudapre_extremes_t& ext, cudapre_polygon_t* poly, K2Par
                 rmin = std::min(rmin, (num - err) / len * (1.0 - 0x1p-50));
             }
             const double r2 = rmin * rmin * (1.0 - 0x1p-16);
-            if (ok && r2 >= 0x1p-100 && r2 <= 0x1p100) {
-                poly->circle[0] = cx;
-                poly->circle[1] = cy;
-                poly->circle[2] = f_down(r2);
+            poly->circle[0] = cx;   // centre kept for the sector test even if the disk is off
+            poly->circle[1] = cy;
+            if (ok && r2 >= 0x1p-100 && r2 <= 0x1p100) poly->circle[2] = f_down(r2);
+        }
+    }
+    // ---- sector table: for bucket b = round(256 pa) the
+    //      radius^2 below which every point whose pseudo-angle lies in
+    //      [(b - 0.5 - g)/256, (b + 0.5 + g)/256] (guard g = 1/64 bucket) is
+    //      strictly inside.  Along one edge j the exit distance of the ray at
+    //      angle th is d_j / cos(th - phi_j) (d_j: rigorous lower bound of the
+    //      distance from the centre to the edge line, phi_j: outward normal),
+    //      convex in th with its minimum d_j at phi_j, so over a bucket
+    //      r_min = min(r(lower end), r(upper end), d_j for normals inside).
+    for (int b = 0; b <= CUDAPRE_SECTORS; ++b) poly->sector_r2[b] = -1.0f;
+    {
+        const float cx = poly->circle[0], cy = poly->circle[1];
+        bool ok = poly->circle[2] > 0.0f || (std::isfinite(cx) && std::isfinite(cy) &&
+                                              strictly_inside_ring(poly->v, nv, cx, cy));
+        double nx[CUDAPRE_MAX_SLOTS], ny[CUDAPRE_MAX_SLOTS], dj[CUDAPRE_MAX_SLOTS], pn[CUDAPRE_MAX_SLOTS];
+        for (int j = 0; j < nv && ok; ++j) {
+            const double ax = poly->v[j].x, ay = poly->v[j].y;
+            const double bx = poly->v[(j + 1) % nv].x, by = poly->v[(j + 1) % nv].y;
+            const double ex = bx - ax, ey = by - ay, px = cx - ax, py = cy - ay;
+            const double t1 = ex * py, t2 = ey * px;
+            const double num = t1 - t2, err = (std::fabs(t1) + std::fabs(t2)) * 0x1p-49;
+            const double len = std::sqrt(ex * ex + ey * ey);
+            if (!(num - err > 0.0) || !(len > 0.0) || !std::isfinite(len)) {
+                ok = false;
+                break;
+            }
+            dj[j] = (num - err) / (len * (1.0 + 0x1p-48));
+            nx[j] = ey / len;   // outward unit normal of a CCW ring
+            ny[j] = -ex / len;
+            pn[j] = pa_of(nx[j], ny[j]);
+        }
+        // Vertex pseudo-angles around the centre: the ray of pseudo-angle pa
+        // exits through edge j iff pa lies in [pv_j, pv_j+1] (cyclically).
+        // Rays are visited in increasing pa, so the exit edge only moves forward.
+        double pv[CUDAPRE_MAX_SLOTS + 1];
+        if (ok)
+            for (int j = 0; j < nv; ++j) pv[j] = pa_of((double)poly->v[j].x - cx, (double)poly->v[j].y - cy);
+        if (ok) {
+            const double g = 1.0 / 64.0;
+            double rb[CUDAPRE_SECTORS + 1];
+            // Exit distances of the rays at pseudo-angles (k - 0.5 -+ g)/256,
+            // k = 0..1025, visited in increasing order so the exit edge only
+            // moves forward; the exit edge and both neighbours are evaluated
+            // (robust at vertex directions).  Bucket b spans
+            // [(b-0.5-g), (b+0.5+g)]/256 -> min(rm[b], rp[b+1]).
+            const SectorSamples& SS = sector_samples();
+            constexpr int kS = SectorSamples::kS;
+            double rs[kS];
+            int cur = 0;
+            for (int k = 0; k < nv; ++k)   // start at the edge whose range holds pa = 4 - eps
+                if (pv[k] > pv[cur]) cur = k;
+            for (int i = 0; i < kS; ++i) {
+                const double pw = SS.pa[i];
+                for (int steps = 0; steps < nv; ++steps) {   // advance to the edge holding pw
+                    const int cn = cur + 1 == nv ? 0 : cur + 1;
+                    double e0 = pv[cur], e1 = pv[cn], q = pw;
+                    if (e1 < e0) e1 += 4.0;
+                    if (q < e0) q += 4.0;
+                    if (q <= e1) break;
+                    cur = cn;
+                }
+                // min over the exit edge and its neighbours of dj / c (c > 0), by
+                // cross-multiplication; one division at the end
+                double bn = INFINITY, bd = 1.0;
+                const int nb[3] = {cur == 0 ? nv - 1 : cur - 1, cur, cur + 1 == nv ? 0 : cur + 1};
+                for (int dd = 0; dd < 3; ++dd) {
+                    const int j = nb[dd];
+                    const double c = nx[j] * SS.ux[i] + ny[j] * SS.uy[i];
+                    if (c > 0.0 && dj[j] * bd < bn * c) {
+                        bn = dj[j];
+                        bd = c;
+                    }
+                }
+                rs[i] = bn / bd * SS.ul[i];
+            }
+            for (int b = 0; b <= CUDAPRE_SECTORS; ++b) rb[b] = std::min(rs[2 * b], rs[2 * (b + 1) + 1]);
+            // edge normals: the minimum d_j of edge j is attained at its normal
+            for (int j = 0; j < nv; ++j) {
+                const double c = pn[j] * 256.0;   // bucket coordinate of the normal
+                for (int b = (int)std::floor(c - 0.5 - g) - 1; b <= (int)std::ceil(c + 0.5 + g) + 1; ++b) {
+                    for (int w = -1; w <= 1; ++w) {   // wrap: buckets 0 and 1024 overlap at pa = 0 / 4
+                        const int bb = b + w * 1024;
+                        if (bb < 0 || bb > CUDAPRE_SECTORS) continue;
+                        const double lo = (bb - 0.5 - g) / 256.0, hi = (bb + 0.5 + g) / 256.0;
+                        for (int w2 = -1; w2 <= 1; ++w2) {
+                            const double q = pn[j] + 4.0 * w2;
+                            if (q >= lo && q <= hi) rb[bb] = std::min(rb[bb], dj[j]);
+                        }
+                    }
+                }
+            }
+            for (int b = 0; b <= CUDAPRE_SECTORS; ++b) {
+                const double r = rb[b] * (1.0 - 0x1p-30);
+                const double r2 = r * r * (1.0 - 0x1p-16);
+                if (r2 >= 0x1p-100 && r2 <= 0x1p100) poly->sector_r2[b] = f_down(r2);
             }
         }
     }
     if (kp) {
+        for (int b = 0; b <= CUDAPRE_SECTORS; ++b) kp->sr2[b] = poly->sector_r2[b];
         kp->ox = poly->circle[0];
         kp->oy = poly->circle[1];
         kp->r2 = poly->circle[2];

@@ -55,10 +55,32 @@ struct SmemT {
     TileT<kL> ts[2];
     unsigned char qslot[kW][2 * kK2Items * 32];
     unsigned char own[kW][32];
+    float sr2[CUDAPRE_SECTORS + 1];   // sector radii^2 (copied from the parameters)
     unsigned wsum[kW];
     unsigned next;
     unsigned long long prefix;
 };
+
+// Sector test: pseudo-angle bucket of p around (ox, oy) by
+// one approximate reciprocal; strictly inside if |p - o|^2 < sr2[bucket].
+// The host's buckets carry a 1/64-bucket guard band, far above the bucket
+// error of this arithmetic (< 2^-12 bucket); NaN/Inf map to a clamped bucket
+// and fail the comparison.
+__device__ __forceinline__ float rcp_approx(float a) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(a));
+    return r;
+}
+__device__ __forceinline__ bool sector_inside(const float* sr2, float x, float y, float ox, float oy) {
+    const float2 d = __fadd2_rn(make_float2(x, y), make_float2(-ox, -oy));
+    const float2 q = __fmul2_rn(d, d);
+    const float d2 = __fadd_rn(q.x, q.y);
+    const float t = __fmul_rn(d.y, rcp_approx(__fadd_rn(fabsf(d.x), fabsf(d.y))));
+    const bool pos = d.x >= 0.0f;
+    const float v = __fmaf_rn(t, pos ? 256.0f : -256.0f, pos ? 8388864.0f : 8389376.0f);   // 2^23 + 256 pa
+    const unsigned b = min(__float_as_uint(v) - 0x4B000000u, (unsigned)CUDAPRE_SECTORS);
+    return d2 < sr2[b];
+}
 
 // global point index of a survivor entry
 __device__ __forceinline__ unsigned entry_index(unsigned tbase, unsigned meta) {
@@ -171,6 +193,8 @@ __global__ void __launch_bounds__(kK2Threads, K2Cfg<CFG>::kMinB) k2_filter_tma(c
         }
     };
 
+    const float ox = p.ox, oy = p.oy;
+    for (int i = threadIdx.x; i <= CUDAPRE_SECTORS; i += kK2Threads) S.sr2[i] = p.sr2[i];
     if (threadIdx.x == kProd) {
         for (int k = 0; k < kNst; ++k) {
             mbar_init(&S.full[k], 1u);
@@ -206,7 +230,8 @@ __global__ void __launch_bounds__(kK2Threads, K2Cfg<CFG>::kMinB) k2_filter_tma(c
 #pragma unroll
                     for (int u = 0; u < kK2Items; ++u) {
                         const float4 v = stg[u * kK2Threads + threadIdx.x];
-                        const unsigned in = (fast_inside(p, v.x, v.y) ? 1u : 0u) | (fast_inside(p, v.z, v.w) ? 2u : 0u);
+                        const unsigned in = (sector_inside(S.sr2, v.x, v.y, ox, oy) ? 1u : 0u) |
+                                            (sector_inside(S.sr2, v.z, v.w, ox, oy) ? 2u : 0u);
                         needy |= (3u & ~in) << (2 * u);
                     }
                 } else {   // last super-tile only: ragged end
@@ -224,7 +249,8 @@ __global__ void __launch_bounds__(kK2Threads, K2Cfg<CFG>::kMinB) k2_filter_tma(c
                             v = make_float4(a.x, a.y, 0.f, 0.f);
                             valid = 1u;
                         }
-                        const unsigned in = (fast_inside(p, v.x, v.y) ? 1u : 0u) | (fast_inside(p, v.z, v.w) ? 2u : 0u);
+                        const unsigned in = (sector_inside(S.sr2, v.x, v.y, ox, oy) ? 1u : 0u) |
+                                            (sector_inside(S.sr2, v.z, v.w, ox, oy) ? 2u : 0u);
                         needy |= (valid & ~in) << (2 * u);
                     }
                 }

@@ -47,7 +47,7 @@ def test_exports_every_declared_symbol(L):
 def test_struct_sizes_match_header(L):
     # offsets derived from the C layout rules of include/cudapre.h
     assert ctypes.sizeof(cp.ExtremesT) == 8 + 8 + 32 * 8 + 32 * 8 + 32 * 8 + 8 * 8 + 8 * 8 + 8
-    assert ctypes.sizeof(cp.PolygonT) == 16 + 32 * 8 + 32 * 8 + 16 + 16 + 8 + 4 * 32 * 4
+    assert ctypes.sizeof(cp.PolygonT) == 16 + 32 * 8 + 32 * 8 + 16 + 16 + 8 + 4 * 32 * 4 + 4 * 1025 + 4
     assert ctypes.sizeof(cp.ReportT) == 48
 
 
@@ -324,3 +324,41 @@ def test_k1_prescreen_is_conservative(L, oracle_lib, family):
         Y = P[:, 1] * c[k] - P[:, 0] * s[k]
         assert (X > float(T[4 * k])).all() and (X < float(T[4 * k + 1])).all()
         assert (Y > float(T[4 * k + 2])).all() and (Y < float(T[4 * k + 3])).all()
+
+
+@pytest.mark.parametrize("family", ["disk", "square", "gauss", "circle"])
+def test_k2_sector_table_is_conservative(L, oracle_lib, family):
+    """every probe the kernel's sector test accepts
+    (RN32(RN32(dx^2)+RN32(dy^2)) < sector_r2[round(256 pa)], pa = pseudo-angle
+    of RN32(p - c)) is strictly inside the ring by the exact predicate; probes
+    sit at radius sqrt(sector_r2) * (1 +- a few ulp) in every bucket."""
+    import time
+
+    xy = synth.generate(family, 50_000, seed=29)
+    ext = _ext_from_oracle(oracle_lib, xy)
+    t0 = time.perf_counter()
+    poly = cp.polygon(cp.Extremes(ext))
+    dt = time.perf_counter() - t0
+    assert dt < 0.05, dt                                  # host Step 2 stays cheap
+    sr2 = np.frombuffer(poly.raw.sector_r2, np.float32)
+    ox, oy = np.float32(poly.circle[0]), np.float32(poly.circle[1])
+    assert (sr2 > 0).all()
+    V = poly.v
+    rng = np.random.default_rng(7)
+    pa = rng.uniform(0, 4, 6000)
+    t = np.where(pa <= 2, pa - 1, 3 - pa)
+    ux = np.where(pa <= 2, 1 - np.abs(t), -(1 - np.abs(t)))
+    u = np.stack([ux, t], 1) / np.hypot(ux, t)[:, None]
+    b0 = np.clip(np.round(256 * pa).astype(int), 0, 1024)
+    f = rng.choice([1 - 1e-6, 1 - 1e-7, 1.0, 1 + 1e-7], len(pa))
+    r = np.sqrt(sr2[b0].astype(np.float64)) * f
+    pts = (np.array([ox, oy], np.float64) + r[:, None] * u).astype(np.float32)
+    d = (pts - np.array([ox, oy], np.float32)).astype(np.float32)
+    d2 = (d[:, 0] * d[:, 0]).astype(np.float32) + (d[:, 1] * d[:, 1]).astype(np.float32)
+    tt = d[:, 1].astype(np.float64) / (np.abs(d[:, 0]).astype(np.float64) + np.abs(d[:, 1]))
+    pe = np.where(d[:, 0] >= 0, tt + 1, 3 - tt)
+    b = np.clip(np.round(256 * pe).astype(int), 0, 1024)
+    acc = d2.astype(np.float32) < sr2[b]
+    assert acc.sum() > 1000
+    for p in pts[acc][:1500]:
+        assert brute.strictly_inside_frac(V, p), (family, p)
