@@ -107,8 +107,11 @@ typedef struct {
      * (dx, dy) = RN32(p - c), t = dy / (|dx| + |dy|) and the pseudo-angle
      * pa = t + 1 (dx >= 0) or 3 - t (dx < 0) in [0, 4], bucket
      * b = round(256 pa); RN32(RN32(dx^2) + RN32(dy^2)) < sector_r2[b] implies p
-     * strictly inside the ring.  -1 = bucket disabled.      */
+     * strictly inside the ring.  -1 = bucket disabled.
+     * sector_out_r2[b]: RN32(...) > sector_out_r2[b] implies p strictly
+     * outside the ring (+inf = disabled).                                  */
     float sector_r2[CUDAPRE_SECTORS + 1];
+    float sector_out_r2[CUDAPRE_SECTORS + 1];
 } cudapre_polygon_t;
 
 /* Per-call report (S:118-123 FilterReport; per-phase timings S:189). */

@@ -62,7 +62,8 @@ class PolygonT(ctypes.Structure):
                 ("err_max", ctypes.c_float), ("pad", ctypes.c_int32),
                 ("A", ctypes.c_float * MAX_SLOTS), ("B", ctypes.c_float * MAX_SLOTS),
                 ("C", ctypes.c_float * MAX_SLOTS), ("E", ctypes.c_float * MAX_SLOTS),
-                ("sector_r2", ctypes.c_float * (SECTORS + 1))]
+                ("sector_r2", ctypes.c_float * (SECTORS + 1)),
+                ("sector_out_r2", ctypes.c_float * (SECTORS + 1))]
 
 
 class ReportT(ctypes.Structure):

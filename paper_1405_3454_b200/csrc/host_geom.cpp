@@ -206,7 +206,10 @@ void build_polygon(const cudapre_extremes_t& ext, cudapre_polygon_t* poly, K2Par
     poly->box[2] = 1.0f;
     poly->box[3] = 0.0f;
     poly->circle[2] = -1.0f;
-    for (int b = 0; b <= CUDAPRE_SECTORS; ++b) poly->sector_r2[b] = -1.0f;
+    for (int b = 0; b <= CUDAPRE_SECTORS; ++b) {
+        poly->sector_r2[b] = -1.0f;
+        poly->sector_out_r2[b] = INFINITY;
+    }
     if (kp) {
         kp->nv = nv;
         kp->mode = poly->degenerate ? 1 : 0;
@@ -214,7 +217,10 @@ void build_polygon(const cudapre_extremes_t& ext, cudapre_polygon_t* poly, K2Par
         kp->e2max = 0.0f;
         kp->ox = kp->oy = 0.0f;
         kp->r2 = -1.0f;
-        for (int b = 0; b <= CUDAPRE_SECTORS; ++b) kp->sr2[b] = -1.0f;
+        for (int b = 0; b <= CUDAPRE_SECTORS; ++b) {
+            kp->sr2[b] = -1.0f;
+            kp->sro2[b] = INFINITY;
+        }
         for (int j = 0; j <= nv && j <= CUDAPRE_MAX_SLOTS; ++j) {
             kp->vx[j] = poly->v[j % (nv ? nv : 1)].x;
             kp->vy[j] = poly->v[j % (nv ? nv : 1)].y;
@@ -352,12 +358,16 @@ void build_polygon(const cudapre_extremes_t& ext, cudapre_polygon_t* poly, K2Par
     //      distance from the centre to the edge line, phi_j: outward normal),
     //      convex in th with its minimum d_j at phi_j, so over a bucket
     //      r_min = min(r(lower end), r(upper end), d_j for normals inside).
-    for (int b = 0; b <= CUDAPRE_SECTORS; ++b) poly->sector_r2[b] = -1.0f;
+    for (int b = 0; b <= CUDAPRE_SECTORS; ++b) {
+        poly->sector_r2[b] = -1.0f;
+        poly->sector_out_r2[b] = INFINITY;
+    }
     {
         const float cx = poly->circle[0], cy = poly->circle[1];
         bool ok = poly->circle[2] > 0.0f || (std::isfinite(cx) && std::isfinite(cy) &&
                                               strictly_inside_ring(poly->v, nv, cx, cy));
         double nx[CUDAPRE_MAX_SLOTS], ny[CUDAPRE_MAX_SLOTS], dj[CUDAPRE_MAX_SLOTS], pn[CUDAPRE_MAX_SLOTS];
+        double rs_up = 1.0;   // max over edges of (upper bound of dj) / (lower bound of dj)
         for (int j = 0; j < nv && ok; ++j) {
             const double ax = poly->v[j].x, ay = poly->v[j].y;
             const double bx = poly->v[(j + 1) % nv].x, by = poly->v[(j + 1) % nv].y;
@@ -370,6 +380,7 @@ void build_polygon(const cudapre_extremes_t& ext, cudapre_polygon_t* poly, K2Par
                 break;
             }
             dj[j] = (num - err) / (len * (1.0 + 0x1p-48));
+            rs_up = std::max(rs_up, ((num + err) * (1.0 + 0x1p-48)) / (num - err));
             nx[j] = ey / len;   // outward unit normal of a CCW ring
             ny[j] = -ex / len;
             pn[j] = pa_of(nx[j], ny[j]);
@@ -419,6 +430,32 @@ void build_polygon(const cudapre_extremes_t& ext, cudapre_polygon_t* poly, K2Par
                 rs[i] = bn / bd * SS.ul[i];
             }
             for (int b = 0; b <= CUDAPRE_SECTORS; ++b) rb[b] = std::min(rs[2 * b], rs[2 * (b + 1) + 1]);
+            // outer bound: r(th) is maximal at the interval ends or at a vertex
+            // inside it; dj is a LOWER bound of the line distance, so the ray
+            // distances are recomputed from an upper bound of dj
+            double ro[CUDAPRE_SECTORS + 1];
+            for (int b = 0; b <= CUDAPRE_SECTORS; ++b)
+                ro[b] = std::max(rs[2 * b], rs[2 * (b + 1) + 1]) * rs_up;
+            for (int j = 0; j < nv; ++j) {   // vertices inside a bucket
+                const double vx = (double)poly->v[j].x - cx, vy = (double)poly->v[j].y - cy;
+                const double vr = std::sqrt(vx * vx + vy * vy) * (1.0 + 0x1p-40);
+                const double c = pv[j] * 256.0;
+                for (int b = (int)std::floor(c - 0.5 - g) - 1; b <= (int)std::ceil(c + 0.5 + g) + 1; ++b)
+                    for (int w = -1; w <= 1; ++w) {
+                        const int bb = b + w * 1024;
+                        if (bb < 0 || bb > CUDAPRE_SECTORS) continue;
+                        const double lo = (bb - 0.5 - g) / 256.0, hi = (bb + 0.5 + g) / 256.0;
+                        for (int w2 = -1; w2 <= 1; ++w2) {
+                            const double q = pv[j] + 4.0 * w2;
+                            if (q >= lo && q <= hi) ro[bb] = std::max(ro[bb], vr);
+                        }
+                    }
+            }
+            for (int b = 0; b <= CUDAPRE_SECTORS; ++b) {
+                const double r = ro[b] * (1.0 + 0x1p-30);
+                const double r2 = r * r * (1.0 + 0x1p-16);
+                if (r2 >= 0x1p-100 && r2 <= 0x1p100) poly->sector_out_r2[b] = f_up(r2);
+            }
             // edge normals: the minimum d_j of edge j is attained at its normal
             for (int j = 0; j < nv; ++j) {
                 const double c = pn[j] * 256.0;   // bucket coordinate of the normal
@@ -442,7 +479,10 @@ void build_polygon(const cudapre_extremes_t& ext, cudapre_polygon_t* poly, K2Par
         }
     }
     if (kp) {
-        for (int b = 0; b <= CUDAPRE_SECTORS; ++b) kp->sr2[b] = poly->sector_r2[b];
+        for (int b = 0; b <= CUDAPRE_SECTORS; ++b) {
+            kp->sr2[b] = poly->sector_r2[b];
+            kp->sro2[b] = poly->sector_out_r2[b];
+        }
         kp->ox = poly->circle[0];
         kp->oy = poly->circle[1];
         kp->r2 = poly->circle[2];

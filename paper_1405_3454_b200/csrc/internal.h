@@ -91,7 +91,8 @@ struct K2Params {
     float e2max;              // 2 * max_j E_j
     float A[CUDAPRE_MAX_SLOTS], B[CUDAPRE_MAX_SLOTS], C[CUDAPRE_MAX_SLOTS];   // C already lowered by E_j
     float vx[CUDAPRE_MAX_SLOTS + 1], vy[CUDAPRE_MAX_SLOTS + 1];               // ring, v[nv] = v[0]
-    float sr2[CUDAPRE_SECTORS + 1];   // sector radii^2 around (ox, oy) (TMA kernel; -1 = off)
+    float sr2[CUDAPRE_SECTORS + 1];    // sector inner radii^2 around (ox, oy) (-1 = off)
+    float sro2[CUDAPRE_SECTORS + 1];   // sector outer radii^2 (+inf = off)
 };
 
 // ---------------------------------------------------------------- launchers (.cu)

@@ -55,7 +55,8 @@ struct SmemT {
     TileT<kL> ts[2];
     unsigned char qslot[kW][2 * kK2Items * 32];
     unsigned char own[kW][32];
-    float sr2[CUDAPRE_SECTORS + 1];   // sector radii^2 (copied from the parameters)
+    float sr2[CUDAPRE_SECTORS + 1];    // sector inner radii^2 (copied from the parameters)
+    float sro2[CUDAPRE_SECTORS + 1];   // sector outer radii^2
     unsigned wsum[kW];
     unsigned next;
     unsigned long long prefix;
@@ -71,7 +72,9 @@ __device__ __forceinline__ float rcp_approx(float a) {
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(a));
     return r;
 }
-__device__ __forceinline__ bool sector_inside(const float* sr2, float x, float y, float ox, float oy) {
+// 0 = strictly inside, 1 = strictly outside, 2 = undecided
+__device__ __forceinline__ int sector_class(const float* sr2, const float* sro2, float x, float y,
+                                            float ox, float oy) {
     const float2 d = __fadd2_rn(make_float2(x, y), make_float2(-ox, -oy));
     const float2 q = __fmul2_rn(d, d);
     const float d2 = __fadd_rn(q.x, q.y);
@@ -79,7 +82,7 @@ __device__ __forceinline__ bool sector_inside(const float* sr2, float x, float y
     const bool pos = d.x >= 0.0f;
     const float v = __fmaf_rn(t, pos ? 256.0f : -256.0f, pos ? 8388864.0f : 8389376.0f);   // 2^23 + 256 pa
     const unsigned b = min(__float_as_uint(v) - 0x4B000000u, (unsigned)CUDAPRE_SECTORS);
-    return d2 < sr2[b];
+    return d2 < sr2[b] ? 0 : (d2 > sro2[b] ? 1 : 2);
 }
 
 // global point index of a survivor entry
@@ -194,7 +197,10 @@ __global__ void __launch_bounds__(kK2Threads, K2Cfg<CFG>::kMinB) k2_filter_tma(c
     };
 
     const float ox = p.ox, oy = p.oy;
-    for (int i = threadIdx.x; i <= CUDAPRE_SECTORS; i += kK2Threads) S.sr2[i] = p.sr2[i];
+    for (int i = threadIdx.x; i <= CUDAPRE_SECTORS; i += kK2Threads) {
+        S.sr2[i] = p.sr2[i];
+        S.sro2[i] = p.sro2[i];
+    }
     if (threadIdx.x == kProd) {
         for (int k = 0; k < kNst; ++k) {
             mbar_init(&S.full[k], 1u);
@@ -230,8 +236,7 @@ __global__ void __launch_bounds__(kK2Threads, K2Cfg<CFG>::kMinB) k2_filter_tma(c
 #pragma unroll
                     for (int u = 0; u < kK2Items; ++u) {
                         const float4 v = stg[u * kK2Threads + threadIdx.x];
-                        const unsigned in = (sector_inside(S.sr2, v.x, v.y, ox, oy) ? 1u : 0u) |
-                                            (sector_inside(S.sr2, v.z, v.w, ox, oy) ? 2u : 0u);
+                        const unsigned in = (fast_inside(p, v.x, v.y) ? 1u : 0u) | (fast_inside(p, v.z, v.w) ? 2u : 0u);
                         needy |= (3u & ~in) << (2 * u);
                     }
                 } else {   // last super-tile only: ragged end
@@ -249,8 +254,7 @@ __global__ void __launch_bounds__(kK2Threads, K2Cfg<CFG>::kMinB) k2_filter_tma(c
                             v = make_float4(a.x, a.y, 0.f, 0.f);
                             valid = 1u;
                         }
-                        const unsigned in = (sector_inside(S.sr2, v.x, v.y, ox, oy) ? 1u : 0u) |
-                                            (sector_inside(S.sr2, v.z, v.w, ox, oy) ? 2u : 0u);
+                        const unsigned in = (fast_inside(p, v.x, v.y) ? 1u : 0u) | (fast_inside(p, v.z, v.w) ? 2u : 0u);
                         needy |= (valid & ~in) << (2 * u);
                     }
                 }
@@ -288,7 +292,8 @@ __global__ void __launch_bounds__(kK2Threads, K2Cfg<CFG>::kMinB) k2_filter_tma(c
                             } else {   // the unpaired last point
                                 q = __ldg(reinterpret_cast<const float2*>(p.pts) + 2u * (qs + pr));
                             }
-                            kp = queue_keep<EDGES>(p, q.x, q.y);
+                            const int sc = sector_class(S.sr2, S.sro2, q.x, q.y, ox, oy);
+                            kp = sc == 1 || (sc == 2 && queue_keep<EDGES>(p, q.x, q.y));
                         }
                         const unsigned kb = __ballot_sync(kFull, kp);
                         if (kp) {

@@ -47,7 +47,7 @@ def test_exports_every_declared_symbol(L):
 def test_struct_sizes_match_header(L):
     # offsets derived from the C layout rules of include/cudapre.h
     assert ctypes.sizeof(cp.ExtremesT) == 8 + 8 + 32 * 8 + 32 * 8 + 32 * 8 + 8 * 8 + 8 * 8 + 8
-    assert ctypes.sizeof(cp.PolygonT) == 16 + 32 * 8 + 32 * 8 + 16 + 16 + 8 + 4 * 32 * 4 + 4 * 1025 + 4
+    assert ctypes.sizeof(cp.PolygonT) == 16 + 32 * 8 + 32 * 8 + 16 + 16 + 8 + 4 * 32 * 4 + 2 * 4 * 1025
     assert ctypes.sizeof(cp.ReportT) == 48
 
 
@@ -362,3 +362,18 @@ def test_k2_sector_table_is_conservative(L, oracle_lib, family):
     assert acc.sum() > 1000
     for p in pts[acc][:1500]:
         assert brute.strictly_inside_frac(V, p), (family, p)
+    # outer table: probes just beyond sqrt(sector_out_r2) classified "outside"
+    # must not be strictly inside (the kernel keeps them without edge tests)
+    so2 = np.frombuffer(poly.raw.sector_out_r2, np.float32)
+    assert np.isfinite(so2).all() and (so2 >= sr2).all()
+    r = np.sqrt(so2[b0].astype(np.float64)) * rng.choice([1 + 1e-6, 1 + 1e-7, 1.0, 1 - 1e-7], len(pa))
+    pts = (np.array([ox, oy], np.float64) + r[:, None] * u).astype(np.float32)
+    d = (pts - np.array([ox, oy], np.float32)).astype(np.float32)
+    d2 = (d[:, 0] * d[:, 0]).astype(np.float32) + (d[:, 1] * d[:, 1]).astype(np.float32)
+    tt = d[:, 1].astype(np.float64) / (np.abs(d[:, 0]).astype(np.float64) + np.abs(d[:, 1]))
+    pe = np.where(d[:, 0] >= 0, tt + 1, 3 - tt)
+    b = np.clip(np.round(256 * pe).astype(int), 0, 1024)
+    out = d2.astype(np.float32) > so2[b]
+    assert out.sum() > 1000
+    for p in pts[out][:1500]:
+        assert not brute.strictly_inside_frac(V, p), (family, p)
