@@ -211,6 +211,7 @@ def main():
     for _ in range(args.warmup):
         step(rep1)
     k1_ms, k2_ms, poly_ms, launches = [], [], [], 0
+    lb_rounds = [0, 0]
     surv = 0
     clocks = ClockSampler(torch.cuda.current_device())
     if group is not None:
@@ -224,6 +225,7 @@ def main():
             k1_ms.append(rep1.ms_extremes_kernels)
             k2_ms.append(rep2["ms_filter_kernel"])
             poly_ms.append(rep2["ms_polygon_host"])
+            lb_rounds[:] = [rep2["lookback_rounds"], rep2["lookback_spins"]]
             launches += rep1.launches + rep2["launches"]
         end.record()
         torch.cuda.synchronize()
@@ -342,6 +344,7 @@ def main():
             "gpu_launches": launches, "clocks": clocks.result(),
             "k1_exact_path_points_per_step": int(exact_pts[0]),
             "host_step2_ms": round(statistics.median(poly_ms), 4),
+            "k2_lookback_rounds_per_step": int(lb_rounds[0]), "k2_lookback_spins_per_step": int(lb_rounds[1]),
         }
         print(json.dumps(line), flush=True)
     if group is not None:

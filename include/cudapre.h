@@ -123,6 +123,9 @@ typedef struct {
     double ms_polygon_host;              /* host time of Step 2 */
     int32_t launches;                    /* kernels launched by the call */
     int32_t pad;
+    int64_t lookback_rounds;             /* Step-3 look-back rounds (256 status words each),
+                                          * counted since the last Step-1 call on the workspace */
+    int64_t lookback_spins;              /* of which had to wait for a predecessor */
 } cudapre_report_t;
 
 /* ---------------------------------------------------------------- helpers */

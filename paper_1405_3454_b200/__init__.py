@@ -70,7 +70,8 @@ class ReportT(ctypes.Structure):
     _fields_ = [("n", ctypes.c_int64), ("survivors", ctypes.c_int64),
                 ("ms_extremes_kernels", ctypes.c_double), ("ms_filter_kernel", ctypes.c_double),
                 ("ms_polygon_host", ctypes.c_double), ("launches", ctypes.c_int32),
-                ("pad", ctypes.c_int32)]
+                ("pad", ctypes.c_int32), ("lookback_rounds", ctypes.c_int64),
+                ("lookback_spins", ctypes.c_int64)]
 
 
 EXTREMES_BYTES = ctypes.sizeof(ExtremesT)
@@ -349,7 +350,8 @@ def filter(pts, ext: Extremes, index_base: int = 0, return_points: bool = True, 
     return (out_idx[:m], out_pts[:m] if out_pts is not None else None,
             {"n": n, "survivors": m, "polygon": Polygon(poly),
              "ms_filter_kernel": rep.ms_filter_kernel, "ms_polygon_host": rep.ms_polygon_host,
-             "launches": rep.launches})
+             "launches": rep.launches, "lookback_rounds": rep.lookback_rounds,
+             "lookback_spins": rep.lookback_spins})
 
 
 # ------------------------------------------------------------------ final hull

@@ -321,6 +321,10 @@ cudapre_status cudapre_filter(const cudapre_pt* d_pts, int64_t n_local, int64_t 
     p.status = ws_status(d_ws);
     p.num_tiles = (unsigned)((n_local + kK2TilePts - 1) / kK2TilePts);   // the TMA launcher re-derives its own
     const int vec16 = (((uintptr_t)d_pts & 15u) == 0);
+    {
+        const char* e = getenv("CUDAPRE_K2_DEBUG");   // perf experiments only: wrong results
+        p.debug = e ? atoi(e) : 0;
+    }
 
     cudaEvent_t* ev = nullptr;
     if (h_rep) {
@@ -334,10 +338,14 @@ cudapre_status cudapre_filter(const cudapre_pt* d_pts, int64_t n_local, int64_t 
     void* stage = nullptr;
     st = staging(&stage);
     if (st) return st;
-    CUDA_TRY(cudaMemcpyAsync(stage, &p.ws->count, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
-                             strm));
+    CUDA_TRY(cudaMemcpyAsync(stage, &p.ws->count, 16, cudaMemcpyDeviceToHost, strm));   // count + stats
     CUDA_TRY(cudaStreamSynchronize(strm));
     const int64_t count = (int64_t) * reinterpret_cast<unsigned long long*>(stage);
+    const unsigned* lb = reinterpret_cast<const unsigned*>(reinterpret_cast<const char*>(stage) + 8);
+    if (h_rep) {
+        h_rep->lookback_rounds = lb[0];
+        h_rep->lookback_spins = lb[1];
+    }
     *h_count = count;
     if (h_rep) {
         float ms = 0.f;

@@ -37,7 +37,8 @@ struct alignas(16) WsHeader {
     unsigned int epoch;          // K2 tile-status epoch (never 0 after the first call)
     unsigned int pad0[2];
     unsigned long long count;    // K2 survivors (written by the last tile)
-    unsigned long long pad1;
+    unsigned int lb_rounds;      // K2 look-back rounds (diagnostic; copied with count)
+    unsigned int lb_spins;       // K2 look-back rounds that waited
     unsigned int seed[CUDAPRE_MAX_SLOTS];   // seed thresholds, order-preserving encoding, 0 = none
     cudapre_extremes_t result;   // K1 final result
 };
@@ -86,6 +87,7 @@ struct K2Params {
     unsigned long long* status;   // ntiles tile-status words
     unsigned int num_tiles;
     int mode;                 // 0 = filter, 1 = keep everything (degenerate), 2 = exact only
+    int debug;                // perf experiments only (CUDAPRE_K2_DEBUG): 1 = skeleton, no classification
     float bx0, bx1, by0, by1; // inner box (closed), strictly inside the ring
     float ox, oy, r2;         // inner disk: RN(RN(dx^2)+RN(dy^2)) < r2 => strictly inside (r2 < 0: off)
     float e2max;              // 2 * max_j E_j

@@ -618,6 +618,8 @@ __global__ void __launch_bounds__(kK1Threads, 2) k1_extremes(const K1Params p) {
             p.ws->k1_ticket = 0u;
             p.ws->k1_nonfinite = 0u;
             p.ws->k1_exact = 0u;
+            p.ws->lb_rounds = 0u;   // Step-3 diagnostics count from here
+            p.ws->lb_spins = 0u;
         }
     }
 }

@@ -129,7 +129,9 @@ __device__ __forceinline__ unsigned long long resolve(const K2Params& p, unsigne
         const unsigned imask = __ballot_sync(kFull, inval);
         const unsigned lim = pmask ? (unsigned)(__ffs(pmask) - 1) : 31u;
         const unsigned need = (lim == 31u) ? kFull : ((2u << lim) - 1u);
+        if (lane == 0) atomicAdd(&p.ws->lb_rounds, 1u);
         if (imask & need) {
+            if (lane == 0) atomicAdd(&p.ws->lb_spins, 1u);
             __nanosleep(64);
             continue;
         }

@@ -55,8 +55,8 @@ struct SmemT {
     TileT<kL> ts[2];
     unsigned char qslot[kW][2 * kK2Items * 32];
     unsigned char own[kW][32];
-    float sr2[CUDAPRE_SECTORS + 1];    // sector inner radii^2 (copied from the parameters)
-    float sro2[CUDAPRE_SECTORS + 1];   // sector outer radii^2
+    float sr2[CUDAPRE_SECTORS + 1];    // sector inner radii^2 (copied from the parameters;
+    float sro2[CUDAPRE_SECTORS + 1];   // divergent parameter-space reads serialise)
     unsigned wsum[kW];
     unsigned next;
     unsigned long long prefix;
@@ -232,7 +232,13 @@ __global__ void __launch_bounds__(kK2Threads, K2Cfg<CFG>::kMinB) k2_filter_tma(c
                 const float4* stg = S.ring[seq % kNst];
                 if (bytes) mbar_wait(&S.full[seq % kNst], (seq / kNst) & 1u);
                 unsigned needy = 0u;   // bit b = 2u + h
-                if (npairs_here == (unsigned)kK2SubPairs) {
+                if (p.debug == 1) {   // perf experiment only: skeleton, no classification
+#pragma unroll
+                    for (int u = 0; u < kK2Items; ++u) {
+                        const float4 v = stg[u * kK2Threads + threadIdx.x];
+                        needy |= (v.x == 12345.0f ? 1u : 0u) << (2 * u);
+                    }
+                } else if (npairs_here == (unsigned)kK2SubPairs) {
 #pragma unroll
                     for (int u = 0; u < kK2Items; ++u) {
                         const float4 v = stg[u * kK2Threads + threadIdx.x];
@@ -328,9 +334,14 @@ __global__ void __launch_bounds__(kK2Threads, K2Cfg<CFG>::kMinB) k2_filter_tma(c
                 if (bytes && lane == 0) mbar_arrive(&S.empty[seq % kNst]);
             }
             if (lane == 0) cur.wcnt[warp] = wc;
-            if (threadIdx.x == kProd && pnext == kNone) {   // short last tile: ticket not taken yet
-                pnext = atomicAdd(&p.ws->k2_ticket, 1u);
-                S.next = pnext;
+            if (threadIdx.x == kProd) {
+                if (pnext == kNone) {   // short last tile: ticket not taken yet
+                    pnext = atomicAdd(&p.ws->k2_ticket, 1u);
+                    S.next = pnext;
+                }
+                // refill the stage just released so the ring stays full through
+                // the scan / look-back / pass B that follow
+                produce((k + 1) * kK2Sub + kNst);
             }
         }
         __syncthreads();   // pass A done everywhere

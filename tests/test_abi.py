@@ -48,7 +48,7 @@ def test_struct_sizes_match_header(L):
     # offsets derived from the C layout rules of include/cudapre.h
     assert ctypes.sizeof(cp.ExtremesT) == 8 + 8 + 32 * 8 + 32 * 8 + 32 * 8 + 8 * 8 + 8 * 8 + 8
     assert ctypes.sizeof(cp.PolygonT) == 16 + 32 * 8 + 32 * 8 + 16 + 16 + 8 + 4 * 32 * 4 + 2 * 4 * 1025
-    assert ctypes.sizeof(cp.ReportT) == 48
+    assert ctypes.sizeof(cp.ReportT) == 64
 
 
 def test_angle_presets_correctly_rounded(L):
