@@ -53,11 +53,15 @@ struct K1Partial {
 constexpr size_t kWsHeaderBytes = 4096;
 constexpr size_t kWsPartialBytes = sizeof(K1Partial) * kMaxK1Blocks * CUDAPRE_MAX_SLOTS;
 
-// tile-status words are sized for the smallest super-tile any K2 kernel uses
-constexpr int kStatusTilePts = 14336;   // warp-specialised K2: 7168 pairs
+// One tile-status word per super-tile, each on its own 128-byte line: packed
+// words put up to 16 publishing SMs and every look-back reader on one L2 line
+// and cost ~0.6 ms per 2e9 points (profiles/r01_experiments.md, "status
+// false sharing"); padded, the 256-wide look-back costs ~0.1 ms.
+constexpr int kStatusTilePts = kK2TilePts;
+constexpr int kStatusStride = 16;   // u64 words per status line (128 B)
 inline size_t ws_tiles(int64_t n) { return (size_t)((n + kStatusTilePts - 1) / kStatusTilePts); }
 inline size_t ws_bytes_for(int64_t n) {
-    return kWsHeaderBytes + kWsPartialBytes + 8 * (ws_tiles(n) + 1);
+    return kWsHeaderBytes + kWsPartialBytes + 8 * kStatusStride * (ws_tiles(n) + 1);
 }
 
 // ---------------------------------------------------------------- kernel params
@@ -84,7 +88,7 @@ struct K2Params {
     float* out_pts;           // nullable, float2 per survivor
     unsigned long long capacity;
     WsHeader* ws;
-    unsigned long long* status;   // ntiles tile-status words
+    unsigned long long* status;   // ntiles tile-status words, kStatusStride apart
     unsigned int num_tiles;
     int mode;                 // 0 = filter, 1 = keep everything (degenerate), 2 = exact only
     int debug;                // perf experiments only (CUDAPRE_K2_DEBUG): 1 = skeleton, no classification

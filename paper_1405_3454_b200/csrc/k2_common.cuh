@@ -86,20 +86,25 @@ __device__ __forceinline__ bool queue_keep(const K2Params& p, float x, float y) 
 }
 
 // ---------------------------------------------------------------- look-back
-// Status word of super-tile t: [epoch:30 | flag:2 | count:32].  publish_*
-// write it with one relaxed 64-bit store; resolve() (warp 0) walks back 256
+// Status word of super-tile t: [epoch:30 | flag:2 | count:32] at
+// status[t * kStatusStride] (one per 128-byte line).  publish() writes it with
+// one relaxed 64-bit store; resolve() (warp 0) walks back 256
 // predecessors per round (8 loads in flight per lane) summing aggregates up to
 // the nearest inclusive prefix.  Because resolve(t) runs one tile-time after
 // t's own aggregate was published (deferred, see the kernel), every
 // predecessor's aggregate is normally already there: no spinning.
 __device__ __forceinline__ void publish(const K2Params& p, unsigned tile, unsigned flag,
                                         unsigned long long value, unsigned epoch) {
-    st_status(&p.status[tile], ((unsigned long long)(epoch & kEpochMask) << 34) |
+    st_status(&p.status[(size_t)tile * kStatusStride], ((unsigned long long)(epoch & kEpochMask) << 34) |
                                    ((unsigned long long)flag << 32) | (value & 0xffffffffull));
 }
 
+// rounds / spins: diagnostic counters kept in registers by the caller and
+// added to the workspace once per block (a per-tile atomic on one address
+// is itself a hot spot).
 __device__ __forceinline__ unsigned long long resolve(const K2Params& p, unsigned tile,
-                                                      unsigned epoch, unsigned lane) {
+                                                      unsigned epoch, unsigned lane,
+                                                      unsigned& rounds, unsigned& spins) {
     constexpr int kPer = 8;
     const unsigned long long PF = (unsigned long long)kFlagP << 32;
     const unsigned long long E = (unsigned long long)(epoch & kEpochMask) << 34;
@@ -110,7 +115,7 @@ __device__ __forceinline__ unsigned long long resolve(const K2Params& p, unsigne
 #pragma unroll
         for (int k = 0; k < kPer; ++k) {
             const long long t = pred - (long long)(kPer * lane + k);
-            w[k] = (t >= 0) ? ld_status(&p.status[t]) : (E | PF);
+            w[k] = (t >= 0) ? ld_status(&p.status[(size_t)t * kStatusStride]) : (E | PF);
         }
         int kp = kPer;
         bool inval = false;
@@ -129,9 +134,9 @@ __device__ __forceinline__ unsigned long long resolve(const K2Params& p, unsigne
         const unsigned imask = __ballot_sync(kFull, inval);
         const unsigned lim = pmask ? (unsigned)(__ffs(pmask) - 1) : 31u;
         const unsigned need = (lim == 31u) ? kFull : ((2u << lim) - 1u);
-        if (lane == 0) atomicAdd(&p.ws->lb_rounds, 1u);
+        ++rounds;
         if (imask & need) {
-            if (lane == 0) atomicAdd(&p.ws->lb_spins, 1u);
+            ++spins;
             __nanosleep(64);
             continue;
         }

@@ -135,6 +135,7 @@ __global__ void __launch_bounds__(kK2Threads, 2) k2_filter(const __grid_constant
     __syncthreads();
     unsigned tile = S.next;
     unsigned pend = 0xffffffffu;   // super-tile awaiting resolve + pass B
+    unsigned lb_rounds = 0, lb_spins = 0;   // warp 0's look-back diagnostics
     float4 v[kK2Items];
     if (tile < p.num_tiles) {
 #pragma unroll
@@ -305,7 +306,7 @@ __global__ void __launch_bounds__(kK2Threads, 2) k2_filter(const __grid_constant
             if (warp == 0) {
                 unsigned long long ex = 0;
                 if (pend != 0) {
-                    ex = resolve(p, pend, epoch, lane);
+                    ex = resolve(p, pend, epoch, lane, lb_rounds, lb_spins);
                     if (lane == 0) {
                         publish(p, pend, kFlagP, ex + prv.total, epoch);
                         if (pend == p.num_tiles - 1) p.ws->count = ex + prv.total;
@@ -324,6 +325,8 @@ __global__ void __launch_bounds__(kK2Threads, 2) k2_filter(const __grid_constant
     // last block out resets the ticket and bumps the epoch (all blocks have
     // read `epoch` and taken their final ticket before incrementing k2_done)
     if (threadIdx.x == 0) {
+        if (lb_rounds) atomicAdd(&p.ws->lb_rounds, lb_rounds);
+        if (lb_spins) atomicAdd(&p.ws->lb_spins, lb_spins);
         __threadfence();
         const unsigned d = atomicAdd(&p.ws->k2_done, 1u);
         if (d == gridDim.x - 1) {

@@ -214,6 +214,7 @@ __global__ void __launch_bounds__(kK2Threads, K2Cfg<CFG>::kMinB) k2_filter_tma(c
     __syncthreads();
     unsigned tile = S.next;
     unsigned pend = kNone;
+    unsigned lb_rounds = 0, lb_spins = 0;   // warp 0's look-back diagnostics
     for (unsigned k = 0;; ++k) {
         const bool have = tile < p.num_tiles;
         TileT<kL>& cur = S.ts[k & 1];
@@ -385,7 +386,7 @@ __global__ void __launch_bounds__(kK2Threads, K2Cfg<CFG>::kMinB) k2_filter_tma(c
             if (warp == 0) {
                 unsigned long long ex = 0;
                 if (pend != 0) {
-                    ex = resolve(p, pend, epoch, lane);
+                    ex = resolve(p, pend, epoch, lane, lb_rounds, lb_spins);
                     if (lane == 0) {
                         publish(p, pend, kFlagP, ex + prv.total, epoch);
                         if (pend == p.num_tiles - 1) p.ws->count = ex + prv.total;
@@ -407,6 +408,8 @@ __global__ void __launch_bounds__(kK2Threads, K2Cfg<CFG>::kMinB) k2_filter_tma(c
         }
     }
     if (threadIdx.x == 0) {
+        if (lb_rounds) atomicAdd(&p.ws->lb_rounds, lb_rounds);
+        if (lb_spins) atomicAdd(&p.ws->lb_spins, lb_spins);
         __threadfence();
         const unsigned d = atomicAdd(&p.ws->k2_done, 1u);
         if (d == gridDim.x - 1) {

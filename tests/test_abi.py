@@ -80,7 +80,7 @@ def test_empty_and_bad_args_without_gpu(L):
                             np.zeros(8).ctypes.data_as(ctypes.c_void_p), None, 0, None, None,
                             None, None)
     assert st == cp.ERR_ARG
-    assert L.cudapre_workspace_bytes(10 ** 9) > 8 * (10 ** 9 // 16384)   # one status word per super-tile
+    assert L.cudapre_workspace_bytes(10 ** 9) > 128 * (10 ** 9 // 16384)   # one 128-byte status line per super-tile
 
 
 # ------------------------------------------------------------ host-side pieces
