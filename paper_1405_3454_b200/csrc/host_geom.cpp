@@ -220,7 +220,9 @@ void build_polygon(const cudapre_extremes_t& ext, cudapre_polygon_t* poly, K2Par
         for (int b = 0; b <= CUDAPRE_SECTORS; ++b) {
             kp->sr2[b] = -1.0f;
             kp->sro2[b] = INFINITY;
+            kp->sedge[b] = 0xffff;
         }
+        kp->fast = 0;
         for (int j = 0; j <= nv && j <= CUDAPRE_MAX_SLOTS; ++j) {
             kp->vx[j] = poly->v[j % (nv ? nv : 1)].x;
             kp->vy[j] = poly->v[j % (nv ? nv : 1)].y;
@@ -402,6 +404,7 @@ void build_polygon(const cudapre_extremes_t& ext, cudapre_polygon_t* poly, K2Par
             const SectorSamples& SS = sector_samples();
             constexpr int kS = SectorSamples::kS;
             double rs[kS];
+            int exe[kS];   // exit edge of each sample ray
             int cur = 0;
             for (int k = 0; k < nv; ++k)   // start at the edge whose range holds pa = 4 - eps
                 if (pv[k] > pv[cur]) cur = k;
@@ -428,7 +431,21 @@ void build_polygon(const cudapre_extremes_t& ext, cudapre_polygon_t* poly, K2Par
                     }
                 }
                 rs[i] = bn / bd * SS.ul[i];
+                exe[i] = cur;
             }
+            // Candidate edges of bucket b: every ray with pseudo-angle strictly
+            // inside the guarded range exits through an edge from exe[2b] to
+            // exe[2b+3] (CCW; the ring is convex around the centre).  A rounding
+            // slip in the walk can only pick the other edge of a vertex lying
+            // within ~1e-15 of a sample ray, which widens the range; points of
+            // the bucket lie >= 2^-15 in pa from the samples (guard 2^-14, bucket
+            // error < 2^-20), so they never need an edge outside it.
+            if (kp)
+                for (int b = 0; b <= CUDAPRE_SECTORS; ++b) {
+                    const int lo = exe[2 * b], hi = exe[2 * (b + 1) + 1];
+                    const int cnt = (hi - lo + nv) % nv + 1;
+                    kp->sedge[b] = cnt <= 2 ? (unsigned short)(lo | (hi << 8)) : (unsigned short)0xffff;
+                }
             for (int b = 0; b <= CUDAPRE_SECTORS; ++b) rb[b] = std::min(rs[2 * b], rs[2 * (b + 1) + 1]);
             // outer bound: r(th) is maximal at the interval ends or at a vertex
             // inside it; dj is a LOWER bound of the line distance, so the ray
@@ -492,6 +509,12 @@ void build_polygon(const cudapre_extremes_t& ext, cudapre_polygon_t* poly, K2Par
         kp->bx1 = poly->box[1];
         kp->by0 = poly->box[2];
         kp->by1 = poly->box[3];
+        // the TMA kernel runs one fast test in pass A: the one covering more area
+        const double disk = kp->r2 > 0.0f ? 3.141592653589793 * (double)kp->r2 : 0.0;
+        const double box = (kp->bx0 <= kp->bx1 && kp->by0 <= kp->by1)
+                               ? ((double)kp->bx1 - kp->bx0) * ((double)kp->by1 - kp->by0)
+                               : 0.0;
+        kp->fast = box > disk ? 1 : 0;
     }
 }
 

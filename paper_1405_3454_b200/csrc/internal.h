@@ -99,6 +99,10 @@ struct K2Params {
     float vx[CUDAPRE_MAX_SLOTS + 1], vy[CUDAPRE_MAX_SLOTS + 1];               // ring, v[nv] = v[0]
     float sr2[CUDAPRE_SECTORS + 1];    // sector inner radii^2 around (ox, oy) (-1 = off)
     float sro2[CUDAPRE_SECTORS + 1];   // sector outer radii^2 (+inf = off)
+    // edges a ray of bucket b can exit through: lo | hi << 8 (hi = lo or lo+1
+    // cyclically); 0xffff = more than two (or no table): test every edge
+    unsigned short sedge[CUDAPRE_SECTORS + 1];
+    int fast;                 // TMA K2 pass-A test: 0 = inner disk, 1 = inner box (the larger)
 };
 
 // ---------------------------------------------------------------- launchers (.cu)

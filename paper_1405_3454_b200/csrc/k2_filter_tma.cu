@@ -1,22 +1,34 @@
 // k2_filter_tma.cu — Step 3 of CudaPre (§2 Step 3; SPEC.md
 // S:156-164), TMA-ring variant for 16-byte aligned input (mode 0).
 //
-// Same classification and ordered compaction as k2_filter.cu (see its header
-// and DESIGN.md §6.2), but the points never pass through registers on their
-// way in: one elected thread streams 16 KiB sub-tiles global -> shared with
-// cp.async.bulk (SASS UBLKCP) into a kNst-deep ring of stages, each guarded by
-// a transaction-counting "full" mbarrier and a per-warp "empty" mbarrier.
-// Warps read their 8 points per sub-tile with LDS.128; undecided points are
-// queued as 1-byte slots that point back into the stage, so the queue pass,
-// the survivor list and the coordinates all come from shared memory.
+// Same classification and ordered compaction contract as k2_filter.cu (see
+// its header and DESIGN.md §6.2), organised so that the common path costs as
+// few instructions per point as possible:
 //
-// Per super-tile (8 sub-tiles, 128 KiB, one ticket):
-//   pass A(k)    classify, queue, ballots + survivor list into ts[k&1];
-//                block scan; publish the aggregate (tile 0: its prefix);
-//   resolve(k-1) decoupled look-back one tile-time later (no spinning);
-//   pass B(k-1)  write the survivors' int64 indices + float2 points.
-// The producer takes the next super-tile's ticket when the ring first needs
-// it (sub-tile 8 - kNst + 1 of pass A) so loads never stall at the boundary.
+//  * Loads: one elected thread streams 16 KiB sub-tiles global -> shared with
+//    cp.async.bulk (SASS UBLKCP) into a kNst-deep ring guarded by a
+//    transaction-counting "full" mbarrier and a per-warp "empty" mbarrier.
+//    The producer never blocks on a stage it only wants to prefetch
+//    (mbarrier.test_wait), so its warp does not fall behind the others, and it
+//    takes the next super-tile's ticket early (the atomic's latency overlaps
+//    the first sub-tiles).
+//  * Ownership: warp w owns the contiguous 256 points [256w, 256w+256) of each
+//    2048-point sub-tile, lane l the pairs u*32+l (u = 0..3).  The groups of
+//    the ordered compaction are the 64 (sub-tile, warp) chunks, in index order.
+//  * Pass A: one fast test per point (inner disk or inner box, whichever the
+//    host found larger; a warp-uniform switch).  Points it cannot decide are
+//    queued in INDEX order (one packed 4x8-bit warp scan), so the per-warp
+//    survivor list comes out sorted and a survivor's rank inside its group is
+//    its list position minus the group's start: no per-group ballots.
+//  * Queue pass: sector table (inner/outer radius of the bucket), then for
+//    the thin undecided band the 1-2 edges the bucket's rays can exit through
+//    (coefficients in shared memory), then the exact predicate.
+//  * Per super-tile: after pass A warp 0 resolves the PREVIOUS super-tile
+//    (decoupled look-back, one tile-time after its aggregate was published)
+//    while warp 1 scans the current one's 64 group counts and publishes its
+//    aggregate; one barrier; all warps write the previous tile's survivors.
+//    Each warp touches only its own lists between barriers, so two barriers
+//    per super-tile suffice.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -29,22 +41,23 @@ namespace cudapre {
 namespace {
 
 constexpr int kW = kK2Threads / 32;                  // 8 warps
-constexpr int kG = kK2Sub * kK2Items * kW;           // 256 ballot groups per super-tile
+constexpr int kGroups = kK2Sub * kW;                 // 64 groups (sub, warp) per super-tile
+constexpr unsigned kChunkPairs = kK2SubPairs / kW;   // 128 pairs = 256 points per warp chunk
 constexpr unsigned kNone = 0xffffffffu;
 constexpr unsigned kProd = kK2Threads - 32;          // producer thread: lane 0 of the last warp
 
 struct SurvT {
     float x, y;
-    unsigned meta;   // (group << 6) | (owner lane << 1) | pair element
+    unsigned meta;   // (sub << 8) | loc,  loc = u*64 + lane*2 + h = point offset in the warp chunk
 };
 
 template <unsigned kL>
 struct TileT {
-    unsigned mask[kG][2];   // keep ballots, group g = (sub*kK2Items + u)*kW + warp
-    unsigned off[kG];       // exclusive offset of each group inside the super-tile
-    unsigned wcnt[kW];      // survivors per warp
+    SurvT list[kW][kL];                 // per-warp survivors in index order
+    unsigned lstart[kW][kK2Sub + 1];    // list position where (warp, sub) starts; [kK2Sub] = total
+    unsigned off[kGroups];              // exclusive offset of group sub*kW + warp in the super-tile
     unsigned total;
-    SurvT list[kW][kL];
+    unsigned char own[kK2Sub][kW][32];  // keep bits per lane (bit 2u+h): list-overflow path only
 };
 
 template <int kNst, unsigned kL>
@@ -54,91 +67,69 @@ struct SmemT {
     unsigned long long empty[kNst];
     TileT<kL> ts[2];
     unsigned char qslot[kW][2 * kK2Items * 32];
-    unsigned char own[kW][32];
-    float sr2[CUDAPRE_SECTORS + 1];    // sector inner radii^2 (copied from the parameters;
-    float sro2[CUDAPRE_SECTORS + 1];   // divergent parameter-space reads serialise)
-    unsigned wsum[kW];
+    float2 sec[CUDAPRE_SECTORS + 1];               // {inner r^2, outer r^2} per bucket
+    unsigned short sedge[CUDAPRE_SECTORS + 1];     // candidate exit edges per bucket
+    float4 edge[CUDAPRE_MAX_SLOTS];                // {A, B, C', 0} (C' already lowered by E_j)
     unsigned next;
     unsigned long long prefix;
 };
 
-// Sector test: pseudo-angle bucket of p around (ox, oy) by
-// one approximate reciprocal; strictly inside if |p - o|^2 < sr2[bucket].
-// The host's buckets carry a 1/64-bucket guard band, far above the bucket
-// error of this arithmetic (< 2^-12 bucket); NaN/Inf map to a clamped bucket
-// and fail the comparison.
 __device__ __forceinline__ float rcp_approx(float a) {
     float r;
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(a));
     return r;
 }
-// 0 = strictly inside, 1 = strictly outside, 2 = undecided
-__device__ __forceinline__ int sector_class(const float* sr2, const float* sro2, float x, float y,
-                                            float ox, float oy) {
-    const float2 d = __fadd2_rn(make_float2(x, y), make_float2(-ox, -oy));
+
+__device__ __forceinline__ bool mbar_test(unsigned long long* bar, unsigned parity) {
+    unsigned ok;
+    asm volatile(
+        "{\n .reg .pred P1;\n mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n selp.u32 %0, 1, 0, P1;\n }"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0u;
+}
+
+// Keep decision for a point the pass-A test could not decide (true = keep).
+// Sector test: pseudo-angle bucket of p around (ox, oy) by one
+// approximate reciprocal; strictly inside if |p - o|^2 < inner[b], strictly
+// outside if > outer[b] (the host's buckets carry a 1/64-bucket guard band,
+// far above this arithmetic's bucket error < 2^-12).  In between, p's ray exits
+// through one of the bucket's candidate edges, so "inside" = inside those
+// edges; float lines with the error margin E_j folded into C' decide unless
+// |g| is within 2 Emax, then the exact predicate over the whole ring.
+template <int EDGES, int kNst, unsigned kL>
+__device__ __forceinline__ bool classify_queued(const K2Params& p, const SmemT<kNst, kL>& S, float x,
+                                                float y) {
+    const float2 d = __fadd2_rn(make_float2(x, y), make_float2(-p.ox, -p.oy));
     const float2 q = __fmul2_rn(d, d);
     const float d2 = __fadd_rn(q.x, q.y);
     const float t = __fmul_rn(d.y, rcp_approx(__fadd_rn(fabsf(d.x), fabsf(d.y))));
     const bool pos = d.x >= 0.0f;
     const float v = __fmaf_rn(t, pos ? 256.0f : -256.0f, pos ? 8388864.0f : 8389376.0f);   // 2^23 + 256 pa
     const unsigned b = min(__float_as_uint(v) - 0x4B000000u, (unsigned)CUDAPRE_SECTORS);
-    return d2 < sr2[b] ? 0 : (d2 > sro2[b] ? 1 : 2);
+    const float2 rr = S.sec[b];
+    if (d2 < rr.x) return false;
+    if (d2 > rr.y) return true;
+    const unsigned se = S.sedge[b];
+    if (se == 0xffffu) return queue_keep<EDGES>(p, x, y);
+    const float4 e0 = S.edge[se & 0xffu], e1 = S.edge[se >> 8];
+    const float mn = fminf(__fmaf_rn(e0.x, x, __fmaf_rn(e0.y, y, e0.z)),
+                           __fmaf_rn(e1.x, x, __fmaf_rn(e1.y, y, e1.z)));
+    if (mn > 0.0f) return false;
+    if (__fadd_rn(mn, p.e2max) < 0.0f) return true;
+    return !exact_inside(p, x, y);
 }
 
-// global point index of a survivor entry
-__device__ __forceinline__ unsigned entry_index(unsigned tbase, unsigned meta) {
-    const unsigned g = meta >> 6, ol = (meta >> 1) & 31u, h = meta & 1u;
-    const unsigned q = tbase + (g >> 5) * kK2SubPairs + ((g >> 3) & 3u) * kK2Threads + (g & 7u) * 32u + ol;
-    return 2u * q + h;
+// inner box, closed (host-proven strictly inside)
+__device__ __forceinline__ bool in_box(const K2Params& p, float x, float y) {
+    return (x >= p.bx0) & (x <= p.bx1) & (y >= p.by0) & (y <= p.by1);
 }
-
-template <unsigned kL>
-__device__ __forceinline__ void emit_t(const K2Params& p, const TileT<kL>& ts, unsigned tbase,
-                                       unsigned long long ex, unsigned warp, unsigned lane,
-                                       unsigned lt) {
-    const unsigned wc = ts.wcnt[warp];
-    if (wc <= kL) {
-        for (unsigned r = lane; r < wc; r += 32) {
-            const SurvT e = ts.list[warp][r];
-            const unsigned g = e.meta >> 6, ol = (e.meta >> 1) & 31u, h = e.meta & 1u;
-            const unsigned m0 = ts.mask[g][0], m1 = ts.mask[g][1], olt = (1u << ol) - 1u;
-            const unsigned rig = __popc(m0 & olt) + __popc(m1 & olt) + (h ? ((m0 >> ol) & 1u) : 0u);
-            const unsigned long long pos = ex + ts.off[g] + rig;
-            if (pos < p.capacity) {
-                p.out_idx[pos] = p.base + (long long)entry_index(tbase, e.meta);
-                if (p.out_pts) reinterpret_cast<float2*>(p.out_pts)[pos] = make_float2(e.x, e.y);
-            }
-        }
-        return;
-    }
-    // dense (list overflow): every group of this warp, coordinates re-read (L2)
-#pragma unroll 1
-    for (int sub = 0; sub < kK2Sub; ++sub) {
-#pragma unroll
-        for (int u = 0; u < kK2Items; ++u) {
-            const int g = (sub * kK2Items + u) * kW + warp;
-            const unsigned b0 = ts.mask[g][0], b1 = ts.mask[g][1];
-            const bool k0 = (b0 >> lane) & 1u, k1 = (b1 >> lane) & 1u;
-            if (!(k0 | k1)) continue;
-            unsigned long long pos = ex + ts.off[g] + __popc(b0 & lt) + __popc(b1 & lt);
-            const unsigned i0 = 2u * (tbase + sub * kK2SubPairs + u * kK2Threads + threadIdx.x);
-            if (k0) {
-                if (pos < p.capacity) {
-                    p.out_idx[pos] = p.base + (long long)i0;
-                    if (p.out_pts)
-                        reinterpret_cast<float2*>(p.out_pts)[pos] =
-                            __ldcg(reinterpret_cast<const float2*>(p.pts) + i0);
-                }
-                ++pos;
-            }
-            if (k1 && pos < p.capacity) {
-                p.out_idx[pos] = p.base + (long long)(i0 + 1u);
-                if (p.out_pts)
-                    reinterpret_cast<float2*>(p.out_pts)[pos] =
-                        __ldcg(reinterpret_cast<const float2*>(p.pts) + i0 + 1);
-            }
-        }
-    }
+// inner disk: RN(RN(dx^2) + RN(dy^2)) < r2 (DESIGN.md §6.2 bound)
+__device__ __forceinline__ bool in_disk(const K2Params& p, float x, float y) {
+    const float2 d = __fadd2_rn(make_float2(x, y), make_float2(-p.ox, -p.oy));
+    const float2 d2 = __fmul2_rn(d, d);
+    return __fadd_rn(d2.x, d2.y) < p.r2;
 }
 
 // bytes of full point pairs of sub-tile `sub` of super-tile `tile` in memory
@@ -149,15 +140,64 @@ __device__ __forceinline__ unsigned sub_bytes(unsigned tile, unsigned sub, unsig
     return (np >= (unsigned)kK2SubPairs ? (unsigned)kK2SubPairs : np) * 16u;
 }
 
-// CFG 0: 4-stage ring, 128-entry lists, 2 blocks/SM (default);
-// CFG 1: 3-stage ring, 64-entry lists, 3 blocks/SM (<= 85 registers).
+// point index (relative to the super-tile) of chunk offset loc of (sub, warp)
+__device__ __forceinline__ unsigned chunk_point(unsigned sub, unsigned warp, unsigned loc) {
+    return sub * (2u * kK2SubPairs) + warp * (2u * kChunkPairs) + loc;
+}
+
+// write the survivors of super-tile `tile` (warp-private lists) from exclusive
+// prefix ex
+template <unsigned kL>
+__device__ __forceinline__ void emit_t(const K2Params& p, const TileT<kL>& ts, unsigned tile,
+                                       unsigned long long ex, unsigned warp, unsigned lane,
+                                       unsigned lt) {
+    const unsigned long long tpt = (unsigned long long)tile * (2u * kK2TilePairs);
+    float2* out_pts = reinterpret_cast<float2*>(p.out_pts);
+    const unsigned wc = ts.lstart[warp][kK2Sub];
+    if (wc <= kL) {
+        for (unsigned r = lane; r < wc; r += 32) {
+            const SurvT e = ts.list[warp][r];
+            const unsigned sub = e.meta >> 8, loc = e.meta & 0xffu;
+            const unsigned long long pos = ex + ts.off[sub * kW + warp] + (r - ts.lstart[warp][sub]);
+            if (pos < p.capacity) {
+                p.out_idx[pos] = p.base + (long long)(tpt + chunk_point(sub, warp, loc));
+                if (out_pts) out_pts[pos] = make_float2(e.x, e.y);
+            }
+        }
+        return;
+    }
+    // list overflow (dense tile): ranks from the keep bits, coordinates re-read
+#pragma unroll 1
+    for (unsigned sub = 0; sub < (unsigned)kK2Sub; ++sub) {
+        const unsigned own = ts.own[sub][warp][lane];
+        unsigned long long run = ex + ts.off[sub * kW + warp];
+#pragma unroll
+        for (int u = 0; u < kK2Items; ++u) {
+            const unsigned k0 = (own >> (2 * u)) & 1u, k1 = (own >> (2 * u + 1)) & 1u;
+            const unsigned b0 = __ballot_sync(kFull, k0), b1 = __ballot_sync(kFull, k1);
+            const unsigned long long pos = run + __popc(b0 & lt) + __popc(b1 & lt);
+            const unsigned long long i0 = tpt + chunk_point(sub, warp, (unsigned)u * 64u + 2u * lane);
+            if (k0 && pos < p.capacity) {
+                p.out_idx[pos] = p.base + (long long)i0;
+                if (out_pts) out_pts[pos] = __ldcg(reinterpret_cast<const float2*>(p.pts) + i0);
+            }
+            if (k1 && pos + k0 < p.capacity) {
+                p.out_idx[pos + k0] = p.base + (long long)(i0 + 1);
+                if (out_pts) out_pts[pos + k0] = __ldcg(reinterpret_cast<const float2*>(p.pts) + i0 + 1);
+            }
+            run += __popc(b0) + __popc(b1);
+        }
+    }
+}
+
+// CFG 0: 4-stage ring (default); CFG 1: 3-stage ring.  128-entry lists per
+// warp and super-tile (6.25 % survivors before the overflow path).
 template <int CFG> struct K2Cfg;
 template <> struct K2Cfg<0> { static constexpr int kNst = 4; static constexpr unsigned kL = 128; static constexpr int kMinB = 2; };
-template <> struct K2Cfg<1> { static constexpr int kNst = 3; static constexpr unsigned kL = 64; static constexpr int kMinB = 3; };
+template <> struct K2Cfg<1> { static constexpr int kNst = 3; static constexpr unsigned kL = 128; static constexpr int kMinB = 2; };
 
 template <int EDGES, int CFG>
 __global__ void __launch_bounds__(kK2Threads, K2Cfg<CFG>::kMinB) k2_filter_tma(const __grid_constant__ K2Params p) {
-    static_assert(kG == kK2Threads, "one scan entry per thread");
     constexpr int kNst = K2Cfg<CFG>::kNst;
     constexpr unsigned kL = K2Cfg<CFG>::kL;
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -169,26 +209,28 @@ __global__ void __launch_bounds__(kK2Threads, K2Cfg<CFG>::kMinB) k2_filter_tma(c
     const bool odd = (p.n & 1u) != 0u;
     const float4* src = reinterpret_cast<const float4*>(p.pts);
 
-    // producer state (thread 0 only)
+    // ---- producer state (thread kProd only)
     unsigned issued = 0, pk = 0, ptile = kNone, pnext = kNone;
-    auto produce = [&](unsigned upto) {   // issue sequences < upto
-        while (issued < upto) {
+    // issue sequence numbers < want; block only for those < need
+    auto produce = [&](unsigned need, unsigned want) {
+        while (issued < want) {
             const unsigned kk = issued / kK2Sub;
             unsigned t;
             if (kk == pk) {
                 t = ptile;
-            } else {   // kk == pk + 1: the next super-tile, ticket taken on first need
-                if (pnext == kNone) {
-                    pnext = atomicAdd(&p.ws->k2_ticket, 1u);
-                    S.next = pnext;
-                }
+            } else {   // kk == pk + 1
+                if (pnext == kNone) pnext = atomicAdd(&p.ws->k2_ticket, 1u);
                 t = pnext;
             }
             if (t >= p.num_tiles) return;
             const unsigned bytes = sub_bytes(t, issued % kK2Sub, full_pairs);
             if (bytes == 0u) return;
             const unsigned st = issued % kNst;
-            if (issued >= (unsigned)kNst) mbar_wait(&S.empty[st], ((issued / kNst) - 1u) & 1u);
+            if (issued >= (unsigned)kNst) {
+                const unsigned par = ((issued / kNst) - 1u) & 1u;
+                if (issued < need) mbar_wait(&S.empty[st], par);
+                else if (!mbar_test(&S.empty[st], par)) return;
+            }
             mbar_expect_tx(&S.full[st], bytes);
             bulk_g2s(&S.ring[st][0], src + (size_t)t * kK2TilePairs + (issued % kK2Sub) * kK2SubPairs,
                      bytes, &S.full[st]);
@@ -196,11 +238,12 @@ __global__ void __launch_bounds__(kK2Threads, K2Cfg<CFG>::kMinB) k2_filter_tma(c
         }
     };
 
-    const float ox = p.ox, oy = p.oy;
     for (int i = threadIdx.x; i <= CUDAPRE_SECTORS; i += kK2Threads) {
-        S.sr2[i] = p.sr2[i];
-        S.sro2[i] = p.sro2[i];
+        S.sec[i] = make_float2(p.sr2[i], p.sro2[i]);
+        S.sedge[i] = p.sedge[i];
     }
+    if (threadIdx.x < (unsigned)CUDAPRE_MAX_SLOTS)
+        S.edge[threadIdx.x] = make_float4(p.A[threadIdx.x], p.B[threadIdx.x], p.C[threadIdx.x], 0.0f);
     if (threadIdx.x == kProd) {
         for (int k = 0; k < kNst; ++k) {
             mbar_init(&S.full[k], 1u);
@@ -209,9 +252,10 @@ __global__ void __launch_bounds__(kK2Threads, K2Cfg<CFG>::kMinB) k2_filter_tma(c
         mbar_fence_init();
         ptile = atomicAdd(&p.ws->k2_ticket, 1u);
         S.next = ptile;
-        produce(kNst);
+        produce(kNst, kNst);
     }
     __syncthreads();
+    const int fast = p.fast;
     unsigned tile = S.next;
     unsigned pend = kNone;
     unsigned lb_rounds = 0, lb_spins = 0;   // warp 0's look-back diagnostics
@@ -219,45 +263,52 @@ __global__ void __launch_bounds__(kK2Threads, K2Cfg<CFG>::kMinB) k2_filter_tma(c
         const bool have = tile < p.num_tiles;
         TileT<kL>& cur = S.ts[k & 1];
         TileT<kL>& prv = S.ts[(k & 1) ^ 1];
-        const unsigned tbase = tile * kK2TilePairs;
         if (have) {
             // ---------------- pass A
             unsigned wc = 0;
+            if (threadIdx.x == kProd && pnext == kNone)
+                pnext = atomicAdd(&p.ws->k2_ticket, 1u);   // result first needed a few sub-tiles later
 #pragma unroll 1
             for (int sub = 0; sub < kK2Sub; ++sub) {
                 const unsigned seq = k * kK2Sub + sub;
-                const unsigned qs = tbase + sub * kK2SubPairs;
                 const unsigned bytes = sub_bytes(tile, sub, full_pairs);
-                const unsigned npairs_here = bytes / 16u;
-                if (threadIdx.x == kProd) produce(seq + kNst);
-                const float4* stg = S.ring[seq % kNst];
+                const unsigned np = bytes / 16u;   // full pairs of this sub-tile in memory
+                if (threadIdx.x == kProd) produce(seq + 1u, seq + kNst);
+                const float4* chunk = &S.ring[seq % kNst][warp * kChunkPairs];
                 if (bytes) mbar_wait(&S.full[seq % kNst], (seq / kNst) & 1u);
-                unsigned needy = 0u;   // bit b = 2u + h
-                if (p.debug == 1) {   // perf experiment only: skeleton, no classification
+                unsigned needy = 0u;   // bit 2u + h: not decided by the fast test
+                if (np == (unsigned)kK2SubPairs) {
+                    if (p.debug == 1) {   // perf experiment only: skeleton, no classification
 #pragma unroll
-                    for (int u = 0; u < kK2Items; ++u) {
-                        const float4 v = stg[u * kK2Threads + threadIdx.x];
-                        needy |= (v.x == 12345.0f ? 1u : 0u) << (2 * u);
+                        for (int u = 0; u < kK2Items; ++u)
+                            needy |= (chunk[u * 32 + lane].x == 12345.0f ? 1u : 0u) << (2 * u);
+                    } else if (fast == 0) {
+#pragma unroll
+                        for (int u = 0; u < kK2Items; ++u) {
+                            const float4 v = chunk[u * 32 + lane];
+                            const unsigned in = (in_disk(p, v.x, v.y) ? 1u : 0u) | (in_disk(p, v.z, v.w) ? 2u : 0u);
+                            needy |= (3u & ~in) << (2 * u);
+                        }
+                    } else {
+#pragma unroll
+                        for (int u = 0; u < kK2Items; ++u) {
+                            const float4 v = chunk[u * 32 + lane];
+                            const unsigned in = (in_box(p, v.x, v.y) ? 1u : 0u) | (in_box(p, v.z, v.w) ? 2u : 0u);
+                            needy |= (3u & ~in) << (2 * u);
+                        }
                     }
-                } else if (npairs_here == (unsigned)kK2SubPairs) {
+                } else {   // last super-tile only: ragged end (+ the unpaired last point)
+                    const unsigned qs = tile * kK2TilePairs + sub * kK2SubPairs;
 #pragma unroll
                     for (int u = 0; u < kK2Items; ++u) {
-                        const float4 v = stg[u * kK2Threads + threadIdx.x];
-                        const unsigned in = (fast_inside(p, v.x, v.y) ? 1u : 0u) | (fast_inside(p, v.z, v.w) ? 2u : 0u);
-                        needy |= (3u & ~in) << (2 * u);
-                    }
-                } else {   // last super-tile only: ragged end
-#pragma unroll
-                    for (int u = 0; u < kK2Items; ++u) {
-                        const unsigned pr = u * kK2Threads + threadIdx.x;
-                        const unsigned q = qs + pr;
-                        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+                        const unsigned pr = warp * kChunkPairs + u * 32 + lane;
                         unsigned valid = 0u;
-                        if (pr < npairs_here) {
-                            v = stg[pr];
+                        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+                        if (pr < np) {
+                            v = S.ring[seq % kNst][pr];
                             valid = 3u;
-                        } else if (odd && q == full_pairs) {
-                            const float2 a = __ldg(reinterpret_cast<const float2*>(p.pts) + 2u * q);
+                        } else if (odd && qs + pr == full_pairs) {
+                            const float2 a = __ldg(reinterpret_cast<const float2*>(p.pts) + 2u * full_pairs);
                             v = make_float4(a.x, a.y, 0.f, 0.f);
                             valid = 1u;
                         }
@@ -265,110 +316,96 @@ __global__ void __launch_bounds__(kK2Threads, K2Cfg<CFG>::kMinB) k2_filter_tma(c
                         needy |= (valid & ~in) << (2 * u);
                     }
                 }
-                // undecided points -> per-warp queue of slots into the stage
-                const unsigned nq = __popc(needy);
-                unsigned incl = nq;
+                // ---- index-ordered queue: slot of (u, lane, h) = sum_{u'<u} T_u'
+                //      + (needy points of pair u in lanes < lane) + (h ? bit(2u) : 0)
+                const unsigned cnt = __popc(needy & 0x03u) | (__popc(needy & 0x0cu) << 8) |
+                                     (__popc(needy & 0x30u) << 16) | (__popc(needy & 0xc0u) << 24);
+                unsigned incl = cnt;   // 4 packed 8-bit fields, each <= 64
 #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) {
                     const unsigned y = __shfl_up_sync(kFull, incl, o);
                     if (lane >= (unsigned)o) incl += y;
                 }
-                const unsigned qtotal = __shfl_sync(kFull, incl, 31);
-                unsigned keep = 0u;
+                const unsigned T = __shfl_sync(kFull, incl, 31);
+                const unsigned qtotal = (T & 0xffu) + ((T >> 8) & 0xffu) + ((T >> 16) & 0xffu) + (T >> 24);
+                if (lane == 0) cur.lstart[warp][sub] = wc;
+                cur.own[sub][warp][lane] = 0;
                 if (qtotal) {
-                    S.own[warp][lane] = 0;
-                    unsigned j = incl - nq;
-#pragma unroll
-                    for (int b = 0; b < 2 * kK2Items; ++b) {   // converged, predicated stores
-                        if ((needy >> b) & 1u) S.qslot[warp][j] = (unsigned char)(lane * 8u + b);
-                        j += (needy >> b) & 1u;
+                    const unsigned sb = (T << 8) + (T << 16) + (T << 24) + (incl - cnt);   // fields <= 254
+                    for (unsigned m = needy; m; m &= m - 1u) {
+                        const unsigned b = __ffs(m) - 1u, u = b >> 1, h = b & 1u;
+                        const unsigned slot = ((sb >> (8u * u)) & 0xffu) + (h & (needy >> (2u * u)));
+                        S.qslot[warp][slot] = (unsigned char)((u << 6) | (lane << 1) | h);
                     }
                     __syncwarp();
                     for (unsigned base = 0; base < qtotal; base += 32) {
                         const unsigned e = base + lane;
                         bool kp = false;
                         float2 q = make_float2(0.f, 0.f);
-                        unsigned sl = 0;
+                        unsigned loc = 0;
                         if (e < qtotal) {
-                            sl = S.qslot[warp][e];
-                            const unsigned ol = sl >> 3, b = sl & 7u;
-                            const unsigned pr = (b >> 1) * kK2Threads + warp * 32u + ol;
-                            if (pr < npairs_here) {
-                                const float4* cell = &stg[pr];
-                                q = (b & 1u) ? make_float2(cell->z, cell->w) : make_float2(cell->x, cell->y);
+                            loc = S.qslot[warp][e];
+                            const unsigned pr = warp * kChunkPairs + (loc >> 1);
+                            if (pr < np) {
+                                q = reinterpret_cast<const float2*>(&S.ring[seq % kNst][0])[2u * pr + (loc & 1u)];
                             } else {   // the unpaired last point
-                                q = __ldg(reinterpret_cast<const float2*>(p.pts) + 2u * (qs + pr));
+                                q = __ldg(reinterpret_cast<const float2*>(p.pts) + 2u * full_pairs);
                             }
-                            const int sc = sector_class(S.sr2, S.sro2, q.x, q.y, ox, oy);
-                            kp = sc == 1 || (sc == 2 && queue_keep<EDGES>(p, q.x, q.y));
+                            kp = classify_queued<EDGES>(p, S, q.x, q.y);
                         }
                         const unsigned kb = __ballot_sync(kFull, kp);
                         if (kp) {
-                            const unsigned ol = sl >> 3, b = sl & 7u;
-                            atomicOr(reinterpret_cast<unsigned*>(&S.own[warp][ol & ~3u]), (1u << b) << (8u * (ol & 3u)));
+                            const unsigned ol = (loc >> 1) & 31u, b = ((loc >> 6) << 1) | (loc & 1u);
+                            atomicOr(reinterpret_cast<unsigned*>(&cur.own[sub][warp][ol & ~3u]),
+                                     (1u << b) << (8u * (ol & 3u)));
                             const unsigned r = wc + __popc(kb & lt);
-                            if (r < kL) {
-                                const unsigned g = (sub * kK2Items + (b >> 1)) * kW + warp;
-                                cur.list[warp][r] = SurvT{q.x, q.y, (g << 6) | (ol << 1) | (b & 1u)};
-                            }
+                            if (r < kL) cur.list[warp][r] = SurvT{q.x, q.y, ((unsigned)sub << 8) | loc};
                         }
                         wc += __popc(kb);
                     }
-                    __syncwarp();
-                    keep = S.own[warp][lane];
-#pragma unroll
-                    for (int u = 0; u < kK2Items; ++u) {
-                        const unsigned b0 = __ballot_sync(kFull, (keep >> (2 * u)) & 1u);
-                        const unsigned b1 = __ballot_sync(kFull, (keep >> (2 * u + 1)) & 1u);
-                        if (lane == 0) {
-                            const unsigned g = (sub * kK2Items + u) * kW + warp;
-                            cur.mask[g][0] = b0;
-                            cur.mask[g][1] = b1;
-                        }
-                    }
-                } else if (lane < (unsigned)kK2Items) {
-                    const unsigned g = (sub * kK2Items + lane) * kW + warp;
-                    cur.mask[g][0] = 0u;
-                    cur.mask[g][1] = 0u;
                 }
                 __syncwarp();
                 if (bytes && lane == 0) mbar_arrive(&S.empty[seq % kNst]);
             }
-            if (lane == 0) cur.wcnt[warp] = wc;
+            if (lane == 0) cur.lstart[warp][kK2Sub] = wc;
             if (threadIdx.x == kProd) {
-                if (pnext == kNone) {   // short last tile: ticket not taken yet
-                    pnext = atomicAdd(&p.ws->k2_ticket, 1u);
-                    S.next = pnext;
-                }
-                // refill the stage just released so the ring stays full through
-                // the scan / look-back / pass B that follow
-                produce((k + 1) * kK2Sub + kNst);
+                S.next = pnext;
+                // refill the stages just released so the ring stays full through
+                // the look-back / scan / survivor writes that follow
+                produce(0u, (k + 1) * kK2Sub + kNst);
             }
         }
-        __syncthreads();   // pass A done everywhere
+        __syncthreads();   // pass A done everywhere; cur complete
         const unsigned next = have ? S.next : kNone;
-        unsigned c = 0, inc = 0;
-        if (have) {   // block scan of the 256 group counts (group order = index order)
-            c = __popc(cur.mask[threadIdx.x][0]) + __popc(cur.mask[threadIdx.x][1]);
-            inc = c;
+        if (warp == 0 && pend != kNone) {
+            // decoupled look-back of the previous super-tile: its aggregate went
+            // out one tile-time ago, so its predecessors' are normally there too
+            unsigned long long ex = 0;
+            if (pend != 0) {
+                ex = resolve(p, pend, epoch, lane, lb_rounds, lb_spins);
+                if (lane == 0) {
+                    publish(p, pend, kFlagP, ex + prv.total, epoch);
+                    if (pend == p.num_tiles - 1) p.ws->count = ex + prv.total;
+                }
+            }
+            if (lane == 0) S.prefix = ex;
+        } else if (warp == 1 && have) {
+            // scan of the 64 group counts (group g = sub*kW + w, index order);
+            // lane l owns groups 2l, 2l+1 (sub-tile l/4, warps 2l%8 and +1)
+            const unsigned sub = lane >> 2, w0 = (2u * lane) & 7u;
+            const unsigned c0 = cur.lstart[w0][sub + 1] - cur.lstart[w0][sub];
+            const unsigned c1 = cur.lstart[w0 + 1][sub + 1] - cur.lstart[w0 + 1][sub];
+            unsigned inc = c0 + c1;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const unsigned y = __shfl_up_sync(kFull, inc, o);
                 if (lane >= (unsigned)o) inc += y;
             }
-            if (lane == 31) S.wsum[warp] = inc;
-        }
-        __syncthreads();
-        if (have) {   // offsets + publish this tile's aggregate (tile 0: its prefix)
-            unsigned wpre = 0, total = 0;
-#pragma unroll
-            for (int w = 0; w < kW; ++w) {
-                const unsigned x = S.wsum[w];
-                wpre += (w < (int)warp) ? x : 0u;
-                total += x;
-            }
-            cur.off[threadIdx.x] = wpre + inc - c;
-            if (threadIdx.x == 0) {
+            const unsigned ex0 = inc - c0 - c1;
+            cur.off[2 * lane] = ex0;
+            cur.off[2 * lane + 1] = ex0 + c0;
+            const unsigned total = __shfl_sync(kFull, inc, 31);
+            if (lane == 0) {
                 cur.total = total;
                 if (tile == 0) {
                     publish(p, 0, kFlagP, total, epoch);
@@ -378,26 +415,10 @@ __global__ void __launch_bounds__(kK2Threads, K2Cfg<CFG>::kMinB) k2_filter_tma(c
                 }
             }
         }
-        // ---------------- resolve + pass B of the pending super-tile: one
-        // tile-time after its aggregate was published, so its predecessors
-        // have published theirs (no spinning); the next super-tile's first
-        // sub-tiles are already in flight in the ring.
-        if (pend != kNone) {
-            if (warp == 0) {
-                unsigned long long ex = 0;
-                if (pend != 0) {
-                    ex = resolve(p, pend, epoch, lane, lb_rounds, lb_spins);
-                    if (lane == 0) {
-                        publish(p, pend, kFlagP, ex + prv.total, epoch);
-                        if (pend == p.num_tiles - 1) p.ws->count = ex + prv.total;
-                    }
-                }
-                if (lane == 0) S.prefix = ex;
-            }
-            __syncthreads();
-            emit_t(p, prv, pend * kK2TilePairs, S.prefix, warp, lane, lt);
-        }
-        __syncthreads();   // prv is reused by the next pass A
+        __syncthreads();   // S.prefix, cur.off ready
+        if (pend != kNone) emit_t(p, prv, pend, S.prefix, warp, lane, lt);
+        // no barrier here: until the next pass-A barrier every warp writes only
+        // its own list / lstart / own bytes, which no other warp reads before it
         if (!have) break;
         pend = tile;
         tile = next;
