@@ -85,6 +85,13 @@ __device__ __forceinline__ bool queue_keep(const K2Params& p, float x, float y) 
     return !exact_inside(p, x, y);
 }
 
+// Out-of-line copy for kernels where the all-edge loop is a rare path: inlined,
+// the compiler hoists its ~20 constant-bank loads onto the common path.
+template <int EDGES>
+__device__ __noinline__ bool queue_keep_rare(const K2Params& p, float x, float y) {
+    return queue_keep<EDGES>(p, x, y);
+}
+
 // ---------------------------------------------------------------- look-back
 // Status word of super-tile t: [epoch:30 | flag:2 | count:32] at
 // status[t * kStatusStride] (one per 128-byte line).  publish() writes it with

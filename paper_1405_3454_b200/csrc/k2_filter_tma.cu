@@ -44,7 +44,9 @@ constexpr int kW = kK2Threads / 32;                  // 8 warps
 constexpr int kGroups = kK2Sub * kW;                 // 64 groups (sub, warp) per super-tile
 constexpr unsigned kChunkPairs = kK2SubPairs / kW;   // 128 pairs = 256 points per warp chunk
 constexpr unsigned kNone = 0xffffffffu;
-constexpr unsigned kProd = kK2Threads - 32;          // producer thread: lane 0 of the last warp
+constexpr unsigned kBlock = kK2Threads + 64;         // 8 compute warps + producer warp + emit warp
+constexpr unsigned kProdWarp = kW, kEmitWarp = kW + 1;
+constexpr int kBufs = 3;                             // survivor-list buffers (tiles in flight)
 
 struct SurvT {
     float x, y;
@@ -57,6 +59,7 @@ struct TileT {
     unsigned lstart[kW][kK2Sub + 1];    // list position where (warp, sub) starts; [kK2Sub] = total
     unsigned off[kGroups];              // exclusive offset of group sub*kW + warp in the super-tile
     unsigned total;
+    unsigned tile;                      // super-tile id (kNone: end of work)
     unsigned char own[kK2Sub][kW][32];  // keep bits per lane (bit 2u+h): list-overflow path only
 };
 
@@ -65,29 +68,20 @@ struct SmemT {
     float4 ring[kNst][kK2SubPairs];
     unsigned long long full[kNst];
     unsigned long long empty[kNst];
-    TileT<kL> ts[2];
+    TileT<kL> ts[kBufs];
+    unsigned long long tile_done[kBufs];   // compute warps -> emit warp (count kW)
+    unsigned long long buf_free[kBufs];    // emit warp -> compute warps (count 1)
     unsigned char qslot[kW][2 * kK2Items * 32];
     float2 sec[CUDAPRE_SECTORS + 1];               // {inner r^2, outer r^2} per bucket
     unsigned short sedge[CUDAPRE_SECTORS + 1];     // candidate exit edges per bucket
     float4 edge[CUDAPRE_MAX_SLOTS];                // {A, B, C', 0} (C' already lowered by E_j)
-    unsigned next;
-    unsigned long long prefix;
+    unsigned stile[kNst];   // super-tile id of the sub-tile-0 stage (kNone = end)
 };
 
 __device__ __forceinline__ float rcp_approx(float a) {
     float r;
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(a));
     return r;
-}
-
-__device__ __forceinline__ bool mbar_test(unsigned long long* bar, unsigned parity) {
-    unsigned ok;
-    asm volatile(
-        "{\n .reg .pred P1;\n mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n selp.u32 %0, 1, 0, P1;\n }"
-        : "=r"(ok)
-        : "r"(smem_u32(bar)), "r"(parity)
-        : "memory");
-    return ok != 0u;
 }
 
 // Keep decision for a point the pass-A test could not decide (true = keep).
@@ -112,7 +106,7 @@ __device__ __forceinline__ bool classify_queued(const K2Params& p, const SmemT<k
     if (d2 < rr.x) return false;
     if (d2 > rr.y) return true;
     const unsigned se = S.sedge[b];
-    if (se == 0xffffu) return queue_keep<EDGES>(p, x, y);
+    if (se == 0xffffu) return queue_keep_rare<EDGES>(p, x, y);
     const float4 e0 = S.edge[se & 0xffu], e1 = S.edge[se >> 8];
     const float mn = fminf(__fmaf_rn(e0.x, x, __fmaf_rn(e0.y, y, e0.z)),
                            __fmaf_rn(e1.x, x, __fmaf_rn(e1.y, y, e1.z)));
@@ -190,14 +184,16 @@ __device__ __forceinline__ void emit_t(const K2Params& p, const TileT<kL>& ts, u
     }
 }
 
-// CFG 0: 4-stage ring (default); CFG 1: 3-stage ring.  128-entry lists per
-// warp and super-tile (6.25 % survivors before the overflow path).
+// CFG 0: 3-stage ring (default); CFG 1: 2-stage ring.  128-entry lists per
+// warp and super-tile (6.25 % survivors before the overflow path); three list
+// buffers; ~105 KB of shared memory, 2 blocks per SM.
 template <int CFG> struct K2Cfg;
-template <> struct K2Cfg<0> { static constexpr int kNst = 4; static constexpr unsigned kL = 128; static constexpr int kMinB = 2; };
-template <> struct K2Cfg<1> { static constexpr int kNst = 3; static constexpr unsigned kL = 128; static constexpr int kMinB = 2; };
+template <> struct K2Cfg<0> { static constexpr int kNst = 3; static constexpr unsigned kL = 128; static constexpr int kMinB = 2; };
+template <> struct K2Cfg<1> { static constexpr int kNst = 2; static constexpr unsigned kL = 128; static constexpr int kMinB = 2; };
 
-template <int EDGES, int CFG>
-__global__ void __launch_bounds__(kK2Threads, K2Cfg<CFG>::kMinB) k2_filter_tma(const __grid_constant__ K2Params p) {
+// DBG: perf-experiment build with per-warp cycle counters (CUDAPRE_K2_DEBUG=2)
+template <int EDGES, int CFG, bool DBG>
+__global__ void __launch_bounds__(kBlock, K2Cfg<CFG>::kMinB) k2_filter_tma(const __grid_constant__ K2Params p) {
     constexpr int kNst = K2Cfg<CFG>::kNst;
     constexpr unsigned kL = K2Cfg<CFG>::kL;
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -207,75 +203,172 @@ __global__ void __launch_bounds__(kK2Threads, K2Cfg<CFG>::kMinB) k2_filter_tma(c
     const unsigned epoch = *(volatile unsigned*)&p.ws->epoch;
     const unsigned full_pairs = p.n / 2u;
     const bool odd = (p.n & 1u) != 0u;
-    const float4* src = reinterpret_cast<const float4*>(p.pts);
 
-    // ---- producer state (thread kProd only)
-    unsigned issued = 0, pk = 0, ptile = kNone, pnext = kNone;
-    // issue sequence numbers < want; block only for those < need
-    auto produce = [&](unsigned need, unsigned want) {
-        while (issued < want) {
-            const unsigned kk = issued / kK2Sub;
-            unsigned t;
-            if (kk == pk) {
-                t = ptile;
-            } else {   // kk == pk + 1
-                if (pnext == kNone) pnext = atomicAdd(&p.ws->k2_ticket, 1u);
-                t = pnext;
-            }
-            if (t >= p.num_tiles) return;
-            const unsigned bytes = sub_bytes(t, issued % kK2Sub, full_pairs);
-            if (bytes == 0u) return;
-            const unsigned st = issued % kNst;
-            if (issued >= (unsigned)kNst) {
-                const unsigned par = ((issued / kNst) - 1u) & 1u;
-                if (issued < need) mbar_wait(&S.empty[st], par);
-                else if (!mbar_test(&S.empty[st], par)) return;
-            }
-            mbar_expect_tx(&S.full[st], bytes);
-            bulk_g2s(&S.ring[st][0], src + (size_t)t * kK2TilePairs + (issued % kK2Sub) * kK2SubPairs,
-                     bytes, &S.full[st]);
-            ++issued;
-        }
-    };
-
-    for (int i = threadIdx.x; i <= CUDAPRE_SECTORS; i += kK2Threads) {
+    for (int i = threadIdx.x; i <= CUDAPRE_SECTORS; i += kBlock) {
         S.sec[i] = make_float2(p.sr2[i], p.sro2[i]);
         S.sedge[i] = p.sedge[i];
     }
     if (threadIdx.x < (unsigned)CUDAPRE_MAX_SLOTS)
         S.edge[threadIdx.x] = make_float4(p.A[threadIdx.x], p.B[threadIdx.x], p.C[threadIdx.x], 0.0f);
-    if (threadIdx.x == kProd) {
+    if (threadIdx.x == 0) {
         for (int k = 0; k < kNst; ++k) {
             mbar_init(&S.full[k], 1u);
             mbar_init(&S.empty[k], (unsigned)kW);
         }
+        for (int k = 0; k < kBufs; ++k) {
+            mbar_init(&S.tile_done[k], (unsigned)kW);
+            mbar_init(&S.buf_free[k], 1u);
+        }
         mbar_fence_init();
-        ptile = atomicAdd(&p.ws->k2_ticket, 1u);
-        S.next = ptile;
-        produce(kNst, kNst);
     }
-    __syncthreads();
-    const int fast = p.fast;
-    unsigned tile = S.next;
-    unsigned pend = kNone;
-    unsigned lb_rounds = 0, lb_spins = 0;   // warp 0's look-back diagnostics
-    for (unsigned k = 0;; ++k) {
-        const bool have = tile < p.num_tiles;
-        TileT<kL>& cur = S.ts[k & 1];
-        TileT<kL>& prv = S.ts[(k & 1) ^ 1];
-        if (have) {
-            // ---------------- pass A
-            unsigned wc = 0;
-            if (threadIdx.x == kProd && pnext == kNone)
-                pnext = atomicAdd(&p.ws->k2_ticket, 1u);   // result first needed a few sub-tiles later
+    __syncthreads();   // the only whole-block barrier
+
+    // ================================================================ producer warp
+    // Lane 0 takes super-tile tickets (the next one while issuing the current
+    // one, so the atomic's latency is hidden), streams every sub-tile of each
+    // into the ring (zero-byte sub-tiles past the end complete their phase by a
+    // plain arrive) and tags the stage of sub-tile 0 with the tile id.  After
+    // the last ticket it publishes kNone in the next stage: the end marker.
+    if (warp == kProdWarp) {
+        if (lane == 0) {
+            const float4* src = reinterpret_cast<const float4*>(p.pts);
+            unsigned seq = 0;
+            unsigned t = atomicAdd(&p.ws->k2_ticket, 1u);
+            for (;;) {
+                const bool valid = t < p.num_tiles;
+                const unsigned tn = valid ? atomicAdd(&p.ws->k2_ticket, 1u) : kNone;
 #pragma unroll 1
-            for (int sub = 0; sub < kK2Sub; ++sub) {
-                const unsigned seq = k * kK2Sub + sub;
+                for (int sub = 0; sub < (valid ? kK2Sub : 1); ++sub, ++seq) {
+                    const unsigned st = seq % kNst;
+                    if (seq >= (unsigned)kNst) mbar_wait(&S.empty[st], ((seq / kNst) - 1u) & 1u);
+                    if (sub == 0) S.stile[st] = valid ? t : kNone;
+                    const unsigned bytes = valid ? sub_bytes(t, sub, full_pairs) : 0u;
+                    if (bytes) {
+                        mbar_expect_tx(&S.full[st], bytes);
+                        bulk_g2s(&S.ring[st][0], src + (size_t)t * kK2TilePairs + sub * kK2SubPairs, bytes,
+                                 &S.full[st]);
+                    } else {
+                        mbar_arrive(&S.full[st]);
+                    }
+                }
+                if (!valid) break;
+                t = tn;
+            }
+        }
+        return;
+    }
+
+    // ================================================================ emit warp
+    // Per super-tile k (list buffer k % kBufs), once all compute warps are done
+    // with it: scan its 64 group counts, publish its aggregate (tile 0: its
+    // prefix); then resolve the PREVIOUS super-tile (decoupled look-back one
+    // tile-time after its aggregate went out: no spinning), publish its
+    // inclusive prefix, write its survivors and hand its buffer back.  The
+    // compute warps never wait for any of this.
+    if (warp == kEmitWarp) {
+        unsigned lb_rounds = 0, lb_spins = 0;
+        unsigned long long dce[4] = {0, 0, 0, 0}, te = 0;   // DBG: wait, scan, resolve, emit
+        unsigned pend = kNone, pbuf = 0;
+        for (unsigned k = 0;; ++k) {
+            const unsigned bi = k % kBufs;
+            TileT<kL>& cur = S.ts[bi];
+            if (DBG) te = clock64();
+            mbar_wait(&S.tile_done[bi], (k / kBufs) & 1u);
+            if (DBG) { const unsigned long long t = clock64(); dce[0] += t - te; te = t; }
+            const unsigned tile = cur.tile;
+            if (tile != kNone) {
+                const unsigned sub = lane >> 2, w0 = (2u * lane) & 7u;
+                const unsigned c0 = cur.lstart[w0][sub + 1] - cur.lstart[w0][sub];
+                const unsigned c1 = cur.lstart[w0 + 1][sub + 1] - cur.lstart[w0 + 1][sub];
+                unsigned inc = c0 + c1;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const unsigned y = __shfl_up_sync(kFull, inc, o);
+                    if (lane >= (unsigned)o) inc += y;
+                }
+                const unsigned ex0 = inc - c0 - c1;
+                cur.off[2 * lane] = ex0;
+                cur.off[2 * lane + 1] = ex0 + c0;
+                const unsigned total = __shfl_sync(kFull, inc, 31);
+                if (lane == 0) {
+                    cur.total = total;
+                    if (tile == 0) {
+                        publish(p, 0, kFlagP, total, epoch);
+                        if (p.num_tiles == 1) p.ws->count = total;
+                    } else {
+                        publish(p, tile, kFlagA, total, epoch);
+                    }
+                }
+                __syncwarp();
+            }
+            if (DBG) { const unsigned long long t = clock64(); dce[1] += t - te; te = t; }
+            if (pend != kNone) {
+                TileT<kL>& prv = S.ts[pbuf];
+                unsigned long long ex = 0;
+                if (pend != 0) {
+                    ex = resolve(p, pend, epoch, lane, lb_rounds, lb_spins);
+                    if (lane == 0) {
+                        publish(p, pend, kFlagP, ex + prv.total, epoch);
+                        if (pend == p.num_tiles - 1) p.ws->count = ex + prv.total;
+                    }
+                }
+                if (DBG) { const unsigned long long t = clock64(); dce[2] += t - te; te = t; }
+#pragma unroll 1
+                for (unsigned w = 0; w < (unsigned)kW; ++w) emit_t(p, prv, pend, ex, w, lane, lt);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&S.buf_free[pbuf]);
+                if (DBG) { const unsigned long long t = clock64(); dce[3] += t - te; te = t; }
+            }
+            if (tile == kNone) break;
+            pend = tile;
+            pbuf = bi;
+        }
+        if (lane == 0) {
+            if (DBG) {
+                unsigned long long* d = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(p.ws) + kWsDbgOffset);
+                for (int i = 0; i < 4; ++i) atomicAdd(&d[16 + i], dce[i]);
+            }
+            if (lb_rounds) atomicAdd(&p.ws->lb_rounds, lb_rounds);
+            if (lb_spins) atomicAdd(&p.ws->lb_spins, lb_spins);
+            __threadfence();
+            const unsigned d = atomicAdd(&p.ws->k2_done, 1u);
+            if (d == gridDim.x - 1) {   // last block out: reset the tickets, bump the epoch
+                unsigned e = (epoch + 1u) & kEpochMask;
+                if (e == 0u) e = 1u;
+                p.ws->k2_ticket = 0u;
+                p.ws->k2_done = 0u;
+                p.ws->epoch = e;
+                __threadfence();
+            }
+        }
+        return;
+    }
+
+    // ================================================================ compute warps
+    // Pass A only: classify each sub-tile from the ring, build the per-warp
+    // survivor lists of super-tile k in buffer k % kBufs, signal the emit warp,
+    // go on with the next super-tile.  No block-wide barriers.
+    const int fast = p.fast;
+    unsigned seq = 0;
+    unsigned long long dc[2] = {0, 0}, t0 = 0;   // DBG: pass A, buffer waits
+    for (unsigned k = 0;; ++k) {
+        const unsigned bi = k % kBufs;
+        TileT<kL>& cur = S.ts[bi];
+        mbar_wait(&S.full[seq % kNst], (seq / kNst) & 1u);
+        const unsigned tile = S.stile[seq % kNst];
+        const bool have = tile != kNone;
+        if (DBG) t0 = clock64();
+        if (k >= (unsigned)kBufs) mbar_wait(&S.buf_free[bi], ((k / kBufs) - 1u) & 1u);
+        if (DBG) { const unsigned long long t = clock64(); dc[1] += t - t0; t0 = t; }
+        if (have) {
+            unsigned wc = 0;
+#pragma unroll 1
+            for (int sub = 0; sub < kK2Sub; ++sub, ++seq) {
+                const unsigned st = seq % kNst;
                 const unsigned bytes = sub_bytes(tile, sub, full_pairs);
                 const unsigned np = bytes / 16u;   // full pairs of this sub-tile in memory
-                if (threadIdx.x == kProd) produce(seq + 1u, seq + kNst);
-                const float4* chunk = &S.ring[seq % kNst][warp * kChunkPairs];
-                if (bytes) mbar_wait(&S.full[seq % kNst], (seq / kNst) & 1u);
+                const float4* chunk = &S.ring[st][warp * kChunkPairs];
+                mbar_wait(&S.full[st], (seq / kNst) & 1u);
                 unsigned needy = 0u;   // bit 2u + h: not decided by the fast test
                 if (np == (unsigned)kK2SubPairs) {
                     if (p.debug == 1) {   // perf experiment only: skeleton, no classification
@@ -305,7 +398,7 @@ __global__ void __launch_bounds__(kK2Threads, K2Cfg<CFG>::kMinB) k2_filter_tma(c
                         unsigned valid = 0u;
                         float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
                         if (pr < np) {
-                            v = S.ring[seq % kNst][pr];
+                            v = S.ring[st][pr];
                             valid = 3u;
                         } else if (odd && qs + pr == full_pairs) {
                             const float2 a = __ldg(reinterpret_cast<const float2*>(p.pts) + 2u * full_pairs);
@@ -347,7 +440,7 @@ __global__ void __launch_bounds__(kK2Threads, K2Cfg<CFG>::kMinB) k2_filter_tma(c
                             loc = S.qslot[warp][e];
                             const unsigned pr = warp * kChunkPairs + (loc >> 1);
                             if (pr < np) {
-                                q = reinterpret_cast<const float2*>(&S.ring[seq % kNst][0])[2u * pr + (loc & 1u)];
+                                q = reinterpret_cast<const float2*>(&S.ring[st][0])[2u * pr + (loc & 1u)];
                             } else {   // the unpaired last point
                                 q = __ldg(reinterpret_cast<const float2*>(p.pts) + 2u * full_pairs);
                             }
@@ -365,98 +458,36 @@ __global__ void __launch_bounds__(kK2Threads, K2Cfg<CFG>::kMinB) k2_filter_tma(c
                     }
                 }
                 __syncwarp();
-                if (bytes && lane == 0) mbar_arrive(&S.empty[seq % kNst]);
+                if (lane == 0) mbar_arrive(&S.empty[st]);
             }
             if (lane == 0) cur.lstart[warp][kK2Sub] = wc;
-            if (threadIdx.x == kProd) {
-                S.next = pnext;
-                // refill the stages just released so the ring stays full through
-                // the look-back / scan / survivor writes that follow
-                produce(0u, (k + 1) * kK2Sub + kNst);
-            }
         }
-        __syncthreads();   // pass A done everywhere; cur complete
-        const unsigned next = have ? S.next : kNone;
-        if (warp == 0 && pend != kNone) {
-            // decoupled look-back of the previous super-tile: its aggregate went
-            // out one tile-time ago, so its predecessors' are normally there too
-            unsigned long long ex = 0;
-            if (pend != 0) {
-                ex = resolve(p, pend, epoch, lane, lb_rounds, lb_spins);
-                if (lane == 0) {
-                    publish(p, pend, kFlagP, ex + prv.total, epoch);
-                    if (pend == p.num_tiles - 1) p.ws->count = ex + prv.total;
-                }
-            }
-            if (lane == 0) S.prefix = ex;
-        } else if (warp == 1 && have) {
-            // scan of the 64 group counts (group g = sub*kW + w, index order);
-            // lane l owns groups 2l, 2l+1 (sub-tile l/4, warps 2l%8 and +1)
-            const unsigned sub = lane >> 2, w0 = (2u * lane) & 7u;
-            const unsigned c0 = cur.lstart[w0][sub + 1] - cur.lstart[w0][sub];
-            const unsigned c1 = cur.lstart[w0 + 1][sub + 1] - cur.lstart[w0 + 1][sub];
-            unsigned inc = c0 + c1;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const unsigned y = __shfl_up_sync(kFull, inc, o);
-                if (lane >= (unsigned)o) inc += y;
-            }
-            const unsigned ex0 = inc - c0 - c1;
-            cur.off[2 * lane] = ex0;
-            cur.off[2 * lane + 1] = ex0 + c0;
-            const unsigned total = __shfl_sync(kFull, inc, 31);
-            if (lane == 0) {
-                cur.total = total;
-                if (tile == 0) {
-                    publish(p, 0, kFlagP, total, epoch);
-                    if (p.num_tiles == 1) p.ws->count = total;
-                } else {
-                    publish(p, tile, kFlagA, total, epoch);
-                }
-            }
-        }
-        __syncthreads();   // S.prefix, cur.off ready
-        if (pend != kNone) emit_t(p, prv, pend, S.prefix, warp, lane, lt);
-        // no barrier here: until the next pass-A barrier every warp writes only
-        // its own list / lstart / own bytes, which no other warp reads before it
+        if (warp == 0 && lane == 0) cur.tile = have ? tile : kNone;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&S.tile_done[bi]);
+        if (DBG) { const unsigned long long t = clock64(); dc[0] += t - t0; }
         if (!have) break;
-        pend = tile;
-        tile = next;
-        if (threadIdx.x == kProd) {   // producer moves to the next super-tile
-            pk += 1;
-            ptile = pnext;
-            pnext = kNone;
-        }
     }
-    if (threadIdx.x == 0) {
-        if (lb_rounds) atomicAdd(&p.ws->lb_rounds, lb_rounds);
-        if (lb_spins) atomicAdd(&p.ws->lb_spins, lb_spins);
-        __threadfence();
-        const unsigned d = atomicAdd(&p.ws->k2_done, 1u);
-        if (d == gridDim.x - 1) {
-            unsigned e = (epoch + 1u) & kEpochMask;
-            if (e == 0u) e = 1u;
-            p.ws->k2_ticket = 0u;
-            p.ws->k2_done = 0u;
-            p.ws->epoch = e;
-            __threadfence();
-        }
+    if (DBG && lane == 0) {
+        unsigned long long* d = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(p.ws) + kWsDbgOffset);
+        atomicAdd(&d[warp], dc[0]);
+        atomicAdd(&d[8 + warp], dc[1]);
     }
 }
 
-template <int EDGES, int CFG>
+template <int EDGES, int CFG, bool DBG = false>
 cudaError_t launch_tma_t(const K2Params& p, cudaStream_t s, int* launches) {
     static int max_blocks = 0;
     const int smem = (int)sizeof(SmemT<K2Cfg<CFG>::kNst, K2Cfg<CFG>::kL>);
     if (!max_blocks) {
-        cudaFuncSetAttribute(k2_filter_tma<EDGES, CFG>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(k2_filter_tma<EDGES, CFG, DBG>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2_filter_tma<EDGES, CFG>, kK2Threads, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2_filter_tma<EDGES, CFG, DBG>, kBlock, smem);
         max_blocks = (per_sm > 0 ? per_sm : 1) * device_sm_count();
     }
     unsigned blocks = p.num_tiles < (unsigned)max_blocks ? p.num_tiles : (unsigned)max_blocks;
     if (blocks < 1) blocks = 1;
-    k2_filter_tma<EDGES, CFG><<<blocks, kK2Threads, smem, s>>>(p);
+    k2_filter_tma<EDGES, CFG, DBG><<<blocks, kBlock, smem, s>>>(p);
     ++*launches;
     return cudaGetLastError();
 }
@@ -475,6 +506,8 @@ int k2_cfg() {
 
 int launch_filter_tma(const K2Params& p, void* stream, int* launches) {
     cudaStream_t s = (cudaStream_t)stream;
+    if (p.debug == 2)
+        return p.nv <= 16 ? (int)launch_tma_t<16, 0, true>(p, s, launches) : (int)launch_tma_t<32, 0, true>(p, s, launches);
     if (k2_cfg() == 1)
         return p.nv <= 16 ? (int)launch_tma_t<16, 1>(p, s, launches) : (int)launch_tma_t<32, 1>(p, s, launches);
     return p.nv <= 16 ? (int)launch_tma_t<16, 0>(p, s, launches) : (int)launch_tma_t<32, 0>(p, s, launches);
