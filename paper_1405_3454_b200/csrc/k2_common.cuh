@@ -144,7 +144,7 @@ __device__ __forceinline__ unsigned long long resolve(const K2Params& p, unsigne
         ++rounds;
         if (imask & need) {
             ++spins;
-            __nanosleep(64);
+            __nanosleep(128);
             continue;
         }
         unsigned long long v = (lane <= lim) ? sum : 0ull;

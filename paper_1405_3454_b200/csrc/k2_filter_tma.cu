@@ -222,6 +222,10 @@ __global__ void __launch_bounds__(kBlock, K2Cfg<CFG>::kMinB) k2_filter_tma(const
         mbar_fence_init();
     }
     __syncthreads();   // the only whole-block barrier
+    // shared-window addresses of the mbarriers and the ring (hot loops use these)
+    const unsigned a_full = smem_u32(&S.full[0]), a_empty = smem_u32(&S.empty[0]);
+    const unsigned a_done = smem_u32(&S.tile_done[0]), a_free = smem_u32(&S.buf_free[0]);
+    const unsigned a_ring = smem_u32(&S.ring[0][0]);
 
     // ================================================================ producer warp
     // Lane 0 takes super-tile tickets (the next one while issuing the current
@@ -240,15 +244,15 @@ __global__ void __launch_bounds__(kBlock, K2Cfg<CFG>::kMinB) k2_filter_tma(const
 #pragma unroll 1
                 for (int sub = 0; sub < (valid ? kK2Sub : 1); ++sub, ++seq) {
                     const unsigned st = seq % kNst;
-                    if (seq >= (unsigned)kNst) mbar_wait(&S.empty[st], ((seq / kNst) - 1u) & 1u);
+                    if (seq >= (unsigned)kNst) mbar_sleep_wait(a_empty + 8u * st, ((seq / kNst) - 1u) & 1u);
                     if (sub == 0) S.stile[st] = valid ? t : kNone;
                     const unsigned bytes = valid ? sub_bytes(t, sub, full_pairs) : 0u;
                     if (bytes) {
-                        mbar_expect_tx(&S.full[st], bytes);
-                        bulk_g2s(&S.ring[st][0], src + (size_t)t * kK2TilePairs + sub * kK2SubPairs, bytes,
-                                 &S.full[st]);
+                        mbar_expect_tx_a(a_full + 8u * st, bytes);
+                        bulk_g2s_a(a_ring + st * (16u * kK2SubPairs), src + (size_t)t * kK2TilePairs + sub * kK2SubPairs,
+                                   bytes, a_full + 8u * st);
                     } else {
-                        mbar_arrive(&S.full[st]);
+                        mbar_arrive_a(a_full + 8u * st);
                     }
                 }
                 if (!valid) break;
@@ -273,7 +277,7 @@ __global__ void __launch_bounds__(kBlock, K2Cfg<CFG>::kMinB) k2_filter_tma(const
             const unsigned bi = k % kBufs;
             TileT<kL>& cur = S.ts[bi];
             if (DBG) te = clock64();
-            mbar_wait(&S.tile_done[bi], (k / kBufs) & 1u);
+            mbar_sleep_wait(a_done + 8u * bi, (k / kBufs) & 1u);
             if (DBG) { const unsigned long long t = clock64(); dce[0] += t - te; te = t; }
             const unsigned tile = cur.tile;
             if (tile != kNone) {
@@ -313,10 +317,13 @@ __global__ void __launch_bounds__(kBlock, K2Cfg<CFG>::kMinB) k2_filter_tma(const
                     }
                 }
                 if (DBG) { const unsigned long long t = clock64(); dce[2] += t - te; te = t; }
+                // per-warp passes (measured faster than one flat pass over the tile:
+                // a quicker emit warp reaches the next look-back before the
+                // other blocks' aggregates are out and spins; r01_experiments.md)
 #pragma unroll 1
                 for (unsigned w = 0; w < (unsigned)kW; ++w) emit_t(p, prv, pend, ex, w, lane, lt);
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&S.buf_free[pbuf]);
+                if (lane == 0) mbar_arrive_a(a_free + 8u * pbuf);
                 if (DBG) { const unsigned long long t = clock64(); dce[3] += t - te; te = t; }
             }
             if (tile == kNone) break;
@@ -354,11 +361,11 @@ __global__ void __launch_bounds__(kBlock, K2Cfg<CFG>::kMinB) k2_filter_tma(const
     for (unsigned k = 0;; ++k) {
         const unsigned bi = k % kBufs;
         TileT<kL>& cur = S.ts[bi];
-        mbar_wait(&S.full[seq % kNst], (seq / kNst) & 1u);
+        mbar_sleep_wait(a_full + 8u * (seq % kNst), (seq / kNst) & 1u);
         const unsigned tile = S.stile[seq % kNst];
         const bool have = tile != kNone;
         if (DBG) t0 = clock64();
-        if (k >= (unsigned)kBufs) mbar_wait(&S.buf_free[bi], ((k / kBufs) - 1u) & 1u);
+        if (k >= (unsigned)kBufs) mbar_sleep_wait(a_free + 8u * bi, ((k / kBufs) - 1u) & 1u);
         if (DBG) { const unsigned long long t = clock64(); dc[1] += t - t0; t0 = t; }
         if (have) {
             unsigned wc = 0;
@@ -368,7 +375,7 @@ __global__ void __launch_bounds__(kBlock, K2Cfg<CFG>::kMinB) k2_filter_tma(const
                 const unsigned bytes = sub_bytes(tile, sub, full_pairs);
                 const unsigned np = bytes / 16u;   // full pairs of this sub-tile in memory
                 const float4* chunk = &S.ring[st][warp * kChunkPairs];
-                mbar_wait(&S.full[st], (seq / kNst) & 1u);
+                mbar_sleep_wait(a_full + 8u * st, (seq / kNst) & 1u);
                 unsigned needy = 0u;   // bit 2u + h: not decided by the fast test
                 if (np == (unsigned)kK2SubPairs) {
                     if (p.debug == 1) {   // perf experiment only: skeleton, no classification
@@ -409,27 +416,23 @@ __global__ void __launch_bounds__(kBlock, K2Cfg<CFG>::kMinB) k2_filter_tma(const
                         needy |= (valid & ~in) << (2 * u);
                     }
                 }
-                // ---- index-ordered queue: slot of (u, lane, h) = sum_{u'<u} T_u'
-                //      + (needy points of pair u in lanes < lane) + (h ? bit(2u) : 0)
-                const unsigned cnt = __popc(needy & 0x03u) | (__popc(needy & 0x0cu) << 8) |
-                                     (__popc(needy & 0x30u) << 16) | (__popc(needy & 0xc0u) << 24);
-                unsigned incl = cnt;   // 4 packed 8-bit fields, each <= 64
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const unsigned y = __shfl_up_sync(kFull, incl, o);
-                    if (lane >= (unsigned)o) incl += y;
-                }
-                const unsigned T = __shfl_sync(kFull, incl, 31);
-                const unsigned qtotal = (T & 0xffu) + ((T >> 8) & 0xffu) + ((T >> 16) & 0xffu) + (T >> 24);
+                // ---- index-ordered queue: slot of (u, lane, h) = (needy points of
+                //      pairs u' < u in the whole chunk) + (needy points of pair u in
+                //      lanes < lane) + (h ? bit(u, 0) : 0), from 8 independent ballots
+                //      (a few dependent levels instead of a shuffle scan + a loop)
                 if (lane == 0) cur.lstart[warp][sub] = wc;
                 cur.own[sub][warp][lane] = 0;
+                unsigned qtotal = 0;
+#pragma unroll
+                for (int u = 0; u < kK2Items; ++u) {
+                    const unsigned n0 = (needy >> (2 * u)) & 1u, n1 = (needy >> (2 * u + 1)) & 1u;
+                    const unsigned b0 = __ballot_sync(kFull, n0), b1 = __ballot_sync(kFull, n1);
+                    const unsigned slot = qtotal + __popc(b0 & lt) + __popc(b1 & lt);
+                    if (n0) S.qslot[warp][slot] = (unsigned char)((u << 6) | (lane << 1));
+                    if (n1) S.qslot[warp][slot + n0] = (unsigned char)((u << 6) | (lane << 1) | 1u);
+                    qtotal += __popc(b0) + __popc(b1);
+                }
                 if (qtotal) {
-                    const unsigned sb = (T << 8) + (T << 16) + (T << 24) + (incl - cnt);   // fields <= 254
-                    for (unsigned m = needy; m; m &= m - 1u) {
-                        const unsigned b = __ffs(m) - 1u, u = b >> 1, h = b & 1u;
-                        const unsigned slot = ((sb >> (8u * u)) & 0xffu) + (h & (needy >> (2u * u)));
-                        S.qslot[warp][slot] = (unsigned char)((u << 6) | (lane << 1) | h);
-                    }
                     __syncwarp();
                     for (unsigned base = 0; base < qtotal; base += 32) {
                         const unsigned e = base + lane;
@@ -458,13 +461,15 @@ __global__ void __launch_bounds__(kBlock, K2Cfg<CFG>::kMinB) k2_filter_tma(const
                     }
                 }
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&S.empty[st]);
+                if (lane == 0) mbar_arrive_a(a_empty + 8u * st);
             }
             if (lane == 0) cur.lstart[warp][kK2Sub] = wc;
         }
         if (warp == 0 && lane == 0) cur.tile = have ? tile : kNone;
         __syncwarp();
-        if (lane == 0) mbar_arrive(&S.tile_done[bi]);
+        if (lane == 0) {
+            mbar_arrive_a(a_done + 8u * bi);
+        }
         if (DBG) { const unsigned long long t = clock64(); dc[0] += t - t0; }
         if (!have) break;
     }

@@ -41,5 +41,30 @@ __device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+// ---- the same on precomputed shared-window addresses (hot loops: no
+// generic -> shared conversion per call).  mbar_sleep_wait passes a
+// suspend-time hint, so a waiting warp is parked by the hardware until the
+// phase completes instead of re-issuing try_wait (spinning steals issue slots
+// from the warps that do the work).
+__device__ __forceinline__ void mbar_sleep_wait(unsigned bar, unsigned parity) {
+    asm volatile(
+        "{\n .reg .pred P1;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
+        " @!P1 bra WAIT_%=;\n }" ::"r"(bar),
+        "r"(parity), "r"(0x989680u)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_a(unsigned bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx_a(unsigned bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s_a(unsigned dst, const void* src, unsigned bytes, unsigned bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+        "l"(src), "r"(bytes), "r"(bar)
+        : "memory");
+}
+
 }  // namespace
 }  // namespace cudapre
