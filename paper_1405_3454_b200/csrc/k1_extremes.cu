@@ -307,8 +307,9 @@ __global__ void __launch_bounds__(kSeedThreads) k1_seed(const K1Params p) {
 }
 
 // ---------------------------------------------------------------- main kernel
+// TMA: one extra (producer) warp
 template <int NANG, bool VEC, bool TMA>
-__global__ void __launch_bounds__(kK1Threads, 2) k1_extremes(const K1Params p) {
+__global__ void __launch_bounds__(kK1Threads + (TMA ? 32 : 0), 2) k1_extremes(const K1Params p) {
     constexpr int NS = 4 * NANG;
     constexpr int kWarps = kK1Threads / 32;
     __shared__ WarpState<NANG> sst[kWarps];
@@ -316,7 +317,7 @@ __global__ void __launch_bounds__(kK1Threads, 2) k1_extremes(const K1Params p) {
     __shared__ unsigned sqi[kWarps][kK1Queue];
     __shared__ bool s_last;
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    WarpState<NANG>& st = sst[warp];
+    WarpState<NANG>& st = sst[warp < (unsigned)kWarps ? warp : 0u];   // (TMA producer warp: unused)
 
     // thresholds from the seed (0 = no seed)
     float T[NS];
@@ -328,7 +329,7 @@ __global__ void __launch_bounds__(kK1Threads, 2) k1_extremes(const K1Params p) {
         else
             T[s] = e ? dec_f(~e) : INFINITY;
     }
-    if (lane < NS) {
+    if (lane < NS && warp < (unsigned)kWarps) {
         st.key[lane] = is_max_slot(lane) ? -INFINITY : INFINITY;
         st.idx[lane] = kNoIdx;
     }
@@ -443,37 +444,49 @@ __global__ void __launch_bounds__(kK1Threads, 2) k1_extremes(const K1Params p) {
     };
     if constexpr (TMA) {
         // Chunks of kK1StagePairs pairs (16 KiB) stream through a kK1Stages-deep
-        // shared-memory ring filled by cp.async.bulk (TMA) and completed on
-        // mbarriers: deep memory-level parallelism without holding loads in
-        // registers.  Chunk c goes to block c % gridDim.x.
+        // shared-memory ring filled by cp.async.bulk (TMA): a dedicated producer
+        // warp (warp kWarps, one lane) issues chunk i once every compute warp
+        // has released stage i % kK1Stages ("empty" mbarrier, kWarps arrivals);
+        // compute warps wait on the stage's transaction-counting "full"
+        // mbarrier.  No block-wide barrier in the loop.  Chunk c goes to block
+        // c % gridDim.x.
         extern __shared__ __align__(128) float4 ring[];
-        __shared__ unsigned long long fullb[kK1Stages];
+        __shared__ unsigned long long fullb[kK1Stages], emptyb[kK1Stages];
         const unsigned nchunks = full_pairs / kK1StagePairs;
         const unsigned mine =
             blockIdx.x < nchunks ? (nchunks - blockIdx.x + gridDim.x - 1) / gridDim.x : 0u;
-        const float4* src = reinterpret_cast<const float4*>(p.pts);
-        auto issue = [&](unsigned i) {
-            const unsigned sidx = i % kK1Stages;
-            const unsigned chunk = blockIdx.x + i * gridDim.x;
-            mbar_expect_tx(&fullb[sidx], kK1StagePairs * 16u);
-            bulk_g2s(&ring[sidx * kK1StagePairs], src + (size_t)chunk * kK1StagePairs, kK1StagePairs * 16u,
-                     &fullb[sidx]);
-        };
         if (threadIdx.x == 0) {
-            for (int k = 0; k < kK1Stages; ++k) mbar_init(&fullb[k], 1u);
+            for (int k = 0; k < kK1Stages; ++k) {
+                mbar_init(&fullb[k], 1u);
+                mbar_init(&emptyb[k], (unsigned)kWarps);
+            }
             mbar_fence_init();
-            for (unsigned i = 0; i < (unsigned)kK1Stages && i < mine; ++i) issue(i);
         }
         __syncthreads();
-        for (unsigned i = 0; i < mine; ++i) {
-            const unsigned sidx = i % kK1Stages;
-            mbar_wait(&fullb[sidx], (i / kK1Stages) & 1u);
-            float4 v[kK1Unroll];
+        const unsigned a_full = smem_u32(&fullb[0]), a_empty = smem_u32(&emptyb[0]), a_ring = smem_u32(ring);
+        if (warp == (unsigned)kWarps) {
+            if (lane == 0) {
+                const float4* src = reinterpret_cast<const float4*>(p.pts);
+                for (unsigned i = 0; i < mine; ++i) {
+                    const unsigned sidx = i % kK1Stages;
+                    if (i >= (unsigned)kK1Stages) mbar_sleep_wait(a_empty + 8u * sidx, ((i / kK1Stages) - 1u) & 1u);
+                    mbar_expect_tx_a(a_full + 8u * sidx, kK1StagePairs * 16u);
+                    bulk_g2s_a(a_ring + sidx * (kK1StagePairs * 16u),
+                               src + (size_t)(blockIdx.x + i * gridDim.x) * kK1StagePairs, kK1StagePairs * 16u,
+                               a_full + 8u * sidx);
+                }
+            }
+        } else {
+            for (unsigned i = 0; i < mine; ++i) {
+                const unsigned sidx = i % kK1Stages;
+                mbar_sleep_wait(a_full + 8u * sidx, (i / kK1Stages) & 1u);
+                float4 v[kK1Unroll];
 #pragma unroll
-            for (int u = 0; u < kK1Unroll; ++u) v[u] = ring[sidx * kK1StagePairs + u * kK1Threads + threadIdx.x];
-            process(v, (blockIdx.x + i * gridDim.x) * kK1StagePairs + threadIdx.x);
-            __syncthreads();   // every warp is done with this stage: refill it
-            if (threadIdx.x == 0 && i + kK1Stages < mine) issue(i + kK1Stages);
+                for (int u = 0; u < kK1Unroll; ++u) v[u] = ring[sidx * kK1StagePairs + u * kK1Threads + threadIdx.x];
+                __syncwarp();
+                if (lane == 0) mbar_arrive_a(a_empty + 8u * sidx);   // data now in registers
+                process(v, (blockIdx.x + i * gridDim.x) * kK1StagePairs + threadIdx.x);
+            }
         }
         q0 = nchunks * kK1StagePairs + blockIdx.x * (kK1Threads * kK1Unroll) + threadIdx.x;
     } else if (full(q0)) {
@@ -493,6 +506,7 @@ __global__ void __launch_bounds__(kK1Threads, 2) k1_extremes(const K1Params p) {
             for (int u = 0; u < kK1Unroll; ++u) v[u] = vn[u];
         }
     }
+    if (!TMA || warp < (unsigned)kWarps) {   // (TMA: the producer warp has no warp state)
     drain(true);
     // remainder (guarded)
     for (; q0 - lane < npairs; q0 += stride) {
@@ -524,6 +538,7 @@ __global__ void __launch_bounds__(kK1Threads, 2) k1_extremes(const K1Params p) {
         }
         if (__any_sync(kFull, cand)) refresh_thresholds<NANG>(T, st);
     }
+    }
 
     // ---- warp states -> block partial
     __syncthreads();
@@ -554,7 +569,7 @@ __global__ void __launch_bounds__(kK1Threads, 2) k1_extremes(const K1Params p) {
     // ---- last block: reduce all block partials, write the result, reset
     __threadfence();
     cudapre_extremes_t* outs[2] = {&p.ws->result, p.d_out};
-    for (int s = warp; s < NS; s += kWarps) {
+    for (int s = warp; s < NS && warp < (unsigned)kWarps; s += kWarps) {
         const bool mx = is_max_slot(s);
         double K = mx ? -INFINITY : INFINITY;
         unsigned I = kNoIdx;
@@ -632,7 +647,7 @@ cudaError_t launch_t(const K1Params& p, cudaStream_t s, int* launches) {
         if (TMA)
             cudaFuncSetAttribute(k1_extremes<NANG, VEC, TMA>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1_extremes<NANG, VEC, TMA>, kK1Threads, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1_extremes<NANG, VEC, TMA>, kK1Threads + (TMA ? 32 : 0), smem);
         const int sms = device_sm_count();
         k1_blocks = per_sm * sms;
         if (k1_blocks > kMaxK1Blocks) k1_blocks = kMaxK1Blocks;
@@ -648,7 +663,7 @@ cudaError_t launch_t(const K1Params& p, cudaStream_t s, int* launches) {
         k1_seed<NANG, VEC><<<sb, kSeedThreads, 0, s>>>(p);
         ++*launches;
     }
-    k1_extremes<NANG, VEC, TMA><<<blocks, kK1Threads, smem, s>>>(p);
+    k1_extremes<NANG, VEC, TMA><<<blocks, kK1Threads + (TMA ? 32 : 0), smem, s>>>(p);
     ++*launches;
     return cudaGetLastError();
 }
