@@ -138,7 +138,9 @@ const char* cudapre_last_error(void);
 
 /* Angle presets (A1).  preset 0 = {0, 30, 45, 60} degrees (default);
  * preset 1 = {0, 30, 45, 45} (P:25, P:35 literal text); preset 2 = {0}
- * (Akl-Toussaint quadrilateral); preset 3 = {0, 22.5, 45, 67.5}.
+ * (Akl-Toussaint quadrilateral); preset 3 = {0, 22.5, 45, 67.5}
+ * (even spacing); preset 4 = {0, 15, 22.5, 30, 45, 60, 67.5, 75} ("more
+ * angles": 32 extremes, rings of up to 32 vertices).
  * Writes *nang and the correctly rounded c[k] = cos, s[k] = sin (A5) into
  * caller arrays of CUDAPRE_MAX_ANGLES doubles.  INVALID_ARGUMENT for an
  * unknown preset.                                                          */

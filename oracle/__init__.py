@@ -68,7 +68,7 @@ def _ptr(a: np.ndarray):
 
 
 PRESETS = {"A": (0.0, 30.0, 45.0, 60.0), "B": (0.0, 30.0, 45.0, 45.0), "AT": (0.0,),
-           "C": (0.0, 22.5, 45.0, 67.5)}
+           "C": (0.0, 22.5, 45.0, 67.5), "D": (0.0, 15.0, 22.5, 30.0, 45.0, 60.0, 67.5, 75.0)}
 
 
 def coeffs(angles) -> tuple[np.ndarray, np.ndarray]:

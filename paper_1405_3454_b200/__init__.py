@@ -34,7 +34,7 @@ SECTORS = 1024
 OK, ERR_EMPTY, ERR_ARG, ERR_NONFINITE, ERR_CUDA, ERR_CAPACITY, ERR_WORKSPACE = range(7)
 _STATUS = {1: "EMPTY_INPUT", 2: "INVALID_ARGUMENT", 3: "NONFINITE_INPUT", 4: "CUDA",
            5: "CAPACITY", 6: "WORKSPACE"}
-PRESETS = {"A": 0, "B": 1, "AT": 2, "C": 3}   # {0,30,45,60} {0,30,45,45} {0} {0,22.5,45,67.5}
+PRESETS = {"A": 0, "B": 1, "AT": 2, "C": 3, "D": 4}   # {0,30,45,60} {0,30,45,45} {0} {0,22.5,45,67.5} {0,15,..,75}
 
 
 class CudaPreError(RuntimeError):

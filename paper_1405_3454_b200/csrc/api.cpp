@@ -70,18 +70,20 @@ cudapre_status events(cudaEvent_t** out) {
 
 // Correctly rounded coefficients (reading A5): the binary64 nearest to the
 // exact cos/sin of each angle.  Typed from the closed forms sqrt(3)/2,
-// sqrt(2)/2, sqrt(2 +- sqrt(2))/2 (tests/test_abi.py checks them against
+// sqrt(2)/2, sqrt(2 +- sqrt(2))/2, (sqrt(6) +- sqrt(2))/4 (tests/test_abi.py checks them against
 // 80-digit decimal evaluations).
 struct Coef {
     double deg, c, s;
 };
 const Coef kCoef[] = {
     {0.0, 1.0, 0.0},
+    {15.0, 0x1.ee8dd4748bf15p-1, 0x1.0907dc1930690p-2},   // (sqrt6 +- sqrt2)/4
     {22.5, 0x1.d906bcf328d46p-1, 0x1.87de2a6aea963p-2},
     {30.0, 0x1.bb67ae8584caap-1, 0x1.0p-1},
     {45.0, 0x1.6a09e667f3bcdp-1, 0x1.6a09e667f3bcdp-1},
     {60.0, 0x1.0p-1, 0x1.bb67ae8584caap-1},
     {67.5, 0x1.87de2a6aea963p-2, 0x1.d906bcf328d46p-1},
+    {75.0, 0x1.0907dc1930690p-2, 0x1.ee8dd4748bf15p-1},
 };
 
 void preset_coef(double deg, double* c, double* s) {
@@ -139,10 +141,13 @@ const char* cudapre_version(void) { return "cudapre-b200 0.1.0 (sm_100a)"; }
 const char* cudapre_last_error(void) { return g_err.c_str(); }
 
 cudapre_status cudapre_angles_preset(int preset, int32_t* nang, double* c, double* s) {
-    static const double lists[4][4] = {
-        {0.0, 30.0, 45.0, 60.0}, {0.0, 30.0, 45.0, 45.0}, {0.0, 0, 0, 0}, {0.0, 22.5, 45.0, 67.5}};
-    static const int counts[4] = {4, 4, 1, 4};
-    if (preset < 0 || preset > 3 || !nang || !c || !s)
+    static const double lists[5][8] = {{0.0, 30.0, 45.0, 60.0},
+                                       {0.0, 30.0, 45.0, 45.0},
+                                       {0.0},
+                                       {0.0, 22.5, 45.0, 67.5},
+                                       {0.0, 15.0, 22.5, 30.0, 45.0, 60.0, 67.5, 75.0}};
+    static const int counts[5] = {4, 4, 1, 4, 8};
+    if (preset < 0 || preset > 4 || !nang || !c || !s)
         return fail(CUDAPRE_ERR_INVALID_ARGUMENT, "unknown angle preset %d", preset);
     *nang = counts[preset];
     for (int k = 0; k < CUDAPRE_MAX_ANGLES; ++k) c[k] = s[k] = 0.0;

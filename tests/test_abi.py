@@ -62,6 +62,11 @@ def test_angle_presets_correctly_rounded(L):
         "C": [(1, 0), ((2 + s2).sqrt() / 2, (2 - s2).sqrt() / 2), (s2 / 2, s2 / 2),
               ((2 - s2).sqrt() / 2, (2 + s2).sqrt() / 2)],
     }
+    s6 = Decimal(6).sqrt()
+    c15, s15 = (s6 + s2) / 4, (s6 - s2) / 4
+    c225, s225 = (2 + s2).sqrt() / 2, (2 - s2).sqrt() / 2
+    want["D"] = [(1, 0), (c15, s15), (c225, s225), (s3 / 2, Decimal(1) / 2), (s2 / 2, s2 / 2),
+                 (Decimal(1) / 2, s3 / 2), (s225, c225), (s15, c15)]
     for name, cs in want.items():
         n, c, s = cp.angles(name)
         assert n == len(cs)
@@ -128,7 +133,7 @@ def test_product_orient_vs_fractions(L, oracle_lib):
 
 
 @pytest.mark.parametrize("family", ["square", "disk", "gauss", "circle"])
-@pytest.mark.parametrize("angles", ["A", "B", "C", "AT"])
+@pytest.mark.parametrize("angles", ["A", "B", "C", "AT", "D"])
 def test_polygon_matches_oracle(L, oracle_lib, family, angles):
     xy = synth.generate(family, 20_000, seed=5)
     ext = cp.Extremes(_ext_from_oracle(oracle_lib, xy, angles))

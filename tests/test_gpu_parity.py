@@ -72,7 +72,7 @@ SIZES = [1, 2, 3, 5, 31, 32, 33, 513, 2047, 2048, 2049, 4097, 65_537, 100_003, 2
 
 
 @pytest.mark.parametrize("family", synth.FAMILIES)
-@pytest.mark.parametrize("angles", ["A", "B", "C", "AT"])
+@pytest.mark.parametrize("angles", ["A", "B", "C", "AT", "D"])
 def test_parity_sizes(family, angles):
     for n in SIZES:
         xy = synth.generate(family, n, seed=n + 7)
@@ -261,21 +261,26 @@ def test_nccl_group_path_under_torchrun():
     assert "nccl ok" in res.stdout
 
 
-def test_register_k2_fallback_matches():
-    """CUDAPRE_K2_TMA=0 routes 16-B aligned input through the register K2
-    kernel; it must give the same bytes (separate process: the switch is read
-    once per process)."""
+@pytest.mark.parametrize("k1_tma,k2_tma", [("0", "0"), ("0", "1"), ("1", "0")])
+def test_register_kernel_fallbacks_match(k1_tma, k2_tma):
+    """CUDAPRE_K1_TMA=0 / CUDAPRE_K2_TMA=0 route 16-B aligned input through
+    the register-loading K1 / K2 kernels instead of the warp-specialised
+    cp.async.bulk ones; they must give the same bytes: extreme indices and
+    survivors (separate process: the switches are read once per process)."""
     import subprocess
     import sys
 
     code = ("import numpy as np, torch, oracle, synth, paper_1405_3454_b200 as cp\n"
             "for fam, n in (('disk', 1000003), ('square', 400001), ('circle', 300007)):\n"
             "    xy = synth.generate(fam, n, seed=3)\n"
-            "    idx, sp, rep = cp.cuda_pre(torch.from_numpy(xy).cuda())\n"
+            "    d = torch.from_numpy(xy).cuda()\n"
+            "    ext = cp.extremes(d, 'A')\n"
+            "    assert np.array_equal(ext.idx, oracle.extremes(xy, 'A', threads=8)), fam\n"
+            "    idx, sp, rep = cp.cuda_pre(d)\n"
             "    want = oracle.cudapre(xy, 'A', threads=8)\n"
             "    assert np.array_equal(idx.cpu().numpy(), want['survivors']), fam\n"
             "print('reg ok')\n")
-    env = dict(os.environ, CUDAPRE_K2_TMA="0")
+    env = dict(os.environ, CUDAPRE_K1_TMA=k1_tma, CUDAPRE_K2_TMA=k2_tma)
     res = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600,
                          env=env, cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     assert res.returncode == 0 and "reg ok" in res.stdout, res.stderr[-3000:]
