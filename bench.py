@@ -194,7 +194,7 @@ def main():
     base = rank * (n_total // world) + min(rank, n_total % world)
     pts = scuda.generate(family, n_local, seed=seed, base=base, **cfg)
     ws = cp.Workspace(n_local)
-    cap = max(1024, n_local // 8)
+    cap = n_local if n_local <= 250_000_000 else n_local // 8   # dense configs (C4) keep ~all points
     out_idx = torch.empty(cap, dtype=torch.int64, device="cuda")
     out_pts = torch.empty((cap, 2), dtype=torch.float32, device="cuda")
     torch.cuda.synchronize()

@@ -103,6 +103,20 @@ unsigned long long* ws_status(void* d_ws) {
     return reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(d_ws) + kWsHeaderBytes +
                                                  kWsPartialBytes);
 }
+// The overflow scratch sits at the END of the caller's workspace: the
+// tile-status words start at a fixed offset and are epoch-tagged across calls,
+// so a workspace reused for a smaller n must never write scratch data where a
+// larger n's status words live (status(n) grows from the front, scratch from
+// the back; ws_bytes >= ws_bytes_for(n) keeps them apart).
+SurvEntry* ws_scratch(void* d_ws, size_t ws_bytes, int64_t n, unsigned* blocks) {
+    const size_t used = kWsHeaderBytes + kWsPartialBytes + ws_status_bytes(n);
+    size_t nb = ws_bytes > used + 16 ? (ws_bytes - used - 16) / kK2ScratchPerBlock : 0;
+    const size_t want = (size_t)kK2BlocksPerSM * (size_t)device_sm_count();
+    if (nb > want) nb = want;
+    *blocks = (unsigned)nb;
+    const size_t off = (ws_bytes - nb * kK2ScratchPerBlock) & ~(size_t)15;
+    return reinterpret_cast<SurvEntry*>(reinterpret_cast<char*>(d_ws) + off);
+}
 
 cudapre_status check_points(const cudapre_pt* d_pts, int64_t n) {
     if (n < 0 || n > (int64_t)0xffffffffll)
@@ -325,6 +339,7 @@ cudapre_status cudapre_filter(const cudapre_pt* d_pts, int64_t n_local, int64_t 
     p.capacity = (unsigned long long)capacity;
     p.ws = ws_header(d_ws);
     p.status = ws_status(d_ws);
+    p.scratch = ws_scratch(d_ws, ws_bytes, n_local, &p.scratch_blocks);
     p.num_tiles = (unsigned)((n_local + kK2TilePts - 1) / kK2TilePts);   // the TMA launcher re-derives its own
     const int vec16 = (((uintptr_t)d_pts & 15u) == 0);
     {

@@ -26,6 +26,7 @@ constexpr int kMaxK1Blocks = 148 * 16;
 // ---------------------------------------------------------------- workspace
 // Device workspace layout (caller-owned, zero-filled once):
 //   [WsHeader, padded to 4 KiB][K1Partial x kMaxK1Blocks x 32][tile status x ntiles]
+//   ... [TMA K2 list-overflow scratch, at the END of the buffer]
 // Every kernel leaves the counters it uses back at their reset values, so the
 // workspace stays valid from call to call.
 struct alignas(16) WsHeader {
@@ -64,8 +65,27 @@ constexpr size_t kWsPartialBytes = sizeof(K1Partial) * kMaxK1Blocks * CUDAPRE_MA
 constexpr int kStatusTilePts = kK2TilePts;
 constexpr int kStatusStride = 16;   // u64 words per status line (128 B)
 inline size_t ws_tiles(int64_t n) { return (size_t)((n + kStatusTilePts - 1) / kStatusTilePts); }
-inline size_t ws_bytes_for(int64_t n) {
-    return kWsHeaderBytes + kWsPartialBytes + 8 * kStatusStride * (ws_tiles(n) + 1);
+inline size_t ws_status_bytes(int64_t n) { return 8 * kStatusStride * (ws_tiles(n) + 1); }
+
+// TMA K2 survivor-list overflow: a warp's list entries beyond its shared-memory
+// capacity go to global scratch, per (resident block, list buffer, warp), sized
+// for the worst case (every point of the warp's 2048-point share survives).
+struct SurvEntry {
+    float x, y;
+    unsigned meta;   // (sub-tile << 8) | offset in the warp's 256-point chunk
+};
+constexpr int kK2Bufs = 3;                          // survivor-list buffers per block
+constexpr int kK2WarpPts = kK2Sub * 256;            // 2048 points per warp per super-tile
+constexpr size_t kK2ScratchPerBlock = (size_t)kK2Bufs * 8 * kK2WarpPts * sizeof(SurvEntry);
+constexpr int kK2BlocksPerSM = 2;
+int device_sm_count();
+inline size_t ws_scratch_blocks(int64_t n) {
+    const size_t cap = (size_t)kK2BlocksPerSM * (size_t)device_sm_count();
+    const size_t t = ws_tiles(n);
+    return t < cap ? t : cap;
+}
+inline size_t ws_bytes_for(int64_t n) {   // (+16: alignment slack of the scratch at the end)
+    return kWsHeaderBytes + kWsPartialBytes + ws_status_bytes(n) + kK2ScratchPerBlock * ws_scratch_blocks(n) + 16;
 }
 
 // ---------------------------------------------------------------- kernel params
@@ -107,6 +127,8 @@ struct K2Params {
     // cyclically); 0xffff = more than two (or no table): test every edge
     unsigned short sedge[CUDAPRE_SECTORS + 1];
     int fast;                 // TMA K2 pass-A test: 0 = inner disk, 1 = inner box (the larger)
+    SurvEntry* scratch;       // TMA K2 list overflow, kK2ScratchPerBlock per block
+    unsigned int scratch_blocks;   // blocks the scratch region covers (caps the TMA K2 grid)
 };
 
 // ---------------------------------------------------------------- launchers (.cu)
@@ -115,7 +137,6 @@ int launch_extremes(const K1Params& p, int vec16, void* stream, int* launches);
 int launch_filter(const K2Params& p, int vec16, void* stream, int* launches);
 int launch_filter_tma(const K2Params& p, void* stream, int* launches);   // vec16, mode 0
 int k2_use_tma();   // CUDAPRE_K2_TMA (default 1)
-int device_sm_count();
 
 // ---------------------------------------------------------------- host geometry (host_geom.cpp)
 int orient_exact(float ax, float ay, float bx, float by, float cx, float cy);

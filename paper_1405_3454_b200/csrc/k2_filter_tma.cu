@@ -46,12 +46,10 @@ constexpr unsigned kChunkPairs = kK2SubPairs / kW;   // 128 pairs = 256 points p
 constexpr unsigned kNone = 0xffffffffu;
 constexpr unsigned kBlock = kK2Threads + 64;         // 8 compute warps + producer warp + emit warp
 constexpr unsigned kProdWarp = kW, kEmitWarp = kW + 1;
-constexpr int kBufs = 3;                             // survivor-list buffers (tiles in flight)
+constexpr int kBufs = kK2Bufs;                       // survivor-list buffers (tiles in flight)
 
-struct SurvT {
-    float x, y;
-    unsigned meta;   // (sub << 8) | loc,  loc = u*64 + lane*2 + h = point offset in the warp chunk
-};
+using SurvT = SurvEntry;   // meta = (sub << 8) | loc, loc = u*64 + lane*2 + h = point offset in the warp chunk
+static_assert(kK2Bufs == 3 && kK2WarpPts == kK2Sub * 2 * (int)(kK2SubPairs / (kK2Threads / 32)), "layout");
 
 template <unsigned kL>
 struct TileT {
@@ -60,7 +58,6 @@ struct TileT {
     unsigned off[kGroups];              // exclusive offset of group sub*kW + warp in the super-tile
     unsigned total;
     unsigned tile;                      // super-tile id (kNone: end of work)
-    unsigned char own[kK2Sub][kW][32];  // keep bits per lane (bit 2u+h): list-overflow path only
 };
 
 template <int kNst, unsigned kL>
@@ -71,6 +68,7 @@ struct SmemT {
     TileT<kL> ts[kBufs];
     unsigned long long tile_done[kBufs];   // compute warps -> emit warp (count kW)
     unsigned long long buf_free[kBufs];    // emit warp -> compute warps (count 1)
+    unsigned long long agg[kBufs];         // (compute warps done << 32) | survivors so far
     unsigned char qslot[kW][2 * kK2Items * 32];
     float2 sec[CUDAPRE_SECTORS + 1];               // {inner r^2, outer r^2} per bucket
     unsigned short sedge[CUDAPRE_SECTORS + 1];     // candidate exit edges per bucket
@@ -139,57 +137,41 @@ __device__ __forceinline__ unsigned chunk_point(unsigned sub, unsigned warp, uns
     return sub * (2u * kK2SubPairs) + warp * (2u * kChunkPairs) + loc;
 }
 
-// write the survivors of super-tile `tile` (warp-private lists) from exclusive
-// prefix ex
+// write the survivors of super-tile `tile` kept by warp `warp` from exclusive
+// prefix ex: list entries [0, kL) from shared memory, the overflow [kL, wc)
+// from the block's global scratch (written by the compute warp before it
+// signalled the tile done; L2-coherent loads)
 template <unsigned kL>
-__device__ __forceinline__ void emit_t(const K2Params& p, const TileT<kL>& ts, unsigned tile,
-                                       unsigned long long ex, unsigned warp, unsigned lane,
-                                       unsigned lt) {
+__device__ __forceinline__ void emit_t(const K2Params& p, const TileT<kL>& ts, const SurvT* ovf, unsigned tile,
+                                       unsigned long long ex, unsigned warp, unsigned lane) {
     const unsigned long long tpt = (unsigned long long)tile * (2u * kK2TilePairs);
     float2* out_pts = reinterpret_cast<float2*>(p.out_pts);
     const unsigned wc = ts.lstart[warp][kK2Sub];
-    if (wc <= kL) {
-        for (unsigned r = lane; r < wc; r += 32) {
-            const SurvT e = ts.list[warp][r];
-            const unsigned sub = e.meta >> 8, loc = e.meta & 0xffu;
-            const unsigned long long pos = ex + ts.off[sub * kW + warp] + (r - ts.lstart[warp][sub]);
-            if (pos < p.capacity) {
-                p.out_idx[pos] = p.base + (long long)(tpt + chunk_point(sub, warp, loc));
-                if (out_pts) out_pts[pos] = make_float2(e.x, e.y);
-            }
+    for (unsigned r = lane; r < wc; r += 32) {
+        SurvT e;
+        if (r < kL) {
+            e = ts.list[warp][r];
+        } else {
+            const SurvT* q = ovf + (r - kL);
+            e.x = __ldcg(&q->x);
+            e.y = __ldcg(&q->y);
+            e.meta = __ldcg(&q->meta);
         }
-        return;
-    }
-    // list overflow (dense tile): ranks from the keep bits, coordinates re-read
-#pragma unroll 1
-    for (unsigned sub = 0; sub < (unsigned)kK2Sub; ++sub) {
-        const unsigned own = ts.own[sub][warp][lane];
-        unsigned long long run = ex + ts.off[sub * kW + warp];
-#pragma unroll
-        for (int u = 0; u < kK2Items; ++u) {
-            const unsigned k0 = (own >> (2 * u)) & 1u, k1 = (own >> (2 * u + 1)) & 1u;
-            const unsigned b0 = __ballot_sync(kFull, k0), b1 = __ballot_sync(kFull, k1);
-            const unsigned long long pos = run + __popc(b0 & lt) + __popc(b1 & lt);
-            const unsigned long long i0 = tpt + chunk_point(sub, warp, (unsigned)u * 64u + 2u * lane);
-            if (k0 && pos < p.capacity) {
-                p.out_idx[pos] = p.base + (long long)i0;
-                if (out_pts) out_pts[pos] = __ldcg(reinterpret_cast<const float2*>(p.pts) + i0);
-            }
-            if (k1 && pos + k0 < p.capacity) {
-                p.out_idx[pos + k0] = p.base + (long long)(i0 + 1);
-                if (out_pts) out_pts[pos + k0] = __ldcg(reinterpret_cast<const float2*>(p.pts) + i0 + 1);
-            }
-            run += __popc(b0) + __popc(b1);
+        const unsigned sub = e.meta >> 8, loc = e.meta & 0xffu;
+        const unsigned long long pos = ex + ts.off[sub * kW + warp] + (r - ts.lstart[warp][sub]);
+        if (pos < p.capacity) {
+            p.out_idx[pos] = p.base + (long long)(tpt + chunk_point(sub, warp, loc));
+            if (out_pts) out_pts[pos] = make_float2(e.x, e.y);
         }
     }
 }
 
-// CFG 0: 3-stage ring (default); CFG 1: 2-stage ring.  128-entry lists per
-// warp and super-tile (6.25 % survivors before the overflow path); three list
-// buffers; ~105 KB of shared memory, 2 blocks per SM.
+// CFG 0: 4-stage ring, 96-entry lists (default: ~110 KB of shared memory,
+// 2 blocks per SM); CFG 1: 3-stage ring, 128-entry lists.  Overflowing lists
+// spill to global scratch, so the list size only trades smem for traffic.
 template <int CFG> struct K2Cfg;
-template <> struct K2Cfg<0> { static constexpr int kNst = 3; static constexpr unsigned kL = 128; static constexpr int kMinB = 2; };
-template <> struct K2Cfg<1> { static constexpr int kNst = 2; static constexpr unsigned kL = 128; static constexpr int kMinB = 2; };
+template <> struct K2Cfg<0> { static constexpr int kNst = 4; static constexpr unsigned kL = 96; static constexpr int kMinB = 2; };
+template <> struct K2Cfg<1> { static constexpr int kNst = 3; static constexpr unsigned kL = 128; static constexpr int kMinB = 2; };
 
 // DBG: perf-experiment build with per-warp cycle counters (CUDAPRE_K2_DEBUG=2)
 template <int EDGES, int CFG, bool DBG>
@@ -203,6 +185,8 @@ __global__ void __launch_bounds__(kBlock, K2Cfg<CFG>::kMinB) k2_filter_tma(const
     const unsigned epoch = *(volatile unsigned*)&p.ws->epoch;
     const unsigned full_pairs = p.n / 2u;
     const bool odd = (p.n & 1u) != 0u;
+    // list-overflow scratch of (this block, buffer b, warp w): sbase + (b*kW + w)*kK2WarpPts
+    SurvT* const sbase = p.scratch + (size_t)blockIdx.x * (kBufs * kW * kK2WarpPts);
 
     for (int i = threadIdx.x; i <= CUDAPRE_SECTORS; i += kBlock) {
         S.sec[i] = make_float2(p.sr2[i], p.sro2[i]);
@@ -218,6 +202,7 @@ __global__ void __launch_bounds__(kBlock, K2Cfg<CFG>::kMinB) k2_filter_tma(const
         for (int k = 0; k < kBufs; ++k) {
             mbar_init(&S.tile_done[k], (unsigned)kW);
             mbar_init(&S.buf_free[k], 1u);
+            S.agg[k] = 0ull;
         }
         mbar_fence_init();
     }
@@ -264,8 +249,8 @@ __global__ void __launch_bounds__(kBlock, K2Cfg<CFG>::kMinB) k2_filter_tma(const
 
     // ================================================================ emit warp
     // Per super-tile k (list buffer k % kBufs), once all compute warps are done
-    // with it: scan its 64 group counts, publish its aggregate (tile 0: its
-    // prefix); then resolve the PREVIOUS super-tile (decoupled look-back one
+    // with it (the last of them has published the tile's aggregate; tile 0:
+    // its inclusive prefix): scan its 64 group counts; then resolve the PREVIOUS super-tile (decoupled look-back one
     // tile-time after its aggregate went out: no spinning), publish its
     // inclusive prefix, write its survivors and hand its buffer back.  The
     // compute warps never wait for any of this.
@@ -296,11 +281,13 @@ __global__ void __launch_bounds__(kBlock, K2Cfg<CFG>::kMinB) k2_filter_tma(const
                 const unsigned total = __shfl_sync(kFull, inc, 31);
                 if (lane == 0) {
                     cur.total = total;
-                    if (tile == 0) {
-                        publish(p, 0, kFlagP, total, epoch);
-                        if (p.num_tiles == 1) p.ws->count = total;
-                    } else {
-                        publish(p, tile, kFlagA, total, epoch);
+                    if (p.debug == 3) {   // perf experiment: publish from the emit warp instead
+                        if (tile == 0) {
+                            publish(p, 0, kFlagP, total, epoch);
+                            if (p.num_tiles == 1) p.ws->count = total;
+                        } else {
+                            publish(p, tile, kFlagA, total, epoch);
+                        }
                     }
                 }
                 __syncwarp();
@@ -321,7 +308,8 @@ __global__ void __launch_bounds__(kBlock, K2Cfg<CFG>::kMinB) k2_filter_tma(const
                 // a quicker emit warp reaches the next look-back before the
                 // other blocks' aggregates are out and spins; r01_experiments.md)
 #pragma unroll 1
-                for (unsigned w = 0; w < (unsigned)kW; ++w) emit_t(p, prv, pend, ex, w, lane, lt);
+                for (unsigned w = 0; w < (unsigned)kW; ++w)
+                    emit_t(p, prv, sbase + (size_t)(pbuf * kW + w) * kK2WarpPts, pend, ex, w, lane);
                 __syncwarp();
                 if (lane == 0) mbar_arrive_a(a_free + 8u * pbuf);
                 if (DBG) { const unsigned long long t = clock64(); dce[3] += t - te; te = t; }
@@ -369,6 +357,7 @@ __global__ void __launch_bounds__(kBlock, K2Cfg<CFG>::kMinB) k2_filter_tma(const
         if (DBG) { const unsigned long long t = clock64(); dc[1] += t - t0; t0 = t; }
         if (have) {
             unsigned wc = 0;
+            SurvT* const wscr = sbase + (size_t)(bi * kW + warp) * kK2WarpPts;
 #pragma unroll 1
             for (int sub = 0; sub < kK2Sub; ++sub, ++seq) {
                 const unsigned st = seq % kNst;
@@ -421,7 +410,6 @@ __global__ void __launch_bounds__(kBlock, K2Cfg<CFG>::kMinB) k2_filter_tma(const
                 //      lanes < lane) + (h ? bit(u, 0) : 0), from 8 independent ballots
                 //      (a few dependent levels instead of a shuffle scan + a loop)
                 if (lane == 0) cur.lstart[warp][sub] = wc;
-                cur.own[sub][warp][lane] = 0;
                 unsigned qtotal = 0;
 #pragma unroll
                 for (int u = 0; u < kK2Items; ++u) {
@@ -451,11 +439,10 @@ __global__ void __launch_bounds__(kBlock, K2Cfg<CFG>::kMinB) k2_filter_tma(const
                         }
                         const unsigned kb = __ballot_sync(kFull, kp);
                         if (kp) {
-                            const unsigned ol = (loc >> 1) & 31u, b = ((loc >> 6) << 1) | (loc & 1u);
-                            atomicOr(reinterpret_cast<unsigned*>(&cur.own[sub][warp][ol & ~3u]),
-                                     (1u << b) << (8u * (ol & 3u)));
                             const unsigned r = wc + __popc(kb & lt);
-                            if (r < kL) cur.list[warp][r] = SurvT{q.x, q.y, ((unsigned)sub << 8) | loc};
+                            const SurvT e{q.x, q.y, ((unsigned)sub << 8) | loc};
+                            if (r < kL) cur.list[warp][r] = e;
+                            else wscr[r - kL] = e;   // overflow: global scratch
                         }
                         wc += __popc(kb);
                     }
@@ -466,8 +453,26 @@ __global__ void __launch_bounds__(kBlock, K2Cfg<CFG>::kMinB) k2_filter_tma(const
             if (lane == 0) cur.lstart[warp][kK2Sub] = wc;
         }
         if (warp == 0 && lane == 0) cur.tile = have ? tile : kNone;
+        if (have && cur.lstart[warp][kK2Sub] > kL) __threadfence_block();   // scratch writes before the signal
         __syncwarp();
         if (lane == 0) {
+            if (have && p.debug != 3) {
+                // the last compute warp done with the tile publishes its aggregate
+                // at once: other blocks' look-backs never wait on this block's
+                // emit warp (a late aggregate stalls every later tile's look-back)
+                const unsigned wc = cur.lstart[warp][kK2Sub];
+                const unsigned long long old = atomicAdd(&S.agg[bi], (1ull << 32) | wc);
+                if ((unsigned)(old >> 32) == (unsigned)kW - 1u) {
+                    const unsigned total = (unsigned)old + wc;
+                    S.agg[bi] = 0ull;   // next use: 3 tiles later, after tile_done / buf_free
+                    if (tile == 0) {
+                        publish(p, 0, kFlagP, total, epoch);
+                        if (p.num_tiles == 1) p.ws->count = total;
+                    } else {
+                        publish(p, tile, kFlagA, total, epoch);
+                    }
+                }
+            }
             mbar_arrive_a(a_done + 8u * bi);
         }
         if (DBG) { const unsigned long long t = clock64(); dc[0] += t - t0; }
@@ -491,7 +496,8 @@ cudaError_t launch_tma_t(const K2Params& p, cudaStream_t s, int* launches) {
         max_blocks = (per_sm > 0 ? per_sm : 1) * device_sm_count();
     }
     unsigned blocks = p.num_tiles < (unsigned)max_blocks ? p.num_tiles : (unsigned)max_blocks;
-    if (blocks < 1) blocks = 1;
+    if (blocks > p.scratch_blocks) blocks = p.scratch_blocks;   // one overflow scratch area per block
+    if (blocks < 1) return cudaErrorInvalidValue;               // (workspace checked by the caller)
     k2_filter_tma<EDGES, CFG, DBG><<<blocks, kBlock, smem, s>>>(p);
     ++*launches;
     return cudaGetLastError();

@@ -23,9 +23,10 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="C5")
     ap.add_argument("--runs", type=int, default=3)
+    ap.add_argument("--points", action="store_true", help="also write survivor coordinates (as bench.py)")
     args = ap.parse_args()
     if os.environ.get("CUDAPRE_K2_DEBUG") != "2":
-        sys.exit("set CUDAPRE_K2_DEBUG=2")
+        print("(CUDAPRE_K2_DEBUG != 2: only the dense-emit counter is meaningful)")
     import torch
 
     import paper_1405_3454_b200 as cp
@@ -38,15 +39,17 @@ def main():
     ws = cp.Workspace(n)
     cap = max(1024, n // 8)
     out_idx = torch.empty(cap, dtype=torch.int64, device="cuda")
+    out_pts = torch.empty((cap, 2), dtype=torch.float32, device="cuda") if args.points else None
     for _ in range(args.runs):
         ws.tensor[DBG_OFFSET:DBG_OFFSET + 384].zero_()
         ext = cp.extremes(pts, "A", ws=ws)
-        idx, _, rep = cp.filter(pts, ext, ws=ws, out_idx=out_idx, return_points=False)
+        idx, _, rep = cp.filter(pts, ext, ws=ws, out_idx=out_idx, out_pts=out_pts, return_points=args.points)
         torch.cuda.synchronize()
     d = ws.tensor[DBG_OFFSET:DBG_OFFSET + 384].cpu().view(torch.int64).tolist()
     clk = torch.cuda.get_device_properties(0).clock_rate * 1e3 if hasattr(
         torch.cuda.get_device_properties(0), "clock_rate") else 1.9e9
     blocks = 2 * torch.cuda.get_device_properties(0).multi_processor_count
+    print(f"dense (list-overflow) warp emits in the last launch: {d[44]}")
     print(f"K2 {rep['ms_filter_kernel']:.3f} ms, survivors {idx.shape[0]}, blocks {blocks}, clock {clk/1e9:.2f} GHz")
     us = lambda c: c / clk / blocks * 1e6
     print("per-block average, microseconds (cycles / clock / blocks)")

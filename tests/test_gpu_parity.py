@@ -284,3 +284,18 @@ def test_register_kernel_fallbacks_match(k1_tma, k2_tma):
     res = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600,
                          env=env, cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     assert res.returncode == 0 and "reg ok" in res.stdout, res.stderr[-3000:]
+
+
+def test_workspace_reuse_across_sizes_and_densities():
+    """One caller workspace serves calls of different n and survivor density
+    in any order (epoch-tagged tile status at the front, list-overflow scratch
+    at the back: a dense small call must not corrupt a later large call)."""
+    big = synth.generate("disk", 3_000_017, seed=21)
+    small_dense = synth.generate("circle", 400_003, seed=22)
+    ws = cp.Workspace(len(big))
+    want_big = oracle.cudapre(big, "A", threads=THREADS)["survivors"]
+    want_small = oracle.cudapre(small_dense, "A", threads=THREADS)["survivors"]
+    for xy, want in ((big, want_big), (small_dense, want_small), (big, want_big), (small_dense, want_small),
+                     (big, want_big)):
+        idx, _, _ = cp.cuda_pre(torch.from_numpy(xy).cuda(), ws=ws)
+        assert np.array_equal(idx.cpu().numpy(), want)
