@@ -26,7 +26,7 @@ from dataclasses import dataclass
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libcudapre.so")
+LIB_PATH = os.environ.get("CUDAPRE_LIB_OVERRIDE") or os.path.join(_HERE, "libcudapre.so")   # (override: A/B perf experiments only)
 MAX_ANGLES = 8
 MAX_SLOTS = 32
 SECTORS = 1024
