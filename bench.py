@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--angles", default="A")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--host-step2", action="store_true",
+                    help="N=1: run Step 2 on the host between the kernels (as the paper) instead of on the device")
     return ap.parse_args()
 
 
@@ -201,15 +203,34 @@ def main():
 
     exact_pts = [0]
 
-    def step(rep1):
+    def step(rep1):   # host Step 2 (and, N > 1, the cross-rank combine)
         ext = cp.extremes(pts, args.angles, index_base=base, group=group, ws=ws, report=rep1)
         exact_pts[0] = ext.raw.exact_points
         idx, sp, rep2 = cp.filter(pts, ext, index_base=base, ws=ws, out_idx=out_idx, out_pts=out_pts)
         return idx.shape[0], rep2
 
+    # N = 1: Steps 1-3 stay on the device (Step 2 by the device builder, SURVEY
+    # §8 f3), the host only enqueues; CUDA events between the three calls
+    # time seed+K1, Step 2 and K2 separately on the stream they run on.
+    device_path = group is None and not args.host_step2
+    count = torch.zeros(1, dtype=torch.int64, device="cuda")
+
+    def dstep(ev):
+        if ev:
+            ev[0].record()
+        cp.extremes_device(pts, args.angles, index_base=base, ws=ws)
+        if ev:
+            ev[1].record()
+        cp.polygon_device(ws)
+        if ev:
+            ev[2].record()
+        cp.filter_geom(pts, index_base=base, ws=ws, out_idx=out_idx, out_pts=out_pts, count=count)
+        if ev:
+            ev[3].record()
+
     rep1 = cp.ReportT()
     for _ in range(args.warmup):
-        step(rep1)
+        dstep(None) if device_path else step(rep1)
     k1_ms, k2_ms, poly_ms, launches = [], [], [], 0
     lb_rounds = [0, 0]
     surv = 0
@@ -218,18 +239,33 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
     with clocks:
         start.record()
-        for _ in range(args.steps):
-            surv, rep2 = step(rep1)
-            k1_ms.append(rep1.ms_extremes_kernels)
-            k2_ms.append(rep2["ms_filter_kernel"])
-            poly_ms.append(rep2["ms_polygon_host"])
-            lb_rounds[:] = [rep2["lookback_rounds"], rep2["lookback_spins"]]
-            launches += rep1.launches + rep2["launches"]
+        for i in range(args.steps):
+            if device_path:
+                dstep(evs[i])
+            else:
+                surv, rep2 = step(rep1)
+                k1_ms.append(rep1.ms_extremes_kernels)
+                k2_ms.append(rep2["ms_filter_kernel"])
+                poly_ms.append(rep2["ms_polygon_host"])
+                lb_rounds[:] = [rep2["lookback_rounds"], rep2["lookback_spins"]]
+                launches += rep1.launches + rep2["launches"]
         end.record()
         torch.cuda.synchronize()
     ms = start.elapsed_time(end)
+    if device_path:
+        k1_ms = [e[0].elapsed_time(e[1]) for e in evs]
+        poly_ms = [e[1].elapsed_time(e[2]) for e in evs]
+        k2_ms = [e[2].elapsed_time(e[3]) for e in evs]
+        surv = int(count.item())
+        # seed (n >= 65536) + K1 + polygon builder + K2 per step
+        launches = args.steps * ((2 if n_local >= 65536 else 1) + 2)
+        # per-step diagnostics (not timed): one host-path step with reports
+        _, rep2 = step(rep1)
+        lb_rounds[:] = [rep2["lookback_rounds"], rep2["lookback_spins"]]
+        assert rep2["survivors"] == surv, (rep2["survivors"], surv)
     if group is not None:
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -336,14 +372,18 @@ def main():
             "data": "synthetic",
             "config": {"workload": f"{args.config}: {n_total} pts uniform {family} (seed {seed}), "
                                    f"contiguous shards of {n_local}", "n_total": n_total,
-                       "angles": args.angles, "l2": "inputs larger than L2 (16 GB vs 126 MB), no flush",
+                       "angles": args.angles,
+                       "l2": (f"inputs larger than L2 ({8 * n_local / 1e9:.2f} GB vs 126 MB), no flush"
+                              if 8 * n_local > 126e6 else
+                              f"inputs ({8 * n_local / 1e6:.0f} MB) fit in L2: warm-L2 numbers, not a roofline claim"),
                        "parallelism": f"dp{world} (point shards; 912 B NCCL all-gather per step)"},
             "discard_pct": round(100 * (1 - surv_total / n_total), 4),
             "remaining_pct": round(100 * surv_total / n_total, 4),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": clocks.result(),
             "k1_exact_path_points_per_step": int(exact_pts[0]),
-            "host_step2_ms": round(statistics.median(poly_ms), 4),
+            ("host_step2_ms" if not device_path else "step2_device_ms"): round(statistics.median(poly_ms), 4),
+            "step2": "device" if device_path else "host",
             "k2_lookback_rounds_per_step": int(lb_rounds[0]), "k2_lookback_spins_per_step": int(lb_rounds[1]),
         }
         print(json.dumps(line), flush=True)

@@ -241,6 +241,76 @@ cudapre_status cudapre_run_host(const cudapre_pt* h_pts, int64_t n, int32_t nang
                                 int64_t* h_surv_idx, int64_t capacity, void* stream,
                                 int64_t* h_count, cudapre_report_t* h_rep);
 
+/* ---------------------------------------------------------------- device-resident Steps 2-3
+ * Step 2 (§2 Step 2, P:39 — the host chain in the
+ * paper) can also run on the device, so Steps 1-3 are enqueued back to back
+ * with no host round trip and can be captured in one CUDA graph.  The device
+ * builder executes the same arithmetic as the host one (shared code, no FMA
+ * contraction): the polygon and the Step-3 geometry are byte-identical.
+ *
+ * Workspace pages written by the device path (readable by the caller): the
+ * Step-3 geometry at byte CUDAPRE_WS_GEOM_OFFSET and the polygon
+ * (cudapre_polygon_t) at CUDAPRE_WS_POLY_OFFSET; the Step-1 result that
+ * cudapre_extremes leaves on the device is in the workspace header.      */
+#define CUDAPRE_WS_GEOM_OFFSET 4096
+#define CUDAPRE_WS_POLY_OFFSET (4096 + 16384)
+
+/* Host build of the Step-3 geometry block for h_ext (the block the device
+ * path writes at CUDAPRE_WS_GEOM_OFFSET), for tests and inspection.
+ * *needed (nullable) receives its size.  INVALID_ARGUMENT if out_bytes is
+ * too small; EMPTY_INPUT if h_ext->n == 0.                                 */
+cudapre_status cudapre_geometry(const cudapre_extremes_t* h_ext, void* h_out, size_t out_bytes,
+                                size_t* needed);
+
+/* Step 2 on the device: builds the polygon and the Step-3 geometry from the
+ * device Step-1 result d_ext (NULL = the one cudapre_extremes left in d_ws)
+ * into the workspace pages (and into d_poly if not NULL).  One block, one
+ * launch; byte-identical to cudapre_polygon / cudapre_geometry.            */
+cudapre_status cudapre_polygon_device(const cudapre_extremes_t* d_ext, void* d_ws, size_t ws_bytes,
+                                      void* stream, cudapre_polygon_t* d_poly);
+
+/* Step 3 alone, with the geometry already in the workspace (from
+ * cudapre_polygon_device): the K2 launch + the device count copy.        */
+cudapre_status cudapre_filter_geom(const cudapre_pt* d_pts, int64_t n_local, int64_t index_base,
+                                   int64_t* d_surv_idx, cudapre_pt* d_surv_pts, int64_t capacity,
+                                   void* d_ws, size_t ws_bytes, void* stream, int64_t* d_count);
+
+/* Steps 2 + 3 on the stream (cudapre_polygon_device + cudapre_filter_geom),
+ * nothing waits for the host.
+ *   d_ext      device Step-1 result; NULL = the one cudapre_extremes left in d_ws
+ *   d_count    device int64 (nullable): the survivor count (may exceed capacity;
+ *              only the first `capacity` survivors are written)
+ *   d_poly     device polygon struct, nullable (default: the workspace page)
+ * Other arguments as cudapre_filter.  A degenerate ring keeps every point;
+ * non-finite input (flagged in the Step-1 result) keeps every point too —
+ * check d_ext->nonfinite before trusting the survivors.  Capture-safe.    */
+cudapre_status cudapre_filter_device(const cudapre_pt* d_pts, int64_t n_local, int64_t index_base,
+                                     const cudapre_extremes_t* d_ext, int64_t* d_surv_idx,
+                                     cudapre_pt* d_surv_pts, int64_t capacity, void* d_ws,
+                                     size_t ws_bytes, void* stream, int64_t* d_count,
+                                     cudapre_polygon_t* d_poly);
+
+/* Steps 1-3 on the stream (single GPU or one shard without the cross-rank
+ * combine): cudapre_extremes without host outputs + cudapre_filter_device.
+ * Capture-safe after one uncaptured call (launcher set-up).               */
+cudapre_status cudapre_pipeline_device(const cudapre_pt* d_pts, int64_t n_local, int64_t index_base,
+                                       int32_t nang, const double* c, const double* s,
+                                       int64_t* d_surv_idx, cudapre_pt* d_surv_pts, int64_t capacity,
+                                       void* d_ws, size_t ws_bytes, void* stream, int64_t* d_count);
+
+/* One CUDA graph of cudapre_pipeline_device on fixed buffers: create runs
+ * the pipeline once on `stream` (synchronised), then captures it; launch
+ * replays it (one graph launch per step); destroy frees it.  The buffers
+ * must outlive the graph.                                                 */
+typedef struct cudapre_graph cudapre_graph_t;
+cudapre_status cudapre_graph_create(const cudapre_pt* d_pts, int64_t n_local, int64_t index_base,
+                                    int32_t nang, const double* c, const double* s,
+                                    int64_t* d_surv_idx, cudapre_pt* d_surv_pts, int64_t capacity,
+                                    void* d_ws, size_t ws_bytes, void* stream, int64_t* d_count,
+                                    cudapre_graph_t** out);
+cudapre_status cudapre_graph_launch(cudapre_graph_t* g, void* stream);
+cudapre_status cudapre_graph_destroy(cudapre_graph_t* g);
+
 #ifdef __cplusplus
 }
 #endif

@@ -79,7 +79,11 @@ EXTREMES_BYTES = ctypes.sizeof(ExtremesT)
 SYMBOLS = ["cudapre_version", "cudapre_last_error", "cudapre_angles_preset",
            "cudapre_workspace_bytes", "cudapre_workspace_init", "cudapre_extremes",
            "cudapre_extremes_merge", "cudapre_polygon", "cudapre_filter", "cudapre_hull",
-           "cudapre_run_host"]
+           "cudapre_run_host", "cudapre_geometry", "cudapre_filter_device", "cudapre_pipeline_device",
+           "cudapre_graph_create", "cudapre_graph_launch", "cudapre_graph_destroy",
+           "cudapre_polygon_device", "cudapre_filter_geom"]
+WS_GEOM_OFFSET = 4096            # include/cudapre.h CUDAPRE_WS_GEOM_OFFSET
+WS_POLY_OFFSET = 4096 + 16384    # CUDAPRE_WS_POLY_OFFSET
 
 _lib = None
 
@@ -108,6 +112,14 @@ def lib():
                                  P(PolygonT), P(ReportT)]
     L.cudapre_hull.argtypes = [vp, vp, i64, vp, P(i64)]
     L.cudapre_run_host.argtypes = [vp, i64, i32, vp, vp, vp, vp, sz, vp, vp, i64, vp, P(i64), P(ReportT)]
+    L.cudapre_geometry.argtypes = [P(ExtremesT), vp, sz, P(sz)]
+    L.cudapre_filter_device.argtypes = [vp, i64, i64, vp, vp, vp, i64, vp, sz, vp, vp, vp]
+    L.cudapre_pipeline_device.argtypes = [vp, i64, i64, i32, vp, vp, vp, vp, i64, vp, sz, vp, vp]
+    L.cudapre_graph_create.argtypes = [vp, i64, i64, i32, vp, vp, vp, vp, i64, vp, sz, vp, vp, P(vp)]
+    L.cudapre_graph_launch.argtypes = [vp, vp]
+    L.cudapre_graph_destroy.argtypes = [vp]
+    L.cudapre_polygon_device.argtypes = [vp, vp, sz, vp, vp]
+    L.cudapre_filter_geom.argtypes = [vp, i64, i64, vp, vp, i64, vp, sz, vp, vp]
     for name in SYMBOLS[2:]:
         if name not in ("cudapre_workspace_bytes",):
             getattr(L, name).restype = ctypes.c_int
@@ -374,6 +386,141 @@ def hull(xy, ids=None) -> np.ndarray:
 
 
 # ------------------------------------------------------------------ whole method
+# ------------------------------------------------------------------ device-resident Steps 2-3 (f3)
+def geometry(ext: Extremes) -> bytes:
+    """Host build of the Step-3 geometry block (the bytes the device builder
+    writes at WS_GEOM_OFFSET of the workspace)."""
+    need = ctypes.c_size_t()
+    lib().cudapre_geometry(ctypes.byref(ext.raw), None, 0, ctypes.byref(need))
+    buf = (ctypes.c_uint8 * need.value)()
+    _check(lib().cudapre_geometry(ctypes.byref(ext.raw), buf, need.value, None))
+    return bytes(buf)
+
+
+def _outputs(pts, out_idx, out_pts, return_points):
+    torch = _torch()
+    n = pts.shape[0]
+    if out_idx is None:
+        out_idx = torch.empty(max(n, 1), dtype=torch.int64, device=pts.device)
+    if return_points and out_pts is None:
+        out_pts = torch.empty((max(n, 1), 2), dtype=torch.float32, device=pts.device)
+    cap = out_idx.shape[0] if out_pts is None else min(out_idx.shape[0], out_pts.shape[0])
+    return out_idx, out_pts, cap
+
+
+def filter_device(pts, ext_dev=None, index_base: int = 0, return_points: bool = True, ws=None,
+                  out_idx=None, out_pts=None, d_poly=None, stream=None):
+    """Steps 2+3 with Step 2 on the device (no host round trip): returns
+    (out_idx, out_pts, count) where count is a device int64 tensor of one
+    element (the survivors are out_idx[:count]).  ext_dev: device
+    cudapre_extremes_t bytes (None: the result extremes() left in ws)."""
+    torch = _torch()
+    pts = _points(pts)
+    n = pts.shape[0]
+    w = _workspace(n, pts.device, ws)
+    out_idx, out_pts, cap = _outputs(pts, out_idx, out_pts, return_points)
+    count = torch.zeros(1, dtype=torch.int64, device=pts.device)
+    _check(lib().cudapre_filter_device(
+        ctypes.c_void_p(pts.data_ptr()), n, index_base,
+        ctypes.c_void_p(ext_dev.data_ptr()) if ext_dev is not None else None,
+        ctypes.c_void_p(out_idx.data_ptr()),
+        ctypes.c_void_p(out_pts.data_ptr()) if out_pts is not None else None, cap,
+        w.ptr, w.nbytes, _stream_ptr(stream), ctypes.c_void_p(count.data_ptr()),
+        ctypes.c_void_p(d_poly.data_ptr()) if d_poly is not None else None))
+    return out_idx, out_pts, count
+
+
+def extremes_device(pts, angles_="A", index_base: int = 0, ws=None, stream=None):
+    """Step 1 with no host output and no synchronisation: the result stays in
+    the workspace for polygon_device / filter_device."""
+    pts = _points(pts)
+    n = pts.shape[0]
+    nang, c, s = _angle_arrays(angles_)
+    w = _workspace(n, pts.device, ws)
+    _check(lib().cudapre_extremes(
+        ctypes.c_void_p(pts.data_ptr()), n, index_base, nang,
+        c.ctypes.data_as(ctypes.c_void_p), s.ctypes.data_as(ctypes.c_void_p),
+        w.ptr, w.nbytes, _stream_ptr(stream), None, None, None))
+
+
+def polygon_device(ws, ext_dev=None, d_poly=None, stream=None):
+    """Step 2 on the device into the workspace pages (see filter_device)."""
+    _check(lib().cudapre_polygon_device(
+        ctypes.c_void_p(ext_dev.data_ptr()) if ext_dev is not None else None, ws.ptr, ws.nbytes,
+        _stream_ptr(stream), ctypes.c_void_p(d_poly.data_ptr()) if d_poly is not None else None))
+
+
+def filter_geom(pts, index_base: int = 0, ws=None, out_idx=None, out_pts=None, count=None, stream=None):
+    """Step 3 alone on the geometry already in ws; count: device int64[1]."""
+    pts = _points(pts)
+    n = pts.shape[0]
+    w = _workspace(n, pts.device, ws)
+    cap = out_idx.shape[0] if out_pts is None else min(out_idx.shape[0], out_pts.shape[0])
+    _check(lib().cudapre_filter_geom(
+        ctypes.c_void_p(pts.data_ptr()), n, index_base, ctypes.c_void_p(out_idx.data_ptr()),
+        ctypes.c_void_p(out_pts.data_ptr()) if out_pts is not None else None, cap, w.ptr, w.nbytes,
+        _stream_ptr(stream), ctypes.c_void_p(count.data_ptr()) if count is not None else None))
+
+
+def pipeline(pts, angles_="A", index_base: int = 0, return_points: bool = True, ws=None, out_idx=None,
+             out_pts=None, stream=None):
+    """Steps 1-3 enqueued on the stream with no host synchronisation; returns
+    (out_idx, out_pts, count) as filter_device."""
+    torch = _torch()
+    pts = _points(pts)
+    n = pts.shape[0]
+    nang, c, s = _angle_arrays(angles_)
+    w = _workspace(n, pts.device, ws)
+    out_idx, out_pts, cap = _outputs(pts, out_idx, out_pts, return_points)
+    count = torch.zeros(1, dtype=torch.int64, device=pts.device)
+    _check(lib().cudapre_pipeline_device(
+        ctypes.c_void_p(pts.data_ptr()), n, index_base, nang,
+        c.ctypes.data_as(ctypes.c_void_p), s.ctypes.data_as(ctypes.c_void_p),
+        ctypes.c_void_p(out_idx.data_ptr()),
+        ctypes.c_void_p(out_pts.data_ptr()) if out_pts is not None else None, cap,
+        w.ptr, w.nbytes, _stream_ptr(stream), ctypes.c_void_p(count.data_ptr())))
+    return out_idx, out_pts, count
+
+
+class Graph:
+    """Steps 1-3 captured once in a CUDA graph on fixed buffers; launch()
+    replays the whole step with one graph launch.  count is a device int64
+    tensor updated by every launch."""
+
+    def __init__(self, pts, angles_="A", index_base: int = 0, return_points: bool = True, ws=None,
+                 out_idx=None, out_pts=None, stream=None):
+        torch = _torch()
+        self.pts = _points(pts)
+        n = self.pts.shape[0]
+        nang, c, s = _angle_arrays(angles_)
+        self.ws = _workspace(n, self.pts.device, ws)
+        self.out_idx, self.out_pts, cap = _outputs(self.pts, out_idx, out_pts, return_points)
+        self.count = torch.zeros(1, dtype=torch.int64, device=self.pts.device)
+        h = ctypes.c_void_p()
+        _check(lib().cudapre_graph_create(
+            ctypes.c_void_p(self.pts.data_ptr()), n, index_base, nang,
+            c.ctypes.data_as(ctypes.c_void_p), s.ctypes.data_as(ctypes.c_void_p),
+            ctypes.c_void_p(self.out_idx.data_ptr()),
+            ctypes.c_void_p(self.out_pts.data_ptr()) if self.out_pts is not None else None, cap,
+            self.ws.ptr, self.ws.nbytes, _stream_ptr(stream), ctypes.c_void_p(self.count.data_ptr()),
+            ctypes.byref(h)))
+        self._h = h
+
+    def launch(self, stream=None):
+        _check(lib().cudapre_graph_launch(self._h, _stream_ptr(stream)))
+
+    def close(self):
+        if self._h:
+            lib().cudapre_graph_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def cuda_pre(pts, angles_="A", group=None, index_base: int = 0, return_points=True, ws=None):
     """Steps 1-3.  Empty input: survivors = input, filter skipped."""
     torch = _torch()

@@ -16,8 +16,12 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libcudapre.so")
 BUILD = os.path.join(HERE, "_build")
-SOURCES = ["api.cpp", "host_geom.cpp", "k1_extremes.cu", "k2_filter.cu", "k2_filter_tma.cu"]
-HEADERS = ["internal.h", "exact.cuh", "k2_common.cuh", "tma.cuh", os.path.join("..", "..", "include", "cudapre.h")]
+SOURCES = ["api.cpp", "host_geom.cpp", "k1_extremes.cu", "k2_filter.cu", "k2_filter_tma.cu", "k_polygon.cu"]
+# per-file extra flags: the device polygon builder must not contract multiply-adds (it has to agree
+# bit for bit with the host builder, compiled with -ffp-contract=off)
+EXTRA = {"k_polygon.cu": ["-fmad=false"]}
+HEADERS = ["internal.h", "exact.cuh", "geom.cuh", "k2_common.cuh", "tma.cuh",
+           os.path.join("..", "..", "include", "cudapre.h")]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-ffp-contract=off,-O2",
               "--expt-relaxed-constexpr"]
@@ -47,7 +51,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         o = os.path.join(BUILD, src + ".o")
         objs.append(o)
         if force or _stale(o, [s, *hdrs]):
-            cmd = [nvcc, *ARCH, *NVCC_FLAGS, "-c", s, "-o", o]
+            cmd = [nvcc, *ARCH, *NVCC_FLAGS, *EXTRA.get(src, []), "-c", s, "-o", o]
             if verbose and src.endswith(".cu"):
                 cmd += ["-Xptxas", "-v"]
             jobs.append(cmd)

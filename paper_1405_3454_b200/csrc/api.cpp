@@ -37,6 +37,10 @@ cudapre_status fail(cudapre_status st, const char* fmt, ...) {
 
 // Small pinned staging buffer per host thread for the 8-byte count and the
 // result struct (a pageable destination would force a staged synchronous copy).
+// per-thread pinned staging: [0, 4 KiB) small D2H results, [4 KiB, ...) the
+// host-built Step-3 geometry on its way to the workspace
+constexpr size_t kStageGeomOff = 4096;
+constexpr size_t kStageBytes = kStageGeomOff + sizeof(K2Geom);
 struct Staging {
     void* p = nullptr;
     ~Staging() {
@@ -46,7 +50,7 @@ struct Staging {
 thread_local Staging g_stage;
 
 cudapre_status staging(void** out) {
-    if (!g_stage.p) CUDA_TRY(cudaHostAlloc(&g_stage.p, 4096, cudaHostAllocPortable));
+    if (!g_stage.p) CUDA_TRY(cudaHostAlloc(&g_stage.p, kStageBytes, cudaHostAllocPortable));
     *out = g_stage.p;
     return CUDAPRE_OK;
 }
@@ -96,11 +100,17 @@ void preset_coef(double deg, double* c, double* s) {
 }
 
 WsHeader* ws_header(void* d_ws) { return reinterpret_cast<WsHeader*>(d_ws); }
+static_assert(CUDAPRE_WS_GEOM_OFFSET == kWsHeaderBytes && CUDAPRE_WS_POLY_OFFSET == kWsHeaderBytes + kWsPolyOff,
+              "workspace page offsets in include/cudapre.h");
+K2Geom* ws_geom(void* d_ws) { return reinterpret_cast<K2Geom*>(reinterpret_cast<char*>(d_ws) + kWsHeaderBytes); }
+cudapre_polygon_t* ws_poly(void* d_ws) {
+    return reinterpret_cast<cudapre_polygon_t*>(reinterpret_cast<char*>(d_ws) + kWsHeaderBytes + kWsPolyOff);
+}
 K1Partial* ws_partials(void* d_ws) {
-    return reinterpret_cast<K1Partial*>(reinterpret_cast<char*>(d_ws) + kWsHeaderBytes);
+    return reinterpret_cast<K1Partial*>(reinterpret_cast<char*>(d_ws) + kWsFixedBytes);
 }
 unsigned long long* ws_status(void* d_ws) {
-    return reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(d_ws) + kWsHeaderBytes +
+    return reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(d_ws) + kWsFixedBytes +
                                                  kWsPartialBytes);
 }
 // The overflow scratch sits at the END of the caller's workspace: the
@@ -109,7 +119,7 @@ unsigned long long* ws_status(void* d_ws) {
 // larger n's status words live (status(n) grows from the front, scratch from
 // the back; ws_bytes >= ws_bytes_for(n) keeps them apart).
 SurvEntry* ws_scratch(void* d_ws, size_t ws_bytes, int64_t n, unsigned* blocks) {
-    const size_t used = kWsHeaderBytes + kWsPartialBytes + ws_status_bytes(n);
+    const size_t used = kWsFixedBytes + kWsPartialBytes + ws_status_bytes(n);
     size_t nb = ws_bytes > used + 16 ? (ws_bytes - used - 16) / kK2ScratchPerBlock : 0;
     const size_t want = (size_t)kK2BlocksPerSM * (size_t)device_sm_count();
     if (nb > want) nb = want;
@@ -144,6 +154,26 @@ void empty_result(cudapre_extremes_t* r, int nang, const double* c, const double
         r->c[k] = c[k];
         r->s[k] = s[k];
     }
+}
+
+// K2 parameters that do not depend on the polygon (the geometry is read from
+// the workspace's geometry page, p.g)
+void k2_params(K2Params& p, const cudapre_pt* d_pts, int64_t n_local, int64_t index_base, int64_t* d_surv_idx,
+               cudapre_pt* d_surv_pts, int64_t capacity, void* d_ws, size_t ws_bytes) {
+    p.pts = reinterpret_cast<const float*>(d_pts);
+    p.n = (unsigned)n_local;
+    p.base = index_base;
+    p.out_idx = reinterpret_cast<long long*>(d_surv_idx);
+    p.out_pts = reinterpret_cast<float*>(d_surv_pts);
+    p.capacity = (unsigned long long)(capacity < 0 ? 0 : capacity);
+    p.ws = ws_header(d_ws);
+    p.status = ws_status(d_ws);
+    p.scratch = ws_scratch(d_ws, ws_bytes, n_local, &p.scratch_blocks);
+    p.num_tiles = (unsigned)((n_local + kK2TilePts - 1) / kK2TilePts);
+    p.g = ws_geom(d_ws);
+    p.edges = 32;
+    const char* e = getenv("CUDAPRE_K2_DEBUG");   // perf experiments only: wrong results
+    p.debug = e ? atoi(e) : 0;
 }
 
 }  // namespace
@@ -317,8 +347,12 @@ cudapre_status cudapre_filter(const cudapre_pt* d_pts, int64_t n_local, int64_t 
     K2Params p;
     std::memset(&p, 0, sizeof(p));
     cudapre_polygon_t poly;
+    void* stage = nullptr;
+    st = staging(&stage);
+    if (st) return st;
+    K2Geom* hg = reinterpret_cast<K2Geom*>(reinterpret_cast<char*>(stage) + kStageGeomOff);
     const auto t0 = std::chrono::steady_clock::now();
-    build_polygon(*h_ext, &poly, &p);
+    build_polygon(*h_ext, &poly, hg);
     const auto t1 = std::chrono::steady_clock::now();
     if (h_poly) *h_poly = poly;
     if (h_rep) {
@@ -331,21 +365,10 @@ cudapre_status cudapre_filter(const cudapre_pt* d_pts, int64_t n_local, int64_t 
     if (st) return st;
 
     cudaStream_t strm = (cudaStream_t)stream;
-    p.pts = reinterpret_cast<const float*>(d_pts);
-    p.n = (unsigned)n_local;
-    p.base = index_base;
-    p.out_idx = reinterpret_cast<long long*>(d_surv_idx);
-    p.out_pts = reinterpret_cast<float*>(d_surv_pts);
-    p.capacity = (unsigned long long)capacity;
-    p.ws = ws_header(d_ws);
-    p.status = ws_status(d_ws);
-    p.scratch = ws_scratch(d_ws, ws_bytes, n_local, &p.scratch_blocks);
-    p.num_tiles = (unsigned)((n_local + kK2TilePts - 1) / kK2TilePts);   // the TMA launcher re-derives its own
+    k2_params(p, d_pts, n_local, index_base, d_surv_idx, d_surv_pts, capacity, d_ws, ws_bytes);
+    p.edges = poly.nv <= 16 ? 16 : 32;
+    CUDA_TRY(cudaMemcpyAsync(ws_geom(d_ws), hg, sizeof(K2Geom), cudaMemcpyHostToDevice, strm));
     const int vec16 = (((uintptr_t)d_pts & 15u) == 0);
-    {
-        const char* e = getenv("CUDAPRE_K2_DEBUG");   // perf experiments only: wrong results
-        p.debug = e ? atoi(e) : 0;
-    }
 
     cudaEvent_t* ev = nullptr;
     if (h_rep) {
@@ -356,9 +379,6 @@ cudapre_status cudapre_filter(const cudapre_pt* d_pts, int64_t n_local, int64_t 
     int launches = 0;
     CUDA_TRY(launch_filter(p, vec16, stream, &launches));
     if (h_rep) CUDA_TRY(cudaEventRecord(ev[3], strm));
-    void* stage = nullptr;
-    st = staging(&stage);
-    if (st) return st;
     CUDA_TRY(cudaMemcpyAsync(stage, &p.ws->count, 16, cudaMemcpyDeviceToHost, strm));   // count + stats
     CUDA_TRY(cudaStreamSynchronize(strm));
     const int64_t count = (int64_t) * reinterpret_cast<unsigned long long*>(stage);
@@ -420,6 +440,140 @@ cudapre_status cudapre_run_host(const cudapre_pt* h_pts, int64_t n, int32_t nang
         h_rep->launches = r1.launches + r2.launches;
     }
     return st;
+}
+
+// ------------------------------------------------------------------ device-resident Steps 2-3 (f3)
+cudapre_status cudapre_geometry(const cudapre_extremes_t* h_ext, void* h_out, size_t out_bytes, size_t* needed) {
+    g_err.clear();
+    if (needed) *needed = sizeof(K2Geom);
+    if (!h_ext || !h_out) return fail(CUDAPRE_ERR_INVALID_ARGUMENT, "NULL argument");
+    if (out_bytes < sizeof(K2Geom))
+        return fail(CUDAPRE_ERR_INVALID_ARGUMENT, "out_bytes %zu < %zu", out_bytes, sizeof(K2Geom));
+    if (h_ext->n <= 0) return fail(CUDAPRE_ERR_EMPTY_INPUT, "empty input");
+    if (h_ext->nang < 1 || h_ext->nang > CUDAPRE_MAX_ANGLES)
+        return fail(CUDAPRE_ERR_INVALID_ARGUMENT, "bad nang in extremes");
+    cudapre_polygon_t poly;
+    build_polygon(*h_ext, &poly, reinterpret_cast<K2Geom*>(h_out));
+    return CUDAPRE_OK;
+}
+
+cudapre_status cudapre_polygon_device(const cudapre_extremes_t* d_ext, void* d_ws, size_t ws_bytes, void* stream,
+                                      cudapre_polygon_t* d_poly) {
+    g_err.clear();
+    if (!d_ws || ((uintptr_t)d_ws & 15u) != 0 || ws_bytes < kWsFixedBytes)
+        return fail(CUDAPRE_ERR_INVALID_ARGUMENT, "d_ws must be a 16-byte aligned workspace");
+    const cudapre_extremes_t* ext = d_ext ? d_ext : &ws_header(d_ws)->result;
+    int launches = 0;
+    CUDA_TRY(launch_build_geom(ext, d_poly ? d_poly : ws_poly(d_ws), ws_geom(d_ws), stream, &launches));
+    return CUDAPRE_OK;
+}
+
+cudapre_status cudapre_filter_geom(const cudapre_pt* d_pts, int64_t n_local, int64_t index_base,
+                                   int64_t* d_surv_idx, cudapre_pt* d_surv_pts, int64_t capacity, void* d_ws,
+                                   size_t ws_bytes, void* stream, int64_t* d_count) {
+    g_err.clear();
+    cudapre_status st = check_points(d_pts, n_local);
+    if (st) return st;
+    if (capacity < 0) return fail(CUDAPRE_ERR_INVALID_ARGUMENT, "capacity < 0");
+    if (n_local > 0 && !d_surv_idx) return fail(CUDAPRE_ERR_INVALID_ARGUMENT, "d_surv_idx is NULL");
+    cudaStream_t strm = (cudaStream_t)stream;
+    if (n_local == 0) {
+        if (d_count) CUDA_TRY(cudaMemsetAsync(d_count, 0, sizeof(int64_t), strm));
+        return CUDAPRE_OK;
+    }
+    st = check_ws(d_ws, ws_bytes, n_local);
+    if (st) return st;
+    K2Params p;
+    std::memset(&p, 0, sizeof(p));
+    k2_params(p, d_pts, n_local, index_base, d_surv_idx, d_surv_pts, capacity, d_ws, ws_bytes);
+    const int vec16 = (((uintptr_t)d_pts & 15u) == 0);
+    int launches = 0;
+    CUDA_TRY(launch_filter(p, vec16, stream, &launches));
+    if (d_count)
+        CUDA_TRY(cudaMemcpyAsync(d_count, &p.ws->count, sizeof(int64_t), cudaMemcpyDeviceToDevice, strm));
+    return CUDAPRE_OK;
+}
+
+cudapre_status cudapre_filter_device(const cudapre_pt* d_pts, int64_t n_local, int64_t index_base,
+                                     const cudapre_extremes_t* d_ext, int64_t* d_surv_idx,
+                                     cudapre_pt* d_surv_pts, int64_t capacity, void* d_ws, size_t ws_bytes,
+                                     void* stream, int64_t* d_count, cudapre_polygon_t* d_poly) {
+    g_err.clear();
+    cudapre_status st = check_points(d_pts, n_local);
+    if (st) return st;
+    if (n_local > 0) {
+        st = check_ws(d_ws, ws_bytes, n_local);
+        if (st) return st;
+        st = cudapre_polygon_device(d_ext, d_ws, ws_bytes, stream, d_poly);
+        if (st) return st;
+    }
+    return cudapre_filter_geom(d_pts, n_local, index_base, d_surv_idx, d_surv_pts, capacity, d_ws, ws_bytes,
+                               stream, d_count);
+}
+
+cudapre_status cudapre_pipeline_device(const cudapre_pt* d_pts, int64_t n_local, int64_t index_base,
+                                       int32_t nang, const double* c, const double* s, int64_t* d_surv_idx,
+                                       cudapre_pt* d_surv_pts, int64_t capacity, void* d_ws, size_t ws_bytes,
+                                       void* stream, int64_t* d_count) {
+    cudapre_status st = cudapre_extremes(d_pts, n_local, index_base, nang, c, s, d_ws, ws_bytes, stream,
+                                         nullptr, nullptr, nullptr);
+    if (st) return st;
+    return cudapre_filter_device(d_pts, n_local, index_base, nullptr, d_surv_idx, d_surv_pts, capacity, d_ws,
+                                 ws_bytes, stream, d_count, nullptr);
+}
+
+struct cudapre_graph {
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+};
+
+cudapre_status cudapre_graph_destroy(cudapre_graph_t* g) {
+    if (!g) return CUDAPRE_OK;
+    if (g->exec) cudaGraphExecDestroy(g->exec);
+    if (g->graph) cudaGraphDestroy(g->graph);
+    delete g;
+    return CUDAPRE_OK;
+}
+
+cudapre_status cudapre_graph_create(const cudapre_pt* d_pts, int64_t n_local, int64_t index_base, int32_t nang,
+                                    const double* c, const double* s, int64_t* d_surv_idx,
+                                    cudapre_pt* d_surv_pts, int64_t capacity, void* d_ws, size_t ws_bytes,
+                                    void* stream, int64_t* d_count, cudapre_graph_t** out) {
+    g_err.clear();
+    if (!out) return fail(CUDAPRE_ERR_INVALID_ARGUMENT, "out is NULL");
+    *out = nullptr;
+    cudaStream_t strm = (cudaStream_t)stream;
+    // one uncaptured run: argument checks and the launchers' lazy set-up
+    cudapre_status st = cudapre_pipeline_device(d_pts, n_local, index_base, nang, c, s, d_surv_idx, d_surv_pts,
+                                                capacity, d_ws, ws_bytes, stream, d_count);
+    if (st) return st;
+    CUDA_TRY(cudaStreamSynchronize(strm));
+    cudaStream_t cs = nullptr;
+    CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    cudapre_graph_t* g = new cudapre_graph_t;
+    cudaError_t e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
+    if (e == cudaSuccess) {
+        st = cudapre_pipeline_device(d_pts, n_local, index_base, nang, c, s, d_surv_idx, d_surv_pts, capacity,
+                                     d_ws, ws_bytes, cs, d_count);
+        const cudaError_t e2 = cudaStreamEndCapture(cs, &g->graph);
+        if (!st && e2 != cudaSuccess) e = e2;
+    }
+    if (!st && e == cudaSuccess) e = cudaGraphInstantiate(&g->exec, g->graph, 0);
+    cudaStreamDestroy(cs);
+    if (st || e != cudaSuccess) {
+        cudapre_graph_destroy(g);
+        if (st) return st;
+        return fail(CUDAPRE_ERR_CUDA, "graph capture: %s", cudaGetErrorString(e));
+    }
+    *out = g;
+    return CUDAPRE_OK;
+}
+
+cudapre_status cudapre_graph_launch(cudapre_graph_t* g, void* stream) {
+    g_err.clear();
+    if (!g || !g->exec) return fail(CUDAPRE_ERR_INVALID_ARGUMENT, "graph is NULL");
+    CUDA_TRY(cudaGraphLaunch(g->exec, (cudaStream_t)stream));
+    return CUDAPRE_OK;
 }
 
 }  // extern "C"

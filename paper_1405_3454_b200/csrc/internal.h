@@ -25,7 +25,7 @@ constexpr int kMaxK1Blocks = 148 * 16;
 
 // ---------------------------------------------------------------- workspace
 // Device workspace layout (caller-owned, zero-filled once):
-//   [WsHeader, padded to 4 KiB][K1Partial x kMaxK1Blocks x 32][tile status x ntiles]
+//   [WsHeader, padded to 4 KiB][geometry page 32 KiB][K1Partial x kMaxK1Blocks x 32][tile status x ntiles]
 //   ... [TMA K2 list-overflow scratch, at the END of the buffer]
 // Every kernel leaves the counters it uses back at their reset values, so the
 // workspace stays valid from call to call.
@@ -56,6 +56,11 @@ struct K1Partial {
 };
 
 constexpr size_t kWsHeaderBytes = 4096;
+// geometry page after the header: K2Geom at +0, the device copy of the
+// polygon (cudapre_polygon_t) at +kWsPolyOff
+constexpr size_t kWsGeomBytes = 32768;
+constexpr size_t kWsPolyOff = 16384;
+constexpr size_t kWsFixedBytes = kWsHeaderBytes + kWsGeomBytes;   // header + geometry page
 constexpr size_t kWsPartialBytes = sizeof(K1Partial) * kMaxK1Blocks * CUDAPRE_MAX_SLOTS;
 
 // One tile-status word per super-tile, each on its own 128-byte line: packed
@@ -85,7 +90,7 @@ inline size_t ws_scratch_blocks(int64_t n) {
     return t < cap ? t : cap;
 }
 inline size_t ws_bytes_for(int64_t n) {   // (+16: alignment slack of the scratch at the end)
-    return kWsHeaderBytes + kWsPartialBytes + ws_status_bytes(n) + kK2ScratchPerBlock * ws_scratch_blocks(n) + 16;
+    return kWsFixedBytes + kWsPartialBytes + ws_status_bytes(n) + kK2ScratchPerBlock * ws_scratch_blocks(n) + 16;
 }
 
 // ---------------------------------------------------------------- kernel params
@@ -103,19 +108,13 @@ struct K1Params {
     int use_tma;                 // 1: stream through the cp.async.bulk ring (16-B aligned input)
 };
 
-struct K2Params {
-    const float* pts;
-    unsigned int n;
+// Step-3 geometry (built from the polygon on the host or on the device,
+// geom.cuh; lives in the workspace, read by the K2 kernels).
+struct K2Geom {
     int nv;                   // ring length
-    long long base;
-    long long* out_idx;
-    float* out_pts;           // nullable, float2 per survivor
-    unsigned long long capacity;
-    WsHeader* ws;
-    unsigned long long* status;   // ntiles tile-status words, kStatusStride apart
-    unsigned int num_tiles;
     int mode;                 // 0 = filter, 1 = keep everything (degenerate), 2 = exact only
-    int debug;                // perf experiments only (CUDAPRE_K2_DEBUG): 1 = skeleton, no classification
+    int fast;                 // TMA K2 pass-A test: 0 = inner disk, 1 = inner box, 2 = none
+    int pad;
     float bx0, bx1, by0, by1; // inner box (closed), strictly inside the ring
     float ox, oy, r2;         // inner disk: RN(RN(dx^2)+RN(dy^2)) < r2 => strictly inside (r2 < 0: off)
     float e2max;              // 2 * max_j E_j
@@ -126,7 +125,23 @@ struct K2Params {
     // edges a ray of bucket b can exit through: lo | hi << 8 (hi = lo or lo+1
     // cyclically); 0xffff = more than two (or no table): test every edge
     unsigned short sedge[CUDAPRE_SECTORS + 1];
-    int fast;                 // TMA K2 pass-A test: 0 = inner disk, 1 = inner box (the larger)
+};
+static_assert(sizeof(K2Geom) <= kWsPolyOff && sizeof(cudapre_polygon_t) <= kWsGeomBytes - kWsPolyOff,
+              "geometry page");
+
+struct K2Params {
+    const float* pts;
+    unsigned int n;
+    int edges;                // 16 or 32: unrolled edge-loop length (>= nv; 32 when nv is not known on the host)
+    long long base;
+    long long* out_idx;
+    float* out_pts;           // nullable, float2 per survivor
+    unsigned long long capacity;
+    WsHeader* ws;
+    unsigned long long* status;   // ntiles tile-status words, kStatusStride apart
+    unsigned int num_tiles;
+    int debug;                // perf experiments only (CUDAPRE_K2_DEBUG): 1 = skeleton, 2 = timing build
+    const K2Geom* g;          // device geometry (workspace)
     SurvEntry* scratch;       // TMA K2 list overflow, kK2ScratchPerBlock per block
     unsigned int scratch_blocks;   // blocks the scratch region covers (caps the TMA K2 grid)
 };
@@ -140,9 +155,13 @@ int k2_use_tma();   // CUDAPRE_K2_TMA (default 1)
 
 // ---------------------------------------------------------------- host geometry (host_geom.cpp)
 int orient_exact(float ax, float ay, float bx, float by, float cx, float cy);
-// Build the polygon + K2 coefficients from global extremes.  Fills poly and,
-// if kp != nullptr, the geometric fields of kp (nv, mode, box, A/B/C, e2max, v).
-void build_polygon(const cudapre_extremes_t& ext, cudapre_polygon_t* poly, K2Params* kp);
+// Step 2 from global extremes (geom.cuh): the polygon (poly) and, if g is
+// not null, the Step-3 geometry.  Sequential host build.
+void build_polygon(const cudapre_extremes_t& ext, cudapre_polygon_t* poly, K2Geom* g);
+// The same on the device: one block reads *d_ext and writes *d_poly, *d_g
+// (byte-identical to the host build).
+int launch_build_geom(const cudapre_extremes_t* d_ext, cudapre_polygon_t* d_poly, K2Geom* d_g, void* stream,
+                      int* launches);
 // Canonical monotone-chain ring of pts[ids[j]] (ids nullptr = identity).
 int64_t hull_ring(const cudapre_pt* pts, const int64_t* ids, int64_t n, int64_t* ring);
 void merge_extremes(const cudapre_extremes_t* parts, int count, cudapre_extremes_t* out);

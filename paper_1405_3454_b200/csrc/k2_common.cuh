@@ -52,9 +52,45 @@ __device__ __forceinline__ float4 load_pair(const float* pts, unsigned q, unsign
     return r;
 }
 
-__device__ __noinline__ bool exact_inside(const K2Params& p, float x, float y) {
-    for (int j = 0; j < p.nv; ++j)
-        if (orient_sign_f(p.vx[j], p.vy[j], p.vx[j + 1], p.vy[j + 1], x, y) <= 0) return false;
+// The part of K2Geom the per-point tests read, copied into shared memory at
+// block start (uniform addresses: broadcast loads).  The sector tables are
+// copied separately by the kernels that use them.
+struct GeomLite {
+    int nv, mode, fast, pad;
+    float bx0, bx1, by0, by1, ox, oy, r2, e2max;
+    float A[CUDAPRE_MAX_SLOTS], B[CUDAPRE_MAX_SLOTS], C[CUDAPRE_MAX_SLOTS];
+    float vx[CUDAPRE_MAX_SLOTS + 1], vy[CUDAPRE_MAX_SLOTS + 1];
+};
+// cooperative copy (all threads of the block; a barrier must follow)
+__device__ __forceinline__ void load_geom_lite(GeomLite& s, const K2Geom* __restrict__ g, unsigned tid,
+                                               unsigned nthreads) {
+    if (tid == 0) {
+        s.nv = g->nv;
+        s.mode = g->mode;
+        s.fast = g->fast;
+        s.bx0 = g->bx0;
+        s.bx1 = g->bx1;
+        s.by0 = g->by0;
+        s.by1 = g->by1;
+        s.ox = g->ox;
+        s.oy = g->oy;
+        s.r2 = g->r2;
+        s.e2max = g->e2max;
+    }
+    for (unsigned j = tid; j < (unsigned)CUDAPRE_MAX_SLOTS; j += nthreads) {
+        s.A[j] = g->A[j];
+        s.B[j] = g->B[j];
+        s.C[j] = g->C[j];
+    }
+    for (unsigned j = tid; j <= (unsigned)CUDAPRE_MAX_SLOTS; j += nthreads) {
+        s.vx[j] = g->vx[j];
+        s.vy[j] = g->vy[j];
+    }
+}
+
+__device__ __noinline__ bool exact_inside(const GeomLite& G, float x, float y) {
+    for (int j = 0; j < G.nv; ++j)
+        if (orient_sign_f(G.vx[j], G.vy[j], G.vx[j + 1], G.vy[j + 1], x, y) <= 0) return false;
     return true;
 }
 
@@ -62,34 +98,34 @@ __device__ __noinline__ bool exact_inside(const K2Params& p, float x, float y) {
 // Disk: (dx, dy) = RN((x, y) - (ox, oy)) in one FADD2, squares in one FMUL2,
 // d2 = RN(dx^2 + dy^2) >= true d^2 (1 - 4u) — the bound DESIGN.md §6.2 uses.
 // Bitwise (not short-circuit) logic: no branches.
-__device__ __forceinline__ bool fast_inside(const K2Params& p, float x, float y) {
-    const float2 d = __fadd2_rn(make_float2(x, y), make_float2(-p.ox, -p.oy));
+__device__ __forceinline__ bool fast_inside(const GeomLite& G, float x, float y) {
+    const float2 d = __fadd2_rn(make_float2(x, y), make_float2(-G.ox, -G.oy));
     const float2 d2 = __fmul2_rn(d, d);
-    const bool in_disk = __fadd_rn(d2.x, d2.y) < p.r2;
-    const bool in_box = (x >= p.bx0) & (x <= p.bx1) & (y >= p.by0) & (y <= p.by1);
+    const bool in_disk = __fadd_rn(d2.x, d2.y) < G.r2;
+    const bool in_box = (x >= G.bx0) & (x <= G.bx1) & (y >= G.by0) & (y <= G.by1);
     return in_disk | in_box;
 }
 
 // Survivor test for a point the fast tests could not decide (true = keep).
-// EDGES: compile-time edge count; the host pads edges nv..EDGES-1 with
-// A = B = 0, C = +inf (never the minimum), so the loop fully unrolls and the
-// coefficients are constant-bank operands of the FFMAs.
+// EDGES: compile-time edge count; the builder pads edges nv..31 with
+// A = B = 0, C = +inf (never the minimum), so the loop fully unrolls.
 template <int EDGES>
-__device__ __forceinline__ bool queue_keep(const K2Params& p, float x, float y) {
-    if (p.mode == 2) return !exact_inside(p, x, y);
+__device__ __forceinline__ bool queue_keep(const GeomLite& G, float x, float y) {
+    if (G.mode == 1) return true;
+    if (G.mode == 2) return !exact_inside(G, x, y);
     float mn = INFINITY;
 #pragma unroll
-    for (int j = 0; j < EDGES; ++j) mn = fminf(mn, __fmaf_rn(p.A[j], x, __fmaf_rn(p.B[j], y, p.C[j])));
+    for (int j = 0; j < EDGES; ++j) mn = fminf(mn, __fmaf_rn(G.A[j], x, __fmaf_rn(G.B[j], y, G.C[j])));
     if (mn > 0.0f) return false;
-    if (__fadd_rn(mn, p.e2max) < 0.0f) return true;
-    return !exact_inside(p, x, y);
+    if (__fadd_rn(mn, G.e2max) < 0.0f) return true;
+    return !exact_inside(G, x, y);
 }
 
 // Out-of-line copy for kernels where the all-edge loop is a rare path: inlined,
-// the compiler hoists its ~20 constant-bank loads onto the common path.
+// the compiler hoists its loads onto the common path.
 template <int EDGES>
-__device__ __noinline__ bool queue_keep_rare(const K2Params& p, float x, float y) {
-    return queue_keep<EDGES>(p, x, y);
+__device__ __noinline__ bool queue_keep_rare(const GeomLite& G, float x, float y) {
+    return queue_keep<EDGES>(G, x, y);
 }
 
 // ---------------------------------------------------------------- look-back

@@ -63,6 +63,7 @@ struct K2Smem {
     unsigned wsum[kK2Warps];
     unsigned next;
     unsigned long long prefix;
+    GeomLite geo;   // polygon scalars + coefficients (copied from p.g)
 };
 
 // Pass B of a resolved super-tile: write indices (+ coordinates).
@@ -131,8 +132,10 @@ __global__ void __launch_bounds__(kK2Threads, 2) k2_filter(const __grid_constant
     const unsigned lt = (1u << lane) - 1u;
     const unsigned epoch = *(volatile unsigned*)&p.ws->epoch;
 
+    load_geom_lite(S.geo, p.g, threadIdx.x, kK2Threads);
     if (threadIdx.x == 0) S.next = atomicAdd(&p.ws->k2_ticket, 1u);
     __syncthreads();
+    const int mode = S.geo.mode;
     unsigned tile = S.next;
     unsigned pend = 0xffffffffu;   // super-tile awaiting resolve + pass B
     unsigned lb_rounds = 0, lb_spins = 0;   // warp 0's look-back diagnostics
@@ -149,7 +152,7 @@ __global__ void __launch_bounds__(kK2Threads, 2) k2_filter(const __grid_constant
         const unsigned tbase = tile * kK2TilePairs;
         if (have) {
             // ---------------- pass A
-            const bool full_tile = p.mode == 0 && 2ull * (tbase + kK2TilePairs) <= (unsigned long long)p.n;
+            const bool full_tile = mode == 0 && 2ull * (tbase + kK2TilePairs) <= (unsigned long long)p.n;
             unsigned wc = 0;
 #pragma unroll 1
             for (int sub = 0; sub < kK2Sub; ++sub) {
@@ -167,8 +170,8 @@ __global__ void __launch_bounds__(kK2Threads, 2) k2_filter(const __grid_constant
                 if (full_tile) {
 #pragma unroll
                     for (int u = 0; u < kK2Items; ++u) {
-                        const unsigned in = (fast_inside(p, v[u].x, v[u].y) ? 1u : 0u) |
-                                            (fast_inside(p, v[u].z, v[u].w) ? 2u : 0u);
+                        const unsigned in = (fast_inside(S.geo, v[u].x, v[u].y) ? 1u : 0u) |
+                                            (fast_inside(S.geo, v[u].z, v[u].w) ? 2u : 0u);
                         needy |= (3u & ~in) << (2 * u);
                     }
                 } else {
@@ -176,12 +179,12 @@ __global__ void __launch_bounds__(kK2Threads, 2) k2_filter(const __grid_constant
                     for (int u = 0; u < kK2Items; ++u) {
                         const unsigned i0 = 2u * (qbase + u * kK2Threads);
                         const unsigned valid = (i0 < p.n ? 1u : 0u) | (i0 + 1u < p.n ? 2u : 0u);
-                        if (p.mode == 1) {
+                        if (mode == 1) {
                             keep |= valid << (2 * u);
                         } else {
                             const unsigned in =
-                                (p.mode == 0 && fast_inside(p, v[u].x, v[u].y) ? 1u : 0u) |
-                                (p.mode == 0 && fast_inside(p, v[u].z, v[u].w) ? 2u : 0u);
+                                (mode == 0 && fast_inside(S.geo, v[u].x, v[u].y) ? 1u : 0u) |
+                                (mode == 0 && fast_inside(S.geo, v[u].z, v[u].w) ? 2u : 0u);
                             needy |= (valid & ~in) << (2 * u);
                         }
                     }
@@ -216,7 +219,7 @@ __global__ void __launch_bounds__(kK2Threads, 2) k2_filter(const __grid_constant
                         if (e < qtotal) {
                             q = S.qxy[warp][e];
                             sl = S.qslot[warp][e];
-                            kp = queue_keep<EDGES>(p, q.x, q.y);
+                            kp = queue_keep<EDGES>(S.geo, q.x, q.y);
                         }
                         const unsigned kb = __ballot_sync(kFull, kp);
                         if (kp) {
@@ -236,7 +239,7 @@ __global__ void __launch_bounds__(kK2Threads, 2) k2_filter(const __grid_constant
                     __syncwarp();
                     keep |= S.own[warp][lane];
                 }
-                if (qtotal || p.mode == 1) {
+                if (qtotal || mode == 1) {
 #pragma unroll
                     for (int u = 0; u < kK2Items; ++u) {
                         const unsigned b0 = __ballot_sync(kFull, (keep >> (2 * u)) & 1u);
@@ -246,7 +249,7 @@ __global__ void __launch_bounds__(kK2Threads, 2) k2_filter(const __grid_constant
                             cur.mask[g][0] = b0;
                             cur.mask[g][1] = b1;
                         }
-                        if (p.mode == 1) wc += __popc(b0) + __popc(b1);   // list unused: dense pass B
+                        if (mode == 1) wc += __popc(b0) + __popc(b1);   // list unused: dense pass B
                     }
                 } else if (lane < kK2Items) {
                     const unsigned g = (sub * kK2Items + lane) * kK2Warps + warp;
@@ -258,7 +261,7 @@ __global__ void __launch_bounds__(kK2Threads, 2) k2_filter(const __grid_constant
                     for (int u = 0; u < kK2Items; ++u) v[u] = vn[u];
                 }
             }
-            if (lane == 0) cur.wcnt[warp] = (p.mode == 1) ? kList + 1u : wc;
+            if (lane == 0) cur.wcnt[warp] = (mode == 1) ? kList + 1u : wc;
             // next ticket only now: a tile is never held while its block is busy
             if (threadIdx.x == 0) S.next = atomicAdd(&p.ws->k2_ticket, 1u);
             __syncthreads();
@@ -369,9 +372,9 @@ int k2_use_tma() {
 }
 
 int launch_filter(const K2Params& p, int vec16, void* stream, int* launches) {
-    if (vec16 && p.mode == 0 && k2_use_tma()) return launch_filter_tma(p, stream, launches);
+    if (vec16 && k2_use_tma()) return launch_filter_tma(p, stream, launches);   // (handles every mode)
     cudaStream_t s = (cudaStream_t)stream;
-    if (p.nv <= 16)
+    if (p.edges <= 16)
         return vec16 ? (int)launch_t<true, 16>(p, s, launches) : (int)launch_t<false, 16>(p, s, launches);
     return vec16 ? (int)launch_t<true, 32>(p, s, launches) : (int)launch_t<false, 32>(p, s, launches);
 }

@@ -73,6 +73,7 @@ struct SmemT {
     float2 sec[CUDAPRE_SECTORS + 1];               // {inner r^2, outer r^2} per bucket
     unsigned short sedge[CUDAPRE_SECTORS + 1];     // candidate exit edges per bucket
     float4 edge[CUDAPRE_MAX_SLOTS];                // {A, B, C', 0} (C' already lowered by E_j)
+    GeomLite geo;                                  // scalars, coefficients, ring (rare paths)
     unsigned stile[kNst];   // super-tile id of the sub-tile-0 stage (kNone = end)
 };
 
@@ -90,10 +91,13 @@ __device__ __forceinline__ float rcp_approx(float a) {
 // through one of the bucket's candidate edges, so "inside" = inside those
 // edges; float lines with the error margin E_j folded into C' decide unless
 // |g| is within 2 Emax, then the exact predicate over the whole ring.
+// Mode 1 (degenerate ring: keep everything) and mode 2 (coefficients out of
+// float range: exact predicate only) take the uniform early exits.
 template <int EDGES, int kNst, unsigned kL>
-__device__ __forceinline__ bool classify_queued(const K2Params& p, const SmemT<kNst, kL>& S, float x,
-                                                float y) {
-    const float2 d = __fadd2_rn(make_float2(x, y), make_float2(-p.ox, -p.oy));
+__device__ __forceinline__ bool classify_queued(const SmemT<kNst, kL>& S, int mode, float ox, float oy,
+                                                float e2max, float x, float y) {
+    if (mode != 0) return mode == 1 ? true : !exact_inside(S.geo, x, y);
+    const float2 d = __fadd2_rn(make_float2(x, y), make_float2(-ox, -oy));
     const float2 q = __fmul2_rn(d, d);
     const float d2 = __fadd_rn(q.x, q.y);
     const float t = __fmul_rn(d.y, rcp_approx(__fadd_rn(fabsf(d.x), fabsf(d.y))));
@@ -104,24 +108,24 @@ __device__ __forceinline__ bool classify_queued(const K2Params& p, const SmemT<k
     if (d2 < rr.x) return false;
     if (d2 > rr.y) return true;
     const unsigned se = S.sedge[b];
-    if (se == 0xffffu) return queue_keep_rare<EDGES>(p, x, y);
+    if (se == 0xffffu) return queue_keep_rare<EDGES>(S.geo, x, y);
     const float4 e0 = S.edge[se & 0xffu], e1 = S.edge[se >> 8];
     const float mn = fminf(__fmaf_rn(e0.x, x, __fmaf_rn(e0.y, y, e0.z)),
                            __fmaf_rn(e1.x, x, __fmaf_rn(e1.y, y, e1.z)));
     if (mn > 0.0f) return false;
-    if (__fadd_rn(mn, p.e2max) < 0.0f) return true;
-    return !exact_inside(p, x, y);
+    if (__fadd_rn(mn, e2max) < 0.0f) return true;
+    return !exact_inside(S.geo, x, y);
 }
 
-// inner box, closed (host-proven strictly inside)
-__device__ __forceinline__ bool in_box(const K2Params& p, float x, float y) {
-    return (x >= p.bx0) & (x <= p.bx1) & (y >= p.by0) & (y <= p.by1);
+// inner box, closed (proven strictly inside by the builder)
+__device__ __forceinline__ bool in_box(float bx0, float bx1, float by0, float by1, float x, float y) {
+    return (x >= bx0) & (x <= bx1) & (y >= by0) & (y <= by1);
 }
 // inner disk: RN(RN(dx^2) + RN(dy^2)) < r2 (DESIGN.md §6.2 bound)
-__device__ __forceinline__ bool in_disk(const K2Params& p, float x, float y) {
-    const float2 d = __fadd2_rn(make_float2(x, y), make_float2(-p.ox, -p.oy));
+__device__ __forceinline__ bool in_disk(float ox, float oy, float r2, float x, float y) {
+    const float2 d = __fadd2_rn(make_float2(x, y), make_float2(-ox, -oy));
     const float2 d2 = __fmul2_rn(d, d);
-    return __fadd_rn(d2.x, d2.y) < p.r2;
+    return __fadd_rn(d2.x, d2.y) < r2;
 }
 
 // bytes of full point pairs of sub-tile `sub` of super-tile `tile` in memory
@@ -189,11 +193,12 @@ __global__ void __launch_bounds__(kBlock, K2Cfg<CFG>::kMinB) k2_filter_tma(const
     SurvT* const sbase = p.scratch + (size_t)blockIdx.x * (kBufs * kW * kK2WarpPts);
 
     for (int i = threadIdx.x; i <= CUDAPRE_SECTORS; i += kBlock) {
-        S.sec[i] = make_float2(p.sr2[i], p.sro2[i]);
-        S.sedge[i] = p.sedge[i];
+        S.sec[i] = make_float2(p.g->sr2[i], p.g->sro2[i]);
+        S.sedge[i] = p.g->sedge[i];
     }
     if (threadIdx.x < (unsigned)CUDAPRE_MAX_SLOTS)
-        S.edge[threadIdx.x] = make_float4(p.A[threadIdx.x], p.B[threadIdx.x], p.C[threadIdx.x], 0.0f);
+        S.edge[threadIdx.x] = make_float4(p.g->A[threadIdx.x], p.g->B[threadIdx.x], p.g->C[threadIdx.x], 0.0f);
+    load_geom_lite(S.geo, p.g, threadIdx.x, kBlock);
     if (threadIdx.x == 0) {
         for (int k = 0; k < kNst; ++k) {
             mbar_init(&S.full[k], 1u);
@@ -343,7 +348,9 @@ __global__ void __launch_bounds__(kBlock, K2Cfg<CFG>::kMinB) k2_filter_tma(const
     // Pass A only: classify each sub-tile from the ring, build the per-warp
     // survivor lists of super-tile k in buffer k % kBufs, signal the emit warp,
     // go on with the next super-tile.  No block-wide barriers.
-    const int fast = p.fast;
+    const int fast = S.geo.fast, mode = S.geo.mode;
+    const float gox = S.geo.ox, goy = S.geo.oy, gr2 = S.geo.r2, ge2 = S.geo.e2max;
+    const float gbx0 = S.geo.bx0, gbx1 = S.geo.bx1, gby0 = S.geo.by0, gby1 = S.geo.by1;
     unsigned seq = 0;
     unsigned long long dc[2] = {0, 0}, t0 = 0;   // DBG: pass A, buffer waits
     for (unsigned k = 0;; ++k) {
@@ -375,16 +382,20 @@ __global__ void __launch_bounds__(kBlock, K2Cfg<CFG>::kMinB) k2_filter_tma(const
 #pragma unroll
                         for (int u = 0; u < kK2Items; ++u) {
                             const float4 v = chunk[u * 32 + lane];
-                            const unsigned in = (in_disk(p, v.x, v.y) ? 1u : 0u) | (in_disk(p, v.z, v.w) ? 2u : 0u);
+                            const unsigned in = (in_disk(gox, goy, gr2, v.x, v.y) ? 1u : 0u) |
+                                                (in_disk(gox, goy, gr2, v.z, v.w) ? 2u : 0u);
                             needy |= (3u & ~in) << (2 * u);
                         }
-                    } else {
+                    } else if (fast == 1) {
 #pragma unroll
                         for (int u = 0; u < kK2Items; ++u) {
                             const float4 v = chunk[u * 32 + lane];
-                            const unsigned in = (in_box(p, v.x, v.y) ? 1u : 0u) | (in_box(p, v.z, v.w) ? 2u : 0u);
+                            const unsigned in = (in_box(gbx0, gbx1, gby0, gby1, v.x, v.y) ? 1u : 0u) |
+                                                (in_box(gbx0, gbx1, gby0, gby1, v.z, v.w) ? 2u : 0u);
                             needy |= (3u & ~in) << (2 * u);
                         }
+                    } else {   // no fast test (degenerate / exact-only rings): queue everything
+                        needy = 0xffu;
                     }
                 } else {   // last super-tile only: ragged end (+ the unpaired last point)
                     const unsigned qs = tile * kK2TilePairs + sub * kK2SubPairs;
@@ -401,7 +412,7 @@ __global__ void __launch_bounds__(kBlock, K2Cfg<CFG>::kMinB) k2_filter_tma(const
                             v = make_float4(a.x, a.y, 0.f, 0.f);
                             valid = 1u;
                         }
-                        const unsigned in = (fast_inside(p, v.x, v.y) ? 1u : 0u) | (fast_inside(p, v.z, v.w) ? 2u : 0u);
+                        const unsigned in = (fast_inside(S.geo, v.x, v.y) ? 1u : 0u) | (fast_inside(S.geo, v.z, v.w) ? 2u : 0u);
                         needy |= (valid & ~in) << (2 * u);
                     }
                 }
@@ -435,7 +446,7 @@ __global__ void __launch_bounds__(kBlock, K2Cfg<CFG>::kMinB) k2_filter_tma(const
                             } else {   // the unpaired last point
                                 q = __ldg(reinterpret_cast<const float2*>(p.pts) + 2u * full_pairs);
                             }
-                            kp = classify_queued<EDGES>(p, S, q.x, q.y);
+                            kp = classify_queued<EDGES>(S, mode, gox, goy, ge2, q.x, q.y);
                         }
                         const unsigned kb = __ballot_sync(kFull, kp);
                         if (kp) {
@@ -518,10 +529,10 @@ int k2_cfg() {
 int launch_filter_tma(const K2Params& p, void* stream, int* launches) {
     cudaStream_t s = (cudaStream_t)stream;
     if (p.debug == 2)
-        return p.nv <= 16 ? (int)launch_tma_t<16, 0, true>(p, s, launches) : (int)launch_tma_t<32, 0, true>(p, s, launches);
+        return p.edges <= 16 ? (int)launch_tma_t<16, 0, true>(p, s, launches) : (int)launch_tma_t<32, 0, true>(p, s, launches);
     if (k2_cfg() == 1)
-        return p.nv <= 16 ? (int)launch_tma_t<16, 1>(p, s, launches) : (int)launch_tma_t<32, 1>(p, s, launches);
-    return p.nv <= 16 ? (int)launch_tma_t<16, 0>(p, s, launches) : (int)launch_tma_t<32, 0>(p, s, launches);
+        return p.edges <= 16 ? (int)launch_tma_t<16, 1>(p, s, launches) : (int)launch_tma_t<32, 1>(p, s, launches);
+    return p.edges <= 16 ? (int)launch_tma_t<16, 0>(p, s, launches) : (int)launch_tma_t<32, 0>(p, s, launches);
 }
 
 }  // namespace cudapre

@@ -1,0 +1,111 @@
+"""Device-resident Steps 2-3: the polygon and the Step-3
+geometry built on the device must equal the host build byte for byte, and
+the device path (filter_device, pipeline, CUDA graph) must return exactly the
+oracle's survivors — the same bar as the host path (tests/test_gpu_parity.py).
+"""
+import ctypes
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_1405_3454_b200 as cp
+import synth
+
+pytestmark = pytest.mark.gpu
+
+THREADS = max(1, min(64, os.cpu_count() or 1))
+
+
+def _device_pages(ws, nbytes_geom):
+    t = ws.tensor
+    geom = bytes(t[cp.WS_GEOM_OFFSET:cp.WS_GEOM_OFFSET + nbytes_geom].cpu().numpy().tobytes())
+    psz = ctypes.sizeof(cp.PolygonT)
+    poly = bytes(t[cp.WS_POLY_OFFSET:cp.WS_POLY_OFFSET + psz].cpu().numpy().tobytes())
+    return geom, poly
+
+
+@pytest.mark.parametrize("family", ["square", "disk", "gauss", "circle"])
+@pytest.mark.parametrize("angles", ["A", "B", "C", "AT", "D"])
+@pytest.mark.parametrize("n", [3, 1_001, 300_007])
+def test_device_geometry_byte_identical_and_survivors(family, angles, n):
+    xy = synth.generate(family, n, seed=n % 97 + 5)
+    pts = torch.from_numpy(xy).cuda()
+    ws = cp.Workspace(n)
+    ext = cp.extremes(pts, angles, ws=ws)                   # K1 leaves its result in ws too
+    out_idx, out_pts, count = cp.filter_device(pts, ws=ws)  # Step 2 on the device, then K2
+    torch.cuda.synchronize()
+    host_geom = cp.geometry(ext)
+    host_poly = bytes(cp.polygon(ext).raw)
+    dev_geom, dev_poly = _device_pages(ws, len(host_geom))
+    assert dev_geom == host_geom
+    assert dev_poly == host_poly
+    m = int(count.item())
+    want = oracle.cudapre(xy, angles, threads=THREADS)
+    assert np.array_equal(out_idx[:m].cpu().numpy(), want["survivors"])
+    assert np.array_equal(out_pts[:m].cpu().numpy(), xy[want["survivors"]])
+
+
+def test_device_geometry_adversarial_inputs():
+    """Ties, collinear extremes, far-off centres, tiny and huge magnitudes."""
+    rng = np.random.default_rng(4)
+    cases = [
+        np.round(synth.generate("disk", 50_001, seed=1) * 8).astype(np.float32),       # heavy ties
+        np.stack([np.linspace(-1, 1, 20_001), np.linspace(-1, 1, 20_001) * 0.5], 1).astype(np.float32),
+        (synth.generate("disk", 80_001, seed=2) + np.float32(4096.0)).astype(np.float32),
+        (synth.generate("gauss", 80_001, seed=3).astype(np.float64) * 1e-30).astype(np.float32),
+        (synth.generate("square", 80_001, seed=4).astype(np.float64) * 1e30).astype(np.float32),
+        rng.integers(-3, 4, (60_001, 2)).astype(np.float32),                              # lattice
+    ]
+    for xy in cases:
+        pts = torch.from_numpy(np.ascontiguousarray(xy)).cuda()
+        ws = cp.Workspace(len(xy))
+        ext = cp.extremes(pts, "A", ws=ws)
+        out_idx, _, count = cp.filter_device(pts, ws=ws, return_points=False)
+        torch.cuda.synchronize()
+        host_geom = cp.geometry(ext)
+        dev_geom, dev_poly = _device_pages(ws, len(host_geom))
+        assert dev_geom == host_geom
+        assert dev_poly == bytes(cp.polygon(ext).raw)
+        want = oracle.cudapre(xy, "A", threads=THREADS)["survivors"]
+        assert np.array_equal(out_idx[: int(count.item())].cpu().numpy(), want)
+
+
+def test_pipeline_and_graph_match_oracle():
+    for fam, n in (("disk", 1_000_003), ("square", 300_001), ("circle", 200_003)):
+        xy = synth.generate(fam, n, seed=11)
+        pts = torch.from_numpy(xy).cuda()
+        want = oracle.cudapre(xy, "A", threads=THREADS)["survivors"]
+        out_idx, out_pts, count = cp.pipeline(pts, "A")
+        torch.cuda.synchronize()
+        assert np.array_equal(out_idx[: int(count.item())].cpu().numpy(), want)
+        g = cp.Graph(pts, "A")
+        for _ in range(3):
+            g.count.zero_()
+            g.launch()
+            torch.cuda.synchronize()
+            m = int(g.count.item())
+            assert np.array_equal(g.out_idx[:m].cpu().numpy(), want)
+            assert np.array_equal(g.out_pts[:m].cpu().numpy(), xy[want])
+        g.close()
+
+
+def test_device_path_degenerate_and_misaligned():
+    # all points on one line: degenerate ring, everything survives
+    t = np.linspace(-1, 1, 10_001, dtype=np.float32)
+    xy = np.stack([t, 2 * t], 1)
+    out_idx, _, count = cp.pipeline(torch.from_numpy(xy).cuda(), "A", return_points=False)
+    torch.cuda.synchronize()
+    assert int(count.item()) == len(xy)
+    assert np.array_equal(out_idx[: len(xy)].cpu().numpy(), np.arange(len(xy)))
+    # 8-byte aligned input: register K2 kernel with the device geometry
+    xy = synth.generate("gauss", 300_000, seed=2)
+    full = torch.from_numpy(xy).cuda()
+    view = full[1:]
+    assert view.data_ptr() % 16 == 8
+    out_idx, _, count = cp.pipeline(view, "A", index_base=1, return_points=False)
+    torch.cuda.synchronize()
+    want = oracle.cudapre(xy[1:], "A", threads=THREADS)["survivors"]
+    assert np.array_equal(out_idx[: int(count.item())].cpu().numpy() - 1, want)
