@@ -46,7 +46,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--host-step2", action="store_true",
-                    help="N=1: run Step 2 on the host between the kernels (as the paper) instead of on the device")
+                    help="run Step 2 (and, N > 1, the merge) on the host between the kernels, as the paper")
     return ap.parse_args()
 
 
@@ -209,11 +209,14 @@ def main():
         idx, sp, rep2 = cp.filter(pts, ext, index_base=base, ws=ws, out_idx=out_idx, out_pts=out_pts)
         return idx.shape[0], rep2
 
-    # N = 1: Steps 1-3 stay on the device (Step 2 by the device builder, SURVEY
-    # §8 f3), the host only enqueues; CUDA events between the three calls
-    # time seed+K1, Step 2 and K2 separately on the stream they run on.
-    device_path = group is None and not args.host_step2
+    # Steps 1-3 stay on the device (Step 2 by the device builder, SURVEY §8
+    # f3; N > 1: NCCL all-gather of the ranks' Step-1 blocks straight from the
+    # workspace, merged by the builder), the host only enqueues; CUDA events
+    # between the calls time seed+K1, (all-gather +) Step 2 and K2 separately
+    # on the stream they run on.
+    device_path = not args.host_step2
     count = torch.zeros(1, dtype=torch.int64, device="cuda")
+    gathered = torch.empty(world * cp.EXTREMES_BYTES, dtype=torch.uint8, device="cuda")
 
     def dstep(ev):
         if ev:
@@ -221,7 +224,11 @@ def main():
         cp.extremes_device(pts, args.angles, index_base=base, ws=ws)
         if ev:
             ev[1].record()
-        cp.polygon_device(ws)
+        if group is not None:
+            dist.all_gather_into_tensor(gathered, cp.result_view(ws), group=group)
+            cp.polygon_device(ws, parts=gathered, nparts=world)
+        else:
+            cp.polygon_device(ws)
         if ev:
             ev[2].record()
         cp.filter_geom(pts, index_base=base, ws=ws, out_idx=out_idx, out_pts=out_pts, count=count)
@@ -376,14 +383,14 @@ def main():
                        "l2": (f"inputs larger than L2 ({8 * n_local / 1e9:.2f} GB vs 126 MB), no flush"
                               if 8 * n_local > 126e6 else
                               f"inputs ({8 * n_local / 1e6:.0f} MB) fit in L2: warm-L2 numbers, not a roofline claim"),
-                       "parallelism": f"dp{world} (point shards; 912 B NCCL all-gather per step)"},
+                       "parallelism": f"dp{world} (point shards; 912 B NCCL all-gather per step)",
+                       "step2": "device" if device_path else "host"},
             "discard_pct": round(100 * (1 - surv_total / n_total), 4),
             "remaining_pct": round(100 * surv_total / n_total, 4),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": clocks.result(),
             "k1_exact_path_points_per_step": int(exact_pts[0]),
             ("host_step2_ms" if not device_path else "step2_device_ms"): round(statistics.median(poly_ms), 4),
-            "step2": "device" if device_path else "host",
             "k2_lookback_rounds_per_step": int(lb_rounds[0]), "k2_lookback_spins_per_step": int(lb_rounds[1]),
         }
         print(json.dumps(line), flush=True)

@@ -251,9 +251,10 @@ cudapre_status cudapre_run_host(const cudapre_pt* h_pts, int64_t n, int32_t nang
  * Workspace pages written by the device path (readable by the caller): the
  * Step-3 geometry at byte CUDAPRE_WS_GEOM_OFFSET and the polygon
  * (cudapre_polygon_t) at CUDAPRE_WS_POLY_OFFSET; the Step-1 result that
- * cudapre_extremes leaves on the device is in the workspace header.      */
+ * cudapre_extremes leaves on the device at CUDAPRE_WS_RESULT_OFFSET.     */
 #define CUDAPRE_WS_GEOM_OFFSET 4096
 #define CUDAPRE_WS_POLY_OFFSET (4096 + 16384)
+#define CUDAPRE_WS_RESULT_OFFSET 176   /* the Step-1 result K1 leaves (cudapre_extremes_t) */
 
 /* Host build of the Step-3 geometry block for h_ext (the block the device
  * path writes at CUDAPRE_WS_GEOM_OFFSET), for tests and inspection.
@@ -262,12 +263,18 @@ cudapre_status cudapre_run_host(const cudapre_pt* h_pts, int64_t n, int32_t nang
 cudapre_status cudapre_geometry(const cudapre_extremes_t* h_ext, void* h_out, size_t out_bytes,
                                 size_t* needed);
 
-/* Step 2 on the device: builds the polygon and the Step-3 geometry from the
- * device Step-1 result d_ext (NULL = the one cudapre_extremes left in d_ws)
- * into the workspace pages (and into d_poly if not NULL).  One block, one
- * launch; byte-identical to cudapre_polygon / cudapre_geometry.            */
-cudapre_status cudapre_polygon_device(const cudapre_extremes_t* d_ext, void* d_ws, size_t ws_bytes,
-                                      void* stream, cudapre_polygon_t* d_poly);
+/* Step 2 on the device: builds the polygon and the Step-3 geometry into the
+ * workspace pages (and into d_poly if not NULL) from
+ *   d_parts, nparts  device Step-1 results of nparts shards (e.g. an NCCL
+ *                    all-gather of every rank's CUDAPRE_WS_RESULT_OFFSET
+ *                    block), merged here with the rule of
+ *                    cudapre_extremes_merge and the merge written to
+ *                    this workspace's result block; d_parts NULL / nparts
+ *                    <= 1: the result cudapre_extremes left in d_ws.
+ * One block, one launch; byte-identical to cudapre_extremes_merge +
+ * cudapre_polygon / cudapre_geometry.                                      */
+cudapre_status cudapre_polygon_device(const cudapre_extremes_t* d_parts, int32_t nparts, void* d_ws,
+                                      size_t ws_bytes, void* stream, cudapre_polygon_t* d_poly);
 
 /* Step 3 alone, with the geometry already in the workspace (from
  * cudapre_polygon_device): the K2 launch + the device count copy.        */

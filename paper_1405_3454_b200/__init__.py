@@ -84,6 +84,7 @@ SYMBOLS = ["cudapre_version", "cudapre_last_error", "cudapre_angles_preset",
            "cudapre_polygon_device", "cudapre_filter_geom"]
 WS_GEOM_OFFSET = 4096            # include/cudapre.h CUDAPRE_WS_GEOM_OFFSET
 WS_POLY_OFFSET = 4096 + 16384    # CUDAPRE_WS_POLY_OFFSET
+WS_RESULT_OFFSET = 176           # CUDAPRE_WS_RESULT_OFFSET
 
 _lib = None
 
@@ -118,7 +119,7 @@ def lib():
     L.cudapre_graph_create.argtypes = [vp, i64, i64, i32, vp, vp, vp, vp, i64, vp, sz, vp, vp, P(vp)]
     L.cudapre_graph_launch.argtypes = [vp, vp]
     L.cudapre_graph_destroy.argtypes = [vp]
-    L.cudapre_polygon_device.argtypes = [vp, vp, sz, vp, vp]
+    L.cudapre_polygon_device.argtypes = [vp, i32, vp, sz, vp, vp]
     L.cudapre_filter_geom.argtypes = [vp, i64, i64, vp, vp, i64, vp, sz, vp, vp]
     for name in SYMBOLS[2:]:
         if name not in ("cudapre_workspace_bytes",):
@@ -443,11 +444,18 @@ def extremes_device(pts, angles_="A", index_base: int = 0, ws=None, stream=None)
         w.ptr, w.nbytes, _stream_ptr(stream), None, None, None))
 
 
-def polygon_device(ws, ext_dev=None, d_poly=None, stream=None):
-    """Step 2 on the device into the workspace pages (see filter_device)."""
+def polygon_device(ws, parts=None, nparts: int = 0, d_poly=None, stream=None):
+    """Step 2 on the device into the workspace pages.  parts: a device buffer
+    of nparts Step-1 results (EXTREMES_BYTES each, e.g. an all-gather of every
+    rank's result_view(ws)), merged first; None: the result in ws."""
     _check(lib().cudapre_polygon_device(
-        ctypes.c_void_p(ext_dev.data_ptr()) if ext_dev is not None else None, ws.ptr, ws.nbytes,
+        ctypes.c_void_p(parts.data_ptr()) if parts is not None else None, int(nparts), ws.ptr, ws.nbytes,
         _stream_ptr(stream), ctypes.c_void_p(d_poly.data_ptr()) if d_poly is not None else None))
+
+
+def result_view(ws):
+    """The workspace's Step-1 result block as a uint8 device tensor (no copy)."""
+    return ws.tensor[WS_RESULT_OFFSET:WS_RESULT_OFFSET + EXTREMES_BYTES]
 
 
 def filter_geom(pts, index_base: int = 0, ws=None, out_idx=None, out_pts=None, count=None, stream=None):

@@ -100,7 +100,8 @@ void preset_coef(double deg, double* c, double* s) {
 }
 
 WsHeader* ws_header(void* d_ws) { return reinterpret_cast<WsHeader*>(d_ws); }
-static_assert(CUDAPRE_WS_GEOM_OFFSET == kWsHeaderBytes && CUDAPRE_WS_POLY_OFFSET == kWsHeaderBytes + kWsPolyOff,
+static_assert(CUDAPRE_WS_GEOM_OFFSET == kWsHeaderBytes && CUDAPRE_WS_POLY_OFFSET == kWsHeaderBytes + kWsPolyOff &&
+                  CUDAPRE_WS_RESULT_OFFSET == offsetof(WsHeader, result),
               "workspace page offsets in include/cudapre.h");
 K2Geom* ws_geom(void* d_ws) { return reinterpret_cast<K2Geom*>(reinterpret_cast<char*>(d_ws) + kWsHeaderBytes); }
 cudapre_polygon_t* ws_poly(void* d_ws) {
@@ -457,14 +458,18 @@ cudapre_status cudapre_geometry(const cudapre_extremes_t* h_ext, void* h_out, si
     return CUDAPRE_OK;
 }
 
-cudapre_status cudapre_polygon_device(const cudapre_extremes_t* d_ext, void* d_ws, size_t ws_bytes, void* stream,
-                                      cudapre_polygon_t* d_poly) {
+cudapre_status cudapre_polygon_device(const cudapre_extremes_t* d_parts, int32_t nparts, void* d_ws,
+                                      size_t ws_bytes, void* stream, cudapre_polygon_t* d_poly) {
     g_err.clear();
     if (!d_ws || ((uintptr_t)d_ws & 15u) != 0 || ws_bytes < kWsFixedBytes)
         return fail(CUDAPRE_ERR_INVALID_ARGUMENT, "d_ws must be a 16-byte aligned workspace");
-    const cudapre_extremes_t* ext = d_ext ? d_ext : &ws_header(d_ws)->result;
+    if (nparts < 0 || (nparts > 1 && !d_parts))
+        return fail(CUDAPRE_ERR_INVALID_ARGUMENT, "nparts > 1 needs d_parts");
+    cudapre_extremes_t* res = &ws_header(d_ws)->result;
+    const cudapre_extremes_t* parts = d_parts ? d_parts : res;
     int launches = 0;
-    CUDA_TRY(launch_build_geom(ext, d_poly ? d_poly : ws_poly(d_ws), ws_geom(d_ws), stream, &launches));
+    CUDA_TRY(launch_build_geom(parts, nparts > 1 ? nparts : 1, nparts > 1 ? res : nullptr,
+                               d_poly ? d_poly : ws_poly(d_ws), ws_geom(d_ws), stream, &launches));
     return CUDAPRE_OK;
 }
 
@@ -504,7 +509,7 @@ cudapre_status cudapre_filter_device(const cudapre_pt* d_pts, int64_t n_local, i
     if (n_local > 0) {
         st = check_ws(d_ws, ws_bytes, n_local);
         if (st) return st;
-        st = cudapre_polygon_device(d_ext, d_ws, ws_bytes, stream, d_poly);
+        st = cudapre_polygon_device(d_ext, d_ext ? 1 : 0, d_ws, ws_bytes, stream, d_poly);
         if (st) return st;
     }
     return cudapre_filter_geom(d_pts, n_local, index_base, d_surv_idx, d_surv_pts, capacity, d_ws, ws_bytes,

@@ -131,6 +131,52 @@ GEOM_HD bool strictly_inside_ring(const float* vx, const float* vy, int nv, floa
     return true;
 }
 
+// ------------------------------------------------------------------ cross-shard merge
+// Slot s of the merge of `count` per-shard Step-1 results: the lexicographic
+// (key, global index) best (lowest index on equal keys, A7); per slot, so
+// slots can be merged in parallel.
+GEOM_HD void merge_slot(const cudapre_extremes_t* parts, int count, int s, cudapre_extremes_t& r) {
+    const bool is_max = (s & 1) != 0;
+    long long idx = -1;
+    double key = 0.0;
+    cudapre_pt pt = {0.f, 0.f};
+    for (int p = 0; p < count; ++p) {
+        const cudapre_extremes_t& q = parts[p];
+        if (q.idx[s] < 0) continue;
+        bool better;
+        if (idx < 0) better = true;
+        else if (q.key[s] == key) better = q.idx[s] < idx;
+        else better = is_max ? (q.key[s] > key) : (q.key[s] < key);
+        if (better) {
+            idx = q.idx[s];
+            key = q.key[s];
+            pt = q.pt[s];
+        }
+    }
+    r.idx[s] = idx;
+    r.key[s] = idx < 0 ? parts[0].key[s] : key;
+    r.pt[s] = idx < 0 ? parts[0].pt[s] : pt;
+}
+// Everything but the slots (one thread): counts and flags summed / or-ed,
+// angles and unused slots from part 0.
+GEOM_HD void merge_header(const cudapre_extremes_t* parts, int count, cudapre_extremes_t& r) {
+    r.nang = parts[0].nang;
+    long long n = 0, ex = 0;
+    int nf = 0;
+    for (int p = 0; p < count; ++p) {
+        n += parts[p].n;
+        nf |= parts[p].nonfinite;
+        ex += parts[p].exact_points;
+    }
+    r.n = n;
+    r.nonfinite = nf;
+    r.exact_points = ex;
+    for (int k = 0; k < CUDAPRE_MAX_ANGLES; ++k) {
+        r.c[k] = parts[0].c[k];
+        r.s[k] = parts[0].s[k];
+    }
+}
+
 // ------------------------------------------------------------------ phase A (one thread)
 // Picks -> Andrew's monotone chain (A9, A10): lexicographic (x, y, id)
 // order, distinct coordinates keep the lowest id (-0 == +0), pop while not a

@@ -80,35 +80,9 @@ int64_t hull_ring(const cudapre_pt* pts, const int64_t* ids, int64_t n, int64_t*
 }
 
 void merge_extremes(const cudapre_extremes_t* parts, int count, cudapre_extremes_t* out) {
-    cudapre_extremes_t r = parts[0];
-    r.n = 0;
-    r.nonfinite = 0;
-    r.exact_points = 0;
-    const int slots = 4 * r.nang;
-    for (int s = 0; s < slots; ++s) r.idx[s] = -1;
-    for (int p = 0; p < count; ++p) {
-        const cudapre_extremes_t& q = parts[p];
-        r.n += q.n;
-        r.nonfinite |= q.nonfinite;
-        r.exact_points += q.exact_points;
-        for (int s = 0; s < slots; ++s) {
-            if (q.idx[s] < 0) continue;
-            const bool is_max = (s & 1) != 0;
-            bool better;
-            if (r.idx[s] < 0) {
-                better = true;
-            } else if (q.key[s] == r.key[s]) {
-                better = q.idx[s] < r.idx[s];   // lowest global index on equal keys (A7)
-            } else {
-                better = is_max ? (q.key[s] > r.key[s]) : (q.key[s] < r.key[s]);
-            }
-            if (better) {
-                r.idx[s] = q.idx[s];
-                r.key[s] = q.key[s];
-                r.pt[s] = q.pt[s];
-            }
-        }
-    }
+    cudapre_extremes_t r = parts[0];   // (padding and unused slots as part 0)
+    geom::merge_header(parts, count, r);
+    for (int s = 0; s < 4 * r.nang; ++s) geom::merge_slot(parts, count, s, r);
     *out = r;
 }
 

@@ -158,10 +158,11 @@ int orient_exact(float ax, float ay, float bx, float by, float cx, float cy);
 // Step 2 from global extremes (geom.cuh): the polygon (poly) and, if g is
 // not null, the Step-3 geometry.  Sequential host build.
 void build_polygon(const cudapre_extremes_t& ext, cudapre_polygon_t* poly, K2Geom* g);
-// The same on the device: one block reads *d_ext and writes *d_poly, *d_g
-// (byte-identical to the host build).
-int launch_build_geom(const cudapre_extremes_t* d_ext, cudapre_polygon_t* d_poly, K2Geom* d_g, void* stream,
-                      int* launches);
+// The same on the device: one block reads d_parts[0..nparts) (merged first
+// if nparts > 1, the merge written to *d_merged if not null) and writes
+// *d_poly, *d_g (byte-identical to the host build).
+int launch_build_geom(const cudapre_extremes_t* d_parts, int nparts, cudapre_extremes_t* d_merged,
+                      cudapre_polygon_t* d_poly, K2Geom* d_g, void* stream, int* launches);
 // Canonical monotone-chain ring of pts[ids[j]] (ids nullptr = identity).
 int64_t hull_ring(const cudapre_pt* pts, const int64_t* ids, int64_t n, int64_t* ring);
 void merge_extremes(const cudapre_extremes_t* parts, int count, cudapre_extremes_t* out);

@@ -24,7 +24,10 @@ constexpr int kGeomThreads = 256;
 #endif
 #define GT(i) do { if (CUDAPRE_GEOM_TIMING && tid == 0) tmark[i] = clock64(); } while (0)
 
-__global__ void __launch_bounds__(kGeomThreads) k_build_geom(const cudapre_extremes_t* __restrict__ d_ext,
+// d_parts[0..nparts): per-shard Step-1 results (nparts > 1: merged here, slot
+// by slot, and the merged result written to *d_merged if not null).
+__global__ void __launch_bounds__(kGeomThreads) k_build_geom(const cudapre_extremes_t* d_parts, int nparts,
+                                                             cudapre_extremes_t* d_merged,
                                                              cudapre_polygon_t* __restrict__ poly,
                                                              K2Geom* __restrict__ g) {
     using namespace geom;
@@ -38,11 +41,19 @@ __global__ void __launch_bounds__(kGeomThreads) k_build_geom(const cudapre_extre
     const int tid = threadIdx.x;
     long long tmark[11] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
     GT(0);
-    {   // stage the Step-1 result (one coalesced load per thread)
+    {   // stage the Step-1 result (one coalesced load per thread) ...
         static_assert(sizeof(cudapre_extremes_t) % 4 == 0 && sizeof(cudapre_extremes_t) / 4 <= kGeomThreads, "ext");
-        const unsigned* src = reinterpret_cast<const unsigned*>(d_ext);
-        if (tid < (int)(sizeof(cudapre_extremes_t) / 4)) reinterpret_cast<unsigned*>(&ext)[tid] = src[tid];
+        constexpr int kWords = (int)(sizeof(cudapre_extremes_t) / 4);
+        const unsigned* src = reinterpret_cast<const unsigned*>(d_parts);
+        if (tid < kWords) reinterpret_cast<unsigned*>(&ext)[tid] = src[tid];
         __syncthreads();
+        if (nparts > 1) {   // ... or the merge of the shards' results
+            if (tid == 0) merge_header(d_parts, nparts, ext);
+            if (tid < 4 * ext.nang) merge_slot(d_parts, nparts, tid, ext);
+            __syncthreads();
+            if (d_merged && tid < kWords)
+                reinterpret_cast<unsigned*>(d_merged)[tid] = reinterpret_cast<const unsigned*>(&ext)[tid];
+        }
     }
     GT(8);
 
@@ -154,9 +165,9 @@ __global__ void __launch_bounds__(kGeomThreads) k_build_geom(const cudapre_extre
 
 }  // namespace
 
-int launch_build_geom(const cudapre_extremes_t* d_ext, cudapre_polygon_t* d_poly, K2Geom* d_g, void* stream,
-                      int* launches) {
-    k_build_geom<<<1, kGeomThreads, 0, (cudaStream_t)stream>>>(d_ext, d_poly, d_g);
+int launch_build_geom(const cudapre_extremes_t* d_parts, int nparts, cudapre_extremes_t* d_merged,
+                      cudapre_polygon_t* d_poly, K2Geom* d_g, void* stream, int* launches) {
+    k_build_geom<<<1, kGeomThreads, 0, (cudaStream_t)stream>>>(d_parts, nparts, d_merged, d_poly, d_g);
     ++*launches;
     return (int)cudaGetLastError();
 }

@@ -27,6 +27,18 @@ def main():
     idx, sp, rep = cp.cuda_pre(pts, "A", group=dist.group.WORLD, index_base=base)
     counts = [None] * world
     dist.all_gather_object(counts, idx.cpu().numpy())
+    # device-resident path: K1 -> NCCL all-gather of the workspace's Step-1
+    # blocks -> merge + Step 2 on the device -> K2, no host round trip
+    ws = cp.Workspace(n_local)
+    gathered = torch.empty(world * cp.EXTREMES_BYTES, dtype=torch.uint8, device="cuda")
+    cp.extremes_device(pts, "A", index_base=base, ws=ws)
+    dist.all_gather_into_tensor(gathered, cp.result_view(ws), group=dist.group.WORLD)
+    cp.polygon_device(ws, parts=gathered, nparts=world)
+    d_idx = torch.empty(n_local, dtype=torch.int64, device="cuda")
+    d_count = torch.zeros(1, dtype=torch.int64, device="cuda")
+    cp.filter_geom(pts, index_base=base, ws=ws, out_idx=d_idx, count=d_count)
+    torch.cuda.synchronize()
+    assert np.array_equal(d_idx[: int(d_count.item())].cpu().numpy(), idx.cpu().numpy()), "device path"
     if rank == 0:
         got = np.concatenate(counts)
         full = synth.generate("disk", N, seed=6)

@@ -109,3 +109,40 @@ def test_device_path_degenerate_and_misaligned():
     torch.cuda.synchronize()
     want = oracle.cudapre(xy[1:], "A", threads=THREADS)["survivors"]
     assert np.array_equal(out_idx[: int(count.item())].cpu().numpy() - 1, want)
+
+
+@pytest.mark.parametrize("k", [2, 3, 8])
+def test_device_merge_of_shards(k):
+    """The device builder's merge of k per-shard Step-1 blocks (what an NCCL
+    all-gather delivers) equals cudapre_extremes_merge + the host polygon,
+    byte for byte, and the sharded device pipeline returns the oracle's
+    survivors (ties across shard borders included)."""
+    xy = np.round(synth.generate("disk", 400_003, seed=17) * 64).astype(np.float32)   # heavy ties
+    n = len(xy)
+    bounds = [n * r // k for r in range(k + 1)]
+    gathered = torch.empty(k * cp.EXTREMES_BYTES, dtype=torch.uint8, device="cuda")
+    parts, shards = [], []
+    for r in range(k):
+        lo, hi = bounds[r], bounds[r + 1]
+        pts = torch.from_numpy(np.ascontiguousarray(xy[lo:hi])).cuda()
+        ws = cp.Workspace(hi - lo)
+        ext = cp.extremes(pts, "A", index_base=lo, ws=ws)      # host copy for the reference merge
+        gathered[r * cp.EXTREMES_BYTES:(r + 1) * cp.EXTREMES_BYTES].copy_(cp.result_view(ws))
+        parts.append(ext.raw)
+        shards.append((pts, ws, lo))
+    merged = cp.merge(parts)
+    want = oracle.cudapre(xy, "A", threads=THREADS)["survivors"]
+    got = []
+    for pts, ws, lo in shards:
+        cp.polygon_device(ws, parts=gathered, nparts=k)
+        out_idx = torch.empty(pts.shape[0], dtype=torch.int64, device="cuda")
+        count = torch.zeros(1, dtype=torch.int64, device="cuda")
+        cp.filter_geom(pts, index_base=lo, ws=ws, out_idx=out_idx, count=count)
+        torch.cuda.synchronize()
+        host_geom = cp.geometry(merged)
+        dev_geom, dev_poly = _device_pages(ws, len(host_geom))
+        assert dev_geom == host_geom
+        assert dev_poly == bytes(cp.polygon(merged).raw)
+        assert bytes(cp.result_view(ws).cpu().numpy().tobytes()) == bytes(merged.raw)
+        got.append(out_idx[: int(count.item())].cpu().numpy())
+    assert np.array_equal(np.concatenate(got), want)
