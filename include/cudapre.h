@@ -318,6 +318,30 @@ cudapre_status cudapre_graph_create(const cudapre_pt* d_pts, int64_t n_local, in
 cudapre_status cudapre_graph_launch(cudapre_graph_t* g, void* stream);
 cudapre_status cudapre_graph_destroy(cudapre_graph_t* g);
 
+/* ---------------------------------------------------------------- final hull on the GPU
+ * SURVEY §8 f1 (the paper runs Qhull on the survivors).
+ * The canonical ring of the survivors (identical to cudapre_hull on them)
+ * from device buffers:
+ *   d_pts, d_ids, m   the survivors: points and their global ids (e.g. the
+ *                     outputs of cudapre_filter / cudapre_filter_device)
+ *   h_poly            the Step-2 polygon they were filtered with (its disk
+ *                     centre anchors the second filter)
+ *   d_scratch         >= cudapre_hull_device_bytes(m) bytes of device memory
+ *   h_ring            host int64[ring_capacity]: the ring's global ids, CCW
+ *                     from the lexicographically smallest vertex
+ *   h_remaining       (nullable) points left for the host chain (diagnostic)
+ * Two kernels filter the survivors again with an inner polygon P' of up to
+ * 4097 survivors (farthest point per pseudo-angle sector, exact hull) —
+ * discarding only points strictly inside P' (exact predicate) — and the
+ * host's monotone chain finishes on the rest.  Without a certified centre
+ * (degenerate polygon) the chain runs on every survivor.  Synchronises the
+ * stream.  CAPACITY if the ring exceeds ring_capacity.                   */
+size_t cudapre_hull_device_bytes(int64_t m);
+cudapre_status cudapre_hull_device(const cudapre_pt* d_pts, const int64_t* d_ids, int64_t m,
+                                   const cudapre_polygon_t* h_poly, void* d_scratch, size_t scratch_bytes,
+                                   void* stream, int64_t* h_ring, int64_t ring_capacity,
+                                   int64_t* h_ring_len, int64_t* h_remaining);
+
 #ifdef __cplusplus
 }
 #endif

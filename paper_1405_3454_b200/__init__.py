@@ -81,7 +81,8 @@ SYMBOLS = ["cudapre_version", "cudapre_last_error", "cudapre_angles_preset",
            "cudapre_extremes_merge", "cudapre_polygon", "cudapre_filter", "cudapre_hull",
            "cudapre_run_host", "cudapre_geometry", "cudapre_filter_device", "cudapre_pipeline_device",
            "cudapre_graph_create", "cudapre_graph_launch", "cudapre_graph_destroy",
-           "cudapre_polygon_device", "cudapre_filter_geom"]
+           "cudapre_polygon_device", "cudapre_filter_geom", "cudapre_hull_device_bytes",
+           "cudapre_hull_device"]
 WS_GEOM_OFFSET = 4096            # include/cudapre.h CUDAPRE_WS_GEOM_OFFSET
 WS_POLY_OFFSET = 4096 + 16384    # CUDAPRE_WS_POLY_OFFSET
 WS_RESULT_OFFSET = 176           # CUDAPRE_WS_RESULT_OFFSET
@@ -121,8 +122,11 @@ def lib():
     L.cudapre_graph_destroy.argtypes = [vp]
     L.cudapre_polygon_device.argtypes = [vp, i32, vp, sz, vp, vp]
     L.cudapre_filter_geom.argtypes = [vp, i64, i64, vp, vp, i64, vp, sz, vp, vp]
+    L.cudapre_hull_device_bytes.argtypes = [i64]
+    L.cudapre_hull_device_bytes.restype = sz
+    L.cudapre_hull_device.argtypes = [vp, vp, i64, P(PolygonT), vp, sz, vp, vp, i64, P(i64), P(i64)]
     for name in SYMBOLS[2:]:
-        if name not in ("cudapre_workspace_bytes",):
+        if name not in ("cudapre_workspace_bytes", "cudapre_hull_device_bytes"):
             getattr(L, name).restype = ctypes.c_int
     _lib = L
     return L
@@ -527,6 +531,25 @@ class Graph:
             self.close()
         except Exception:
             pass
+
+
+def hull_device(pts, ids, m: int, poly, stream=None, return_remaining: bool = False):
+    """Final hull of the survivors pts[:m] (device float2) with
+    global ids ids[:m] (device int64), filtered with polygon `poly` (the
+    Polygon Step 2 returned): the canonical ring of global ids (numpy)."""
+    torch = _torch()
+    m = int(m)
+    nbytes = int(lib().cudapre_hull_device_bytes(m))
+    scratch = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=pts.device)
+    ring = np.empty(max(m, 1), np.int64)
+    n_ring, rem = ctypes.c_int64(), ctypes.c_int64()
+    raw = poly.raw if isinstance(poly, Polygon) else poly
+    _check(lib().cudapre_hull_device(
+        ctypes.c_void_p(pts.data_ptr()), ctypes.c_void_p(ids.data_ptr()), m, ctypes.byref(raw),
+        ctypes.c_void_p(scratch.data_ptr()), nbytes, _stream_ptr(stream),
+        ring.ctypes.data_as(ctypes.c_void_p), len(ring), ctypes.byref(n_ring), ctypes.byref(rem)))
+    out = ring[: n_ring.value].copy()
+    return (out, rem.value) if return_remaining else out
 
 
 def cuda_pre(pts, angles_="A", group=None, index_base: int = 0, return_points=True, ws=None):

@@ -8,6 +8,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "internal.h"
 
@@ -578,6 +579,145 @@ cudapre_status cudapre_graph_launch(cudapre_graph_t* g, void* stream) {
     g_err.clear();
     if (!g || !g->exec) return fail(CUDAPRE_ERR_INVALID_ARGUMENT, "graph is NULL");
     CUDA_TRY(cudaGraphLaunch(g->exec, (cudaStream_t)stream));
+    return CUDAPRE_OK;
+}
+
+// ------------------------------------------------------------------ final hull on the GPU (f1)
+namespace {
+struct HullScratch {
+    unsigned long long* gmax;
+    cudapre_pt* cand_pts;
+    int64_t* cand_ids;
+    unsigned* table;
+    float* vx;
+    float* vy;
+    unsigned long long* count;
+    cudapre_pt* out_pts;
+    int64_t* out_ids;
+    size_t bytes;
+};
+HullScratch hull_scratch(void* base, int64_t m) {
+    HullScratch h;
+    size_t off = 0;
+    auto take = [&](size_t n) {
+        const size_t o = off;
+        off = (off + n + 255) & ~(size_t)255;
+        return reinterpret_cast<char*>(base) + o;
+    };
+    h.gmax = reinterpret_cast<unsigned long long*>(take(sizeof(unsigned long long) * kHullBuckets));
+    h.cand_pts = reinterpret_cast<cudapre_pt*>(take(sizeof(cudapre_pt) * kHullBuckets));
+    h.cand_ids = reinterpret_cast<int64_t*>(take(sizeof(int64_t) * kHullBuckets));
+    h.table = reinterpret_cast<unsigned*>(take(sizeof(unsigned) * kHullBuckets));
+    h.vx = reinterpret_cast<float*>(take(sizeof(float) * (kHullMaxVerts + 1)));
+    h.vy = reinterpret_cast<float*>(take(sizeof(float) * (kHullMaxVerts + 1)));
+    h.count = reinterpret_cast<unsigned long long*>(take(sizeof(unsigned long long)));
+    h.out_pts = reinterpret_cast<cudapre_pt*>(take(sizeof(cudapre_pt) * (size_t)(m > 0 ? m : 1)));
+    h.out_ids = reinterpret_cast<int64_t*>(take(sizeof(int64_t) * (size_t)(m > 0 ? m : 1)));
+    h.bytes = off;
+    return h;
+}
+bool inside_ring(const cudapre_pt* v, int nv, float px, float py) {
+    if (nv < 3) return false;
+    for (int j = 0; j < nv; ++j) {
+        const cudapre_pt a = v[j], b = v[(j + 1) % nv];
+        if (orient_exact(a.x, a.y, b.x, b.y, px, py) <= 0) return false;
+    }
+    return true;
+}
+}  // namespace
+
+size_t cudapre_hull_device_bytes(int64_t m) { return hull_scratch(nullptr, m < 0 ? 0 : m).bytes; }
+
+cudapre_status cudapre_hull_device(const cudapre_pt* d_pts, const int64_t* d_ids, int64_t m,
+                                   const cudapre_polygon_t* h_poly, void* d_scratch, size_t scratch_bytes,
+                                   void* stream, int64_t* h_ring, int64_t ring_capacity, int64_t* h_ring_len,
+                                   int64_t* h_remaining) {
+    g_err.clear();
+    if (m < 0 || !h_ring_len || (m > 0 && (!d_pts || !d_ids || !h_poly || !d_scratch)))
+        return fail(CUDAPRE_ERR_INVALID_ARGUMENT, "bad hull_device arguments");
+    if (m > (int64_t)0xffffffffll) return fail(CUDAPRE_ERR_INVALID_ARGUMENT, "m out of range");
+    *h_ring_len = 0;
+    if (h_remaining) *h_remaining = m;
+    if (m == 0) return CUDAPRE_OK;
+    const HullScratch S = hull_scratch(d_scratch, m);
+    if (scratch_bytes < S.bytes)
+        return fail(CUDAPRE_ERR_WORKSPACE, "scratch %zu B < %zu B needed", scratch_bytes, S.bytes);
+    cudaStream_t strm = (cudaStream_t)stream;
+    std::vector<cudapre_pt> keep_pts;
+    std::vector<int64_t> keep_ids;
+    const float cx = h_poly->circle[0], cy = h_poly->circle[1];
+    bool filtered = false;
+    if (!h_poly->degenerate && inside_ring(h_poly->v, h_poly->nv, cx, cy)) {
+        // H1: sector maxima around c -> candidates
+        int launches = 0;
+        CUDA_TRY(cudaMemsetAsync(S.gmax, 0, sizeof(unsigned long long) * kHullBuckets, strm));
+        CUDA_TRY(launch_hull_votes(d_pts, d_ids, m, cx, cy, S.gmax, S.cand_pts, S.cand_ids, stream, &launches));
+        std::vector<cudapre_pt> cp_((size_t)kHullBuckets + CUDAPRE_MAX_SLOTS);
+        std::vector<int64_t> ci((size_t)kHullBuckets + CUDAPRE_MAX_SLOTS);
+        CUDA_TRY(cudaMemcpyAsync(cp_.data(), S.cand_pts, sizeof(cudapre_pt) * kHullBuckets, cudaMemcpyDeviceToHost,
+                                 strm));
+        CUDA_TRY(cudaMemcpyAsync(ci.data(), S.cand_ids, sizeof(int64_t) * kHullBuckets, cudaMemcpyDeviceToHost,
+                                 strm));
+        CUDA_TRY(cudaStreamSynchronize(strm));
+        int64_t nc = 0;
+        for (int b = 0; b < kHullBuckets; ++b)
+            if (ci[b] >= 0) {
+                cp_[nc] = cp_[b];
+                ci[nc++] = ci[b];
+            }
+        for (int j = 0; j < h_poly->nv; ++j) {   // the Step-2 ring (survivors too): P' contains c
+            cp_[nc] = h_poly->v[j];
+            ci[nc++] = h_poly->vidx[j];
+        }
+        std::vector<int64_t> rid((size_t)nc);
+        std::vector<cudapre_pt> rpt((size_t)nc + 1);
+        const int nv = (int)hull_ring_points(cp_.data(), ci.data(), nc, rid.data(), rpt.data());
+        if (nv >= 3 && nv <= kHullMaxVerts && inside_ring(rpt.data(), nv, cx, cy)) {
+            // H2: drop the survivors strictly inside P'
+            std::vector<unsigned> table((size_t)kHullBuckets);
+            hull_bucket_table(rpt.data(), nv, cx, cy, table.data());
+            std::vector<float> vx((size_t)nv + 1), vy((size_t)nv + 1);
+            for (int j = 0; j <= nv; ++j) {
+                vx[j] = rpt[j % nv].x;
+                vy[j] = rpt[j % nv].y;
+            }
+            CUDA_TRY(cudaMemcpyAsync(S.table, table.data(), sizeof(unsigned) * kHullBuckets,
+                                     cudaMemcpyHostToDevice, strm));
+            CUDA_TRY(cudaMemcpyAsync(S.vx, vx.data(), sizeof(float) * (nv + 1), cudaMemcpyHostToDevice, strm));
+            CUDA_TRY(cudaMemcpyAsync(S.vy, vy.data(), sizeof(float) * (nv + 1), cudaMemcpyHostToDevice, strm));
+            CUDA_TRY(cudaMemsetAsync(S.count, 0, sizeof(unsigned long long), strm));
+            CUDA_TRY(launch_hull_filter(d_pts, d_ids, m, cx, cy, S.table, S.vx, S.vy, nv, S.out_pts, S.out_ids,
+                                        S.count, stream, &launches));
+            unsigned long long k = 0;
+            CUDA_TRY(cudaMemcpyAsync(&k, S.count, sizeof(k), cudaMemcpyDeviceToHost, strm));
+            CUDA_TRY(cudaStreamSynchronize(strm));
+            keep_pts.resize((size_t)k);
+            keep_ids.resize((size_t)k);
+            if (k) {
+                CUDA_TRY(cudaMemcpyAsync(keep_pts.data(), S.out_pts, sizeof(cudapre_pt) * k, cudaMemcpyDeviceToHost,
+                                         strm));
+                CUDA_TRY(cudaMemcpyAsync(keep_ids.data(), S.out_ids, sizeof(int64_t) * k, cudaMemcpyDeviceToHost,
+                                         strm));
+                CUDA_TRY(cudaStreamSynchronize(strm));
+            }
+            filtered = true;
+        }
+    }
+    if (!filtered) {   // no certified centre: the host chain on every survivor
+        keep_pts.resize((size_t)m);
+        keep_ids.resize((size_t)m);
+        CUDA_TRY(cudaMemcpyAsync(keep_pts.data(), d_pts, sizeof(cudapre_pt) * m, cudaMemcpyDeviceToHost, strm));
+        CUDA_TRY(cudaMemcpyAsync(keep_ids.data(), d_ids, sizeof(int64_t) * m, cudaMemcpyDeviceToHost, strm));
+        CUDA_TRY(cudaStreamSynchronize(strm));
+    }
+    if (h_remaining) *h_remaining = (int64_t)keep_ids.size();
+    std::vector<int64_t> ring(keep_ids.size() + 1);
+    const int64_t len =
+        keep_ids.empty() ? 0 : hull_ring_points(keep_pts.data(), keep_ids.data(), (int64_t)keep_ids.size(),
+                                                ring.data(), nullptr);
+    if (len > ring_capacity) return fail(CUDAPRE_ERR_CAPACITY, "hull of %lld vertices > capacity", (long long)len);
+    if (len > 0) std::memcpy(h_ring, ring.data(), sizeof(int64_t) * len);
+    *h_ring_len = len;
     return CUDAPRE_OK;
 }
 

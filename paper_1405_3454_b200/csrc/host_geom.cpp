@@ -79,6 +79,56 @@ int64_t hull_ring(const cudapre_pt* pts, const int64_t* ids, int64_t n, int64_t*
     return chain(P, ring);
 }
 
+int64_t hull_ring_points(const cudapre_pt* pts, const int64_t* ids, int64_t n, int64_t* ring_ids,
+                         cudapre_pt* ring_pts) {
+    std::vector<CP> P((size_t)n);
+    for (int64_t j = 0; j < n; ++j) P[j] = CP{pts[j].x, pts[j].y, ids[j]};
+    const int64_t k = chain(P, ring_ids);
+    if (ring_pts) {   // chain() sorted P; look the ring ids up by binary search over ids
+        std::vector<CP> byid(P);
+        std::sort(byid.begin(), byid.end(), [](const CP& a, const CP& b) { return a.id < b.id; });
+        for (int64_t j = 0; j < k; ++j) {
+            const auto it = std::lower_bound(byid.begin(), byid.end(), ring_ids[j],
+                                             [](const CP& a, int64_t id) { return a.id < id; });
+            ring_pts[j] = cudapre_pt{it->x, it->y};
+        }
+    }
+    return k;
+}
+
+void hull_bucket_table(const cudapre_pt* v, int nv, float cx, float cy, unsigned* table) {
+    // exit edge of the ray of pseudo-angle pa around c: the first edge counted
+    // from cs (first max of the vertex pseudo-angles) whose closed range holds
+    // pa (geom.cuh phase F); candidates of bucket b: exit edge of its lower
+    // guarded boundary ray to that of its upper one (a rounding slip near a
+    // vertex only widens the range; points of the bucket lie >= 2^-16 in pa
+    // from the boundary rays)
+    std::vector<double> pv((size_t)nv), U((size_t)nv);
+    for (int j = 0; j < nv; ++j) pv[j] = geom::pa_of((double)v[j].x - cx, (double)v[j].y - cy);
+    int cs = 0;
+    for (int j = 0; j < nv; ++j)
+        if (pv[j] > pv[cs]) cs = j;
+    for (int k = 0; k < nv; ++k) U[k] = pv[(cs + k + 1) % nv] + 4.0;
+    auto exit_edge = [&](double pa) {
+        if (pa < 0.0) pa += 4.0;
+        if (pa >= 4.0) pa -= 4.0;
+        const double q = pa < pv[cs] ? pa + 4.0 : pa;
+        int lo = 0, hi = nv - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (q <= U[mid]) hi = mid;
+            else lo = mid + 1;
+        }
+        return (cs + lo) % nv;
+    };
+    const double g = geom::kGuard;
+    for (int b = 0; b < kHullBuckets; ++b) {
+        const int e0 = exit_edge((b - 0.5 - g) / 1024.0), e1 = exit_edge((b + 0.5 + g) / 1024.0);
+        const int cnt = (e1 - e0 + nv) % nv + 1;
+        table[b] = (unsigned)e0 | ((unsigned)cnt << 16);
+    }
+}
+
 void merge_extremes(const cudapre_extremes_t* parts, int count, cudapre_extremes_t* out) {
     cudapre_extremes_t r = parts[0];   // (padding and unused slots as part 0)
     geom::merge_header(parts, count, r);

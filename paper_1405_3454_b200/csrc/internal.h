@@ -153,6 +153,24 @@ int launch_filter(const K2Params& p, int vec16, void* stream, int* launches);
 int launch_filter_tma(const K2Params& p, void* stream, int* launches);   // vec16, mode 0
 int k2_use_tma();   // CUDAPRE_K2_TMA (default 1)
 
+// ---------------------------------------------------------------- final hull on the GPU (k_hull.cu, f1)
+constexpr int kHullBuckets = 4097;   // b = round(1024 pa), pa in [0, 4]
+constexpr int kHullMaxVerts = kHullBuckets + CUDAPRE_MAX_SLOTS;
+int launch_hull_votes(const cudapre_pt* d_pts, const int64_t* d_ids, int64_t m, float cx, float cy,
+                      unsigned long long* gmax, cudapre_pt* cand_pts, int64_t* cand_ids, void* stream,
+                      int* launches);
+int launch_hull_filter(const cudapre_pt* d_pts, const int64_t* d_ids, int64_t m, float cx, float cy,
+                       const unsigned* table, const float* vx, const float* vy, int nv, cudapre_pt* out_pts,
+                       int64_t* out_ids, unsigned long long* count, void* stream, int* launches);
+// Canonical ring (monotone chain) of the points (pts[j], ids[j]), ids
+// distinct: ring ids (and coordinates if ring_pts), CCW from the
+// lexicographically smallest vertex; returns its length.
+int64_t hull_ring_points(const cudapre_pt* pts, const int64_t* ids, int64_t n, int64_t* ring_ids,
+                         cudapre_pt* ring_pts);
+// Candidate-edge table of ring v[0..nv) around c for the hull filter
+// (kHullBuckets entries: first edge | count << 16, count 0 = all edges).
+void hull_bucket_table(const cudapre_pt* v, int nv, float cx, float cy, unsigned* table);
+
 // ---------------------------------------------------------------- host geometry (host_geom.cpp)
 int orient_exact(float ax, float ay, float bx, float by, float cx, float cy);
 // Step 2 from global extremes (geom.cuh): the polygon (poly) and, if g is
