@@ -13,11 +13,12 @@
 //    takes the next super-tile's ticket early (the atomic's latency overlaps
 //    the first sub-tiles).
 //  * Ownership: warp w owns the contiguous 256 points [256w, 256w+256) of each
-//    2048-point sub-tile, lane l the pairs u*32+l (u = 0..3).  The groups of
-//    the ordered compaction are the 64 (sub-tile, warp) chunks, in index order.
+//    2048-point sub-tile, lane l the points r*32+l (round r = 0..7, one float2
+//    each).  The groups of the ordered compaction are the 64 (sub-tile, warp)
+//    chunks, in index order.
 //  * Pass A: one fast test per point (inner disk or inner box, whichever the
 //    host found larger; a warp-uniform switch).  Points it cannot decide are
-//    queued in INDEX order (one packed 4x8-bit warp scan), so the per-warp
+//    queued in INDEX order (one ballot per round), so the per-warp
 //    survivor list comes out sorted and a survivor's rank inside its group is
 //    its list position minus the group's start: no per-group ballots.
 //  * Queue pass: sector table (inner/outer radius of the bucket), then for
@@ -48,7 +49,7 @@ constexpr unsigned kBlock = kK2Threads + 64;         // 8 compute warps + produc
 constexpr unsigned kProdWarp = kW, kEmitWarp = kW + 1;
 constexpr int kBufs = kK2Bufs;                       // survivor-list buffers (tiles in flight)
 
-using SurvT = SurvEntry;   // meta = (sub << 8) | loc, loc = u*64 + lane*2 + h = point offset in the warp chunk
+using SurvT = SurvEntry;   // meta = (sub << 8) | loc, loc = r*32 + lane = point offset in the warp chunk
 static_assert(kK2Bufs == 3 && kK2WarpPts == kK2Sub * 2 * (int)(kK2SubPairs / (kK2Threads / 32)), "layout");
 
 template <unsigned kL>
@@ -372,64 +373,57 @@ __global__ void __launch_bounds__(kBlock, K2Cfg<CFG>::kMinB) k2_filter_tma(const
                 const unsigned np = bytes / 16u;   // full pairs of this sub-tile in memory
                 const float4* chunk = &S.ring[st][warp * kChunkPairs];
                 mbar_sleep_wait(a_full + 8u * st, (seq / kNst) & 1u);
-                unsigned needy = 0u;   // bit 2u + h: not decided by the fast test
+                // warp-chunk points loc = r*32 + lane (round r = 0..7): one float2
+                // per lane per round, so the index order inside the chunk is
+                // (round, lane) and one ballot per round orders the queue
+                const float2* chunk2 = reinterpret_cast<const float2*>(chunk);
+                unsigned needy = 0u;   // bit r: point r*32 + lane not decided by the fast test
                 if (np == (unsigned)kK2SubPairs) {
                     if (p.debug == 1) {   // perf experiment only: skeleton, no classification
 #pragma unroll
-                        for (int u = 0; u < kK2Items; ++u)
-                            needy |= (chunk[u * 32 + lane].x == 12345.0f ? 1u : 0u) << (2 * u);
+                        for (int r = 0; r < 8; ++r) needy |= (chunk2[r * 32 + lane].x == 12345.0f ? 1u : 0u) << r;
                     } else if (fast == 0) {
 #pragma unroll
-                        for (int u = 0; u < kK2Items; ++u) {
-                            const float4 v = chunk[u * 32 + lane];
-                            const unsigned in = (in_disk(gox, goy, gr2, v.x, v.y) ? 1u : 0u) |
-                                                (in_disk(gox, goy, gr2, v.z, v.w) ? 2u : 0u);
-                            needy |= (3u & ~in) << (2 * u);
+                        for (int r = 0; r < 8; ++r) {
+                            const float2 v = chunk2[r * 32 + lane];
+                            needy |= (in_disk(gox, goy, gr2, v.x, v.y) ? 0u : 1u) << r;
                         }
                     } else if (fast == 1) {
 #pragma unroll
-                        for (int u = 0; u < kK2Items; ++u) {
-                            const float4 v = chunk[u * 32 + lane];
-                            const unsigned in = (in_box(gbx0, gbx1, gby0, gby1, v.x, v.y) ? 1u : 0u) |
-                                                (in_box(gbx0, gbx1, gby0, gby1, v.z, v.w) ? 2u : 0u);
-                            needy |= (3u & ~in) << (2 * u);
+                        for (int r = 0; r < 8; ++r) {
+                            const float2 v = chunk2[r * 32 + lane];
+                            needy |= (in_box(gbx0, gbx1, gby0, gby1, v.x, v.y) ? 0u : 1u) << r;
                         }
                     } else {   // no fast test (degenerate / exact-only rings): queue everything
                         needy = 0xffu;
                     }
                 } else {   // last super-tile only: ragged end (+ the unpaired last point)
-                    const unsigned qs = tile * kK2TilePairs + sub * kK2SubPairs;
+                    const unsigned qs = tile * kK2TilePairs + sub * kK2SubPairs;   // first pair of the sub-tile
 #pragma unroll
-                    for (int u = 0; u < kK2Items; ++u) {
-                        const unsigned pr = warp * kChunkPairs + u * 32 + lane;
-                        unsigned valid = 0u;
-                        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-                        if (pr < np) {
-                            v = S.ring[st][pr];
-                            valid = 3u;
-                        } else if (odd && qs + pr == full_pairs) {
-                            const float2 a = __ldg(reinterpret_cast<const float2*>(p.pts) + 2u * full_pairs);
-                            v = make_float4(a.x, a.y, 0.f, 0.f);
-                            valid = 1u;
+                    for (int r = 0; r < 8; ++r) {
+                        const unsigned pt = warp * (2u * kChunkPairs) + r * 32 + lane;   // point in the sub-tile
+                        bool valid = false;
+                        float2 v = make_float2(0.f, 0.f);
+                        if (pt < 2u * np) {
+                            v = chunk2[r * 32 + lane];
+                            valid = true;
+                        } else if (odd && 2u * qs + pt == 2u * full_pairs) {
+                            v = __ldg(reinterpret_cast<const float2*>(p.pts) + 2u * full_pairs);
+                            valid = true;
                         }
-                        const unsigned in = (fast_inside(S.geo, v.x, v.y) ? 1u : 0u) | (fast_inside(S.geo, v.z, v.w) ? 2u : 0u);
-                        needy |= (valid & ~in) << (2 * u);
+                        needy |= (valid && !fast_inside(S.geo, v.x, v.y) ? 1u : 0u) << r;
                     }
                 }
-                // ---- index-ordered queue: slot of (u, lane, h) = (needy points of
-                //      pairs u' < u in the whole chunk) + (needy points of pair u in
-                //      lanes < lane) + (h ? bit(u, 0) : 0), from 8 independent ballots
-                //      (a few dependent levels instead of a shuffle scan + a loop)
+                // ---- index-ordered queue: slot of (r, lane) = (needy points of
+                //      rounds < r) + (needy points of round r in lanes < lane)
                 if (lane == 0) cur.lstart[warp][sub] = wc;
                 unsigned qtotal = 0;
 #pragma unroll
-                for (int u = 0; u < kK2Items; ++u) {
-                    const unsigned n0 = (needy >> (2 * u)) & 1u, n1 = (needy >> (2 * u + 1)) & 1u;
-                    const unsigned b0 = __ballot_sync(kFull, n0), b1 = __ballot_sync(kFull, n1);
-                    const unsigned slot = qtotal + __popc(b0 & lt) + __popc(b1 & lt);
-                    if (n0) S.qslot[warp][slot] = (unsigned char)((u << 6) | (lane << 1));
-                    if (n1) S.qslot[warp][slot + n0] = (unsigned char)((u << 6) | (lane << 1) | 1u);
-                    qtotal += __popc(b0) + __popc(b1);
+                for (int r = 0; r < 8; ++r) {
+                    const unsigned nb = (needy >> r) & 1u;
+                    const unsigned b = __ballot_sync(kFull, nb);
+                    if (nb) S.qslot[warp][qtotal + __popc(b & lt)] = (unsigned char)((r << 5) | lane);
+                    qtotal += __popc(b);
                 }
                 if (qtotal) {
                     __syncwarp();
@@ -440,9 +434,9 @@ __global__ void __launch_bounds__(kBlock, K2Cfg<CFG>::kMinB) k2_filter_tma(const
                         unsigned loc = 0;
                         if (e < qtotal) {
                             loc = S.qslot[warp][e];
-                            const unsigned pr = warp * kChunkPairs + (loc >> 1);
-                            if (pr < np) {
-                                q = reinterpret_cast<const float2*>(&S.ring[st][0])[2u * pr + (loc & 1u)];
+                            const unsigned pt = warp * (2u * kChunkPairs) + loc;   // point in the sub-tile
+                            if (pt < 2u * np) {
+                                q = reinterpret_cast<const float2*>(&S.ring[st][0])[pt];
                             } else {   // the unpaired last point
                                 q = __ldg(reinterpret_cast<const float2*>(p.pts) + 2u * full_pairs);
                             }
