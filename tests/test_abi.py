@@ -382,3 +382,62 @@ def test_k2_sector_table_is_conservative(L, oracle_lib, family):
     assert out.sum() > 1000
     for p in pts[out][:1500]:
         assert not brute.strictly_inside_frac(V, p), (family, p)
+
+
+@pytest.mark.parametrize("family", ["disk", "square", "gauss", "circle"])
+@pytest.mark.parametrize("angles", ["A", "D"])
+def test_k2_candidate_edges_hold_the_exit_edge(L, oracle_lib, family, angles):
+    """for every bucket a probe's ray can land in (its exact
+    pseudo-angle bucket +- the kernel's error, < 2^-12 bucket), the bucket's
+    candidate-edge range (sedge) holds the edge the ray from the centre exits
+    through — decided exactly with rationals on the probe's float coordinates
+    (a ray through a vertex may use either adjacent edge)."""
+    from fractions import Fraction as Fr
+
+    xy = synth.generate(family, 50_000, seed=31)
+    ext = cp.Extremes(_ext_from_oracle(oracle_lib, xy, angles))
+    g = cp.geometry(ext)
+    nv = int(np.frombuffer(g[:4], np.int32)[0])
+    ox, oy = np.frombuffer(g[32:40], np.float32)
+    vx = np.frombuffer(g[432:432 + 132], np.float32)[:nv]
+    vy = np.frombuffer(g[564:564 + 132], np.float32)[:nv]
+    sedge = np.frombuffer(g[8896:8896 + 2 * 1025], np.uint16)
+    assert nv >= 3 and (sedge != 0xFFFF).mean() > 0.9
+    c = (Fr(float(ox)), Fr(float(oy)))
+    V = [(Fr(float(a)), Fr(float(b))) for a, b in zip(vx, vy)]
+
+    def cross(ax, ay, bx, by):
+        return ax * by - ay * bx
+
+    rng = np.random.default_rng(3)
+    pa = rng.uniform(0, 4, 1500)
+    t = np.where(pa <= 2, pa - 1, 3 - pa)
+    u = np.stack([np.where(pa <= 2, 1 - np.abs(t), -(1 - np.abs(t))), t], 1)
+    pts = (np.array([ox, oy], np.float64) + rng.uniform(0.5, 1.5, (len(pa), 1)) * u).astype(np.float32)
+    checked = 0
+    for p in pts:
+        dx, dy = Fr(float(p[0])) - c[0], Fr(float(p[1])) - c[1]
+        if dx == 0 and dy == 0:
+            continue
+        # exit edges: j with the direction in the closed wedge (v_j - c, v_j+1 - c)
+        exits = set()
+        for j in range(nv):
+            k = (j + 1) % nv
+            s0 = cross(V[j][0] - c[0], V[j][1] - c[1], dx, dy)
+            s1 = cross(V[k][0] - c[0], V[k][1] - c[1], dx, dy)
+            if s0 >= 0 and s1 <= 0:
+                exits.add(j)
+        assert exits
+        pe = float(dy / (abs(dx) + abs(dy)))
+        pe = pe + 1 if dx >= 0 else 3 - pe
+        for b in range(int(np.floor(256 * pe - 0.5 - 2 ** -10)), int(np.ceil(256 * pe + 0.5 + 2 ** -10)) + 1):
+            if abs(b - 256 * pe) > 0.5 + 2 ** -10:
+                continue
+            for bb in {b % 1024, b % 1024 + (1024 if b % 1024 == 0 else 0)}:
+                if bb > 1024 or sedge[bb] == 0xFFFF:
+                    continue
+                lo, hi = int(sedge[bb]) & 0xFF, int(sedge[bb]) >> 8
+                rng_edges = {(lo + i) % nv for i in range((hi - lo) % nv + 1)}
+                assert exits & rng_edges, (family, angles, bb, lo, hi, exits)
+                checked += 1
+    assert checked > 1000
