@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--angles", default="A")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-points", action="store_true",
+                    help="write only the survivors' indices (perf experiment; not the benchmark workload)")
     ap.add_argument("--host-step2", action="store_true",
                     help="run Step 2 (and, N > 1, the merge) on the host between the kernels, as the paper")
     return ap.parse_args()
@@ -198,7 +200,7 @@ def main():
     ws = cp.Workspace(n_local)
     cap = n_local if n_local <= 250_000_000 else n_local // 8   # dense configs (C4) keep ~all points
     out_idx = torch.empty(cap, dtype=torch.int64, device="cuda")
-    out_pts = torch.empty((cap, 2), dtype=torch.float32, device="cuda")
+    out_pts = None if args.no_points else torch.empty((cap, 2), dtype=torch.float32, device="cuda")
     torch.cuda.synchronize()
 
     exact_pts = [0]

@@ -16,8 +16,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libcudapre.so")
 BUILD = os.path.join(HERE, "_build")
-SOURCES = ["api.cpp", "host_geom.cpp", "k1_extremes.cu", "k2_filter.cu", "k2_filter_tma.cu", "k_polygon.cu",
-           "k_hull.cu"]
+SOURCES = ["api.cpp", "host_geom.cpp", "k1_extremes.cu", "k2_filter.cu", "k2_filter_tma.cu", "k2_filter_tma10.cu",
+           "k_polygon.cu", "k_hull.cu"]
 # per-file extra flags: the device polygon builder must not contract multiply-adds (it has to agree
 # bit for bit with the host builder, compiled with -ffp-contract=off)
 EXTRA = {"k_polygon.cu": ["-fmad=false"]}

@@ -81,7 +81,8 @@ struct SurvEntry {
 };
 constexpr int kK2Bufs = 3;                          // survivor-list buffers per block
 constexpr int kK2WarpPts = kK2Sub * 256;            // 2048 points per warp per super-tile
-constexpr size_t kK2ScratchPerBlock = (size_t)kK2Bufs * 8 * kK2WarpPts * sizeof(SurvEntry);
+constexpr int kK2MaxWarps = 10;                    // compute warps per TMA K2 block, at most
+constexpr size_t kK2ScratchPerBlock = (size_t)kK2Bufs * kK2MaxWarps * kK2WarpPts * sizeof(SurvEntry);
 constexpr int kK2BlocksPerSM = 2;
 int device_sm_count();
 inline size_t ws_scratch_blocks(int64_t n) {
@@ -150,7 +151,9 @@ struct K2Params {
 // All return a cudaError_t as int (0 = success).
 int launch_extremes(const K1Params& p, int vec16, void* stream, int* launches);
 int launch_filter(const K2Params& p, int vec16, void* stream, int* launches);
-int launch_filter_tma(const K2Params& p, void* stream, int* launches);   // vec16, mode 0
+int launch_filter_tma(const K2Params& p, void* stream, int* launches);     // vec16: 8 compute warps
+int launch_filter_tma10(const K2Params& p, void* stream, int* launches);   // vec16: 10 compute warps
+int k2_warps();   // CUDAPRE_K2_WARPS (8 or 10)
 int k2_use_tma();   // CUDAPRE_K2_TMA (default 1)
 
 // ---------------------------------------------------------------- final hull on the GPU (k_hull.cu, f1)

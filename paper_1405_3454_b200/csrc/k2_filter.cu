@@ -371,8 +371,18 @@ int k2_use_tma() {
     return v;
 }
 
+int k2_warps() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("CUDAPRE_K2_WARPS");
+        v = (e && atoi(e) == 10) ? 10 : 8;
+    }
+    return v;
+}
+
 int launch_filter(const K2Params& p, int vec16, void* stream, int* launches) {
-    if (vec16 && k2_use_tma()) return launch_filter_tma(p, stream, launches);   // (handles every mode)
+    if (vec16 && k2_use_tma())   // (handles every mode)
+        return k2_warps() == 10 ? launch_filter_tma10(p, stream, launches) : launch_filter_tma(p, stream, launches);
     cudaStream_t s = (cudaStream_t)stream;
     if (p.edges <= 16)
         return vec16 ? (int)launch_t<true, 16>(p, s, launches) : (int)launch_t<false, 16>(p, s, launches);

@@ -41,16 +41,26 @@
 namespace cudapre {
 namespace {
 
-constexpr int kW = kK2Threads / 32;                  // 8 warps
-constexpr int kGroups = kK2Sub * kW;                 // 64 groups (sub, warp) per super-tile
-constexpr unsigned kChunkPairs = kK2SubPairs / kW;   // 128 pairs = 256 points per warp chunk
+// K2_NW: compute warps per block (8 here; k2_filter_tma10.cu builds the same
+// source with 10).  A warp chunk is always 256 points; a sub-tile is NW
+// chunks, a super-tile 8 sub-tiles.
+#ifndef K2_NW
+#define K2_NW 8
+#define K2_ENTRY launch_filter_tma
+#endif
+constexpr int kW = K2_NW;
+constexpr int kGroups = kK2Sub * kW;                 // groups (sub, warp) per super-tile
+constexpr unsigned kChunkPairs = 128;                // 256 points per warp chunk
+constexpr unsigned kSubPairsT = kW * kChunkPairs;    // pairs per sub-tile (16 KiB at 8 warps)
+constexpr unsigned kTilePairsT = kK2Sub * kSubPairsT;
+constexpr int kGroupsPerLane = (kGroups + 31) / 32;
 constexpr unsigned kNone = 0xffffffffu;
-constexpr unsigned kBlock = kK2Threads + 64;         // 8 compute warps + producer warp + emit warp
+constexpr unsigned kBlock = kW * 32 + 64;            // compute warps + producer warp + emit warp
 constexpr unsigned kProdWarp = kW, kEmitWarp = kW + 1;
 constexpr int kBufs = kK2Bufs;                       // survivor-list buffers (tiles in flight)
 
 using SurvT = SurvEntry;   // meta = (sub << 8) | loc, loc = r*32 + lane = point offset in the warp chunk
-static_assert(kK2Bufs == 3 && kK2WarpPts == kK2Sub * 2 * (int)(kK2SubPairs / (kK2Threads / 32)), "layout");
+static_assert(kK2Bufs == 3 && kK2WarpPts == kK2Sub * 2 * (int)kChunkPairs && kW <= kK2MaxWarps, "layout");
 
 template <unsigned kL>
 struct TileT {
@@ -63,14 +73,14 @@ struct TileT {
 
 template <int kNst, unsigned kL>
 struct SmemT {
-    float4 ring[kNst][kK2SubPairs];
+    float4 ring[kNst][kSubPairsT];
     unsigned long long full[kNst];
     unsigned long long empty[kNst];
     TileT<kL> ts[kBufs];
     unsigned long long tile_done[kBufs];   // compute warps -> emit warp (count kW)
     unsigned long long buf_free[kBufs];    // emit warp -> compute warps (count 1)
     unsigned long long agg[kBufs];         // (compute warps done << 32) | survivors so far
-    unsigned char qslot[kW][2 * kK2Items * 32];
+    unsigned char qslot[kW][8 * 32];
     float2 sec[CUDAPRE_SECTORS + 1];               // {inner r^2, outer r^2} per bucket
     unsigned short sedge[CUDAPRE_SECTORS + 1];     // candidate exit edges per bucket
     float4 edge[CUDAPRE_MAX_SLOTS];                // {A, B, C', 0} (C' already lowered by E_j)
@@ -131,15 +141,15 @@ __device__ __forceinline__ bool in_disk(float ox, float oy, float r2, float x, f
 
 // bytes of full point pairs of sub-tile `sub` of super-tile `tile` in memory
 __device__ __forceinline__ unsigned sub_bytes(unsigned tile, unsigned sub, unsigned full_pairs) {
-    const unsigned qs = tile * kK2TilePairs + sub * kK2SubPairs;
+    const unsigned qs = tile * kTilePairsT + sub * kSubPairsT;
     if (qs >= full_pairs) return 0u;
     const unsigned np = full_pairs - qs;
-    return (np >= (unsigned)kK2SubPairs ? (unsigned)kK2SubPairs : np) * 16u;
+    return (np >= (unsigned)kSubPairsT ? (unsigned)kSubPairsT : np) * 16u;
 }
 
 // point index (relative to the super-tile) of chunk offset loc of (sub, warp)
 __device__ __forceinline__ unsigned chunk_point(unsigned sub, unsigned warp, unsigned loc) {
-    return sub * (2u * kK2SubPairs) + warp * (2u * kChunkPairs) + loc;
+    return sub * (2u * kSubPairsT) + warp * (2u * kChunkPairs) + loc;
 }
 
 // write the survivors of super-tile `tile` kept by warp `warp` from exclusive
@@ -149,7 +159,7 @@ __device__ __forceinline__ unsigned chunk_point(unsigned sub, unsigned warp, uns
 template <unsigned kL>
 __device__ __forceinline__ void emit_t(const K2Params& p, const TileT<kL>& ts, const SurvT* ovf, unsigned tile,
                                        unsigned long long ex, unsigned warp, unsigned lane) {
-    const unsigned long long tpt = (unsigned long long)tile * (2u * kK2TilePairs);
+    const unsigned long long tpt = (unsigned long long)tile * (2u * kTilePairsT);
     float2* out_pts = reinterpret_cast<float2*>(p.out_pts);
     const unsigned wc = ts.lstart[warp][kK2Sub];
     for (unsigned r = lane; r < wc; r += 32) {
@@ -175,7 +185,7 @@ __device__ __forceinline__ void emit_t(const K2Params& p, const TileT<kL>& ts, c
 // 2 blocks per SM); CFG 1: 3-stage ring, 128-entry lists.  Overflowing lists
 // spill to global scratch, so the list size only trades smem for traffic.
 template <int CFG> struct K2Cfg;
-template <> struct K2Cfg<0> { static constexpr int kNst = 4; static constexpr unsigned kL = 96; static constexpr int kMinB = 2; };
+template <> struct K2Cfg<0> { static constexpr int kNst = K2_NW == 10 ? 3 : 4; static constexpr unsigned kL = 96; static constexpr int kMinB = 2; };
 template <> struct K2Cfg<1> { static constexpr int kNst = 3; static constexpr unsigned kL = 128; static constexpr int kMinB = 2; };
 
 // DBG: perf-experiment build with per-warp cycle counters (CUDAPRE_K2_DEBUG=2)
@@ -240,7 +250,7 @@ __global__ void __launch_bounds__(kBlock, K2Cfg<CFG>::kMinB) k2_filter_tma(const
                     const unsigned bytes = valid ? sub_bytes(t, sub, full_pairs) : 0u;
                     if (bytes) {
                         mbar_expect_tx_a(a_full + 8u * st, bytes);
-                        bulk_g2s_a(a_ring + st * (16u * kK2SubPairs), src + (size_t)t * kK2TilePairs + sub * kK2SubPairs,
+                        bulk_g2s_a(a_ring + st * (16u * kSubPairsT), src + (size_t)t * kTilePairsT + sub * kSubPairsT,
                                    bytes, a_full + 8u * st);
                     } else {
                         mbar_arrive_a(a_full + 8u * st);
@@ -272,18 +282,31 @@ __global__ void __launch_bounds__(kBlock, K2Cfg<CFG>::kMinB) k2_filter_tma(const
             if (DBG) { const unsigned long long t = clock64(); dce[0] += t - te; te = t; }
             const unsigned tile = cur.tile;
             if (tile != kNone) {
-                const unsigned sub = lane >> 2, w0 = (2u * lane) & 7u;
-                const unsigned c0 = cur.lstart[w0][sub + 1] - cur.lstart[w0][sub];
-                const unsigned c1 = cur.lstart[w0 + 1][sub + 1] - cur.lstart[w0 + 1][sub];
-                unsigned inc = c0 + c1;
+                // lane l owns groups g = l*kGroupsPerLane + i (g = sub*kW + w, index order)
+                unsigned c[kGroupsPerLane], mine = 0;
+#pragma unroll
+                for (int i = 0; i < kGroupsPerLane; ++i) {
+                    const unsigned g = lane * kGroupsPerLane + i;
+                    c[i] = 0u;
+                    if (g < (unsigned)kGroups) {
+                        const unsigned sub = g / kW, w = g % kW;
+                        c[i] = cur.lstart[w][sub + 1] - cur.lstart[w][sub];
+                    }
+                    mine += c[i];
+                }
+                unsigned inc = mine;
 #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) {
                     const unsigned y = __shfl_up_sync(kFull, inc, o);
                     if (lane >= (unsigned)o) inc += y;
                 }
-                const unsigned ex0 = inc - c0 - c1;
-                cur.off[2 * lane] = ex0;
-                cur.off[2 * lane + 1] = ex0 + c0;
+                unsigned run = inc - mine;
+#pragma unroll
+                for (int i = 0; i < kGroupsPerLane; ++i) {
+                    const unsigned g = lane * kGroupsPerLane + i;
+                    if (g < (unsigned)kGroups) cur.off[g] = run;
+                    run += c[i];
+                }
                 const unsigned total = __shfl_sync(kFull, inc, 31);
                 if (lane == 0) {
                     cur.total = total;
@@ -378,7 +401,7 @@ __global__ void __launch_bounds__(kBlock, K2Cfg<CFG>::kMinB) k2_filter_tma(const
                 // (round, lane) and one ballot per round orders the queue
                 const float2* chunk2 = reinterpret_cast<const float2*>(chunk);
                 unsigned needy = 0u;   // bit r: point r*32 + lane not decided by the fast test
-                if (np == (unsigned)kK2SubPairs) {
+                if (np == (unsigned)kSubPairsT) {
                     if (p.debug == 1) {   // perf experiment only: skeleton, no classification
 #pragma unroll
                         for (int r = 0; r < 8; ++r) needy |= (chunk2[r * 32 + lane].x == 12345.0f ? 1u : 0u) << r;
@@ -398,7 +421,7 @@ __global__ void __launch_bounds__(kBlock, K2Cfg<CFG>::kMinB) k2_filter_tma(const
                         needy = 0xffu;
                     }
                 } else {   // last super-tile only: ragged end (+ the unpaired last point)
-                    const unsigned qs = tile * kK2TilePairs + sub * kK2SubPairs;   // first pair of the sub-tile
+                    const unsigned qs = tile * kTilePairsT + sub * kSubPairsT;   // first pair of the sub-tile
 #pragma unroll
                     for (int r = 0; r < 8; ++r) {
                         const unsigned pt = warp * (2u * kChunkPairs) + r * 32 + lane;   // point in the sub-tile
@@ -520,8 +543,10 @@ int k2_cfg() {
 
 }  // namespace
 
-int launch_filter_tma(const K2Params& p, void* stream, int* launches) {
+int K2_ENTRY(const K2Params& p_in, void* stream, int* launches) {
     cudaStream_t s = (cudaStream_t)stream;
+    K2Params p = p_in;   // this kernel's super-tiles: kTilePairsT pairs
+    p.num_tiles = (unsigned)((2ull * kTilePairsT - 1 + p.n) / (2ull * kTilePairsT));
     if (p.debug == 2)
         return p.edges <= 16 ? (int)launch_tma_t<16, 0, true>(p, s, launches) : (int)launch_tma_t<32, 0, true>(p, s, launches);
     if (k2_cfg() == 1)
