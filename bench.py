@@ -208,7 +208,8 @@ def main():
     def step(rep1):   # host Step 2 (and, N > 1, the cross-rank combine)
         ext = cp.extremes(pts, args.angles, index_base=base, group=group, ws=ws, report=rep1)
         exact_pts[0] = ext.raw.exact_points
-        idx, sp, rep2 = cp.filter(pts, ext, index_base=base, ws=ws, out_idx=out_idx, out_pts=out_pts)
+        idx, sp, rep2 = cp.filter(pts, ext, index_base=base, ws=ws, out_idx=out_idx, out_pts=out_pts,
+                                  return_points=out_pts is not None)
         return idx.shape[0], rep2
 
     # Steps 1-3 stay on the device (Step 2 by the device builder, SURVEY §8
