@@ -33,6 +33,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 
 #include "k2_common.cuh"
@@ -522,6 +523,9 @@ cudaError_t launch_tma_t(const K2Params& p, cudaStream_t s, int* launches) {
         int per_sm = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2_filter_tma<EDGES, CFG, DBG>, kBlock, smem);
         max_blocks = (per_sm > 0 ? per_sm : 1) * device_sm_count();
+        if (getenv("CUDAPRE_K2_VERBOSE"))
+            fprintf(stderr, "k2_filter_tma<%d warps>: %d B shared memory, %d threads, %d blocks/SM\n", K2_NW, smem,
+                    (int)kBlock, per_sm);
     }
     unsigned blocks = p.num_tiles < (unsigned)max_blocks ? p.num_tiles : (unsigned)max_blocks;
     if (blocks > p.scratch_blocks) blocks = p.scratch_blocks;   // one overflow scratch area per block
