@@ -311,14 +311,6 @@ __global__ void __launch_bounds__(kBlock, K2Cfg<CFG>::kMinB) k2_filter_tma(const
                 const unsigned total = __shfl_sync(kFull, inc, 31);
                 if (lane == 0) {
                     cur.total = total;
-                    if (p.debug == 3) {   // perf experiment: publish from the emit warp instead
-                        if (tile == 0) {
-                            publish(p, 0, kFlagP, total, epoch);
-                            if (p.num_tiles == 1) p.ws->count = total;
-                        } else {
-                            publish(p, tile, kFlagA, total, epoch);
-                        }
-                    }
                 }
                 __syncwarp();
             }
@@ -403,9 +395,18 @@ __global__ void __launch_bounds__(kBlock, K2Cfg<CFG>::kMinB) k2_filter_tma(const
                 const float2* chunk2 = reinterpret_cast<const float2*>(chunk);
                 unsigned needy = 0u;   // bit r: point r*32 + lane not decided by the fast test
                 if (np == (unsigned)kSubPairsT) {
-                    if (p.debug == 1) {   // perf experiment only: skeleton, no classification
+                    if (p.debug == 1 || p.debug == 3) {
+                        // perf experiments only (wrong results): 1 = skeleton, nothing
+                        // survives; 3 = no classification, 1/32 of the points
+                        // (a hash of the global index) survive
 #pragma unroll
-                        for (int r = 0; r < 8; ++r) needy |= (chunk2[r * 32 + lane].x == 12345.0f ? 1u : 0u) << r;
+                        for (int r = 0; r < 8; ++r) {
+                            const float x = chunk2[r * 32 + lane].x;
+                            const unsigned h = (tile * (2u * kTilePairsT) + sub * (2u * kSubPairsT) + warp * 256u +
+                                                r * 32u + lane) * 2654435761u;
+                            const bool sel = p.debug == 1 ? x == 12345.0f : (h >> 27) == 0u;
+                            needy |= (sel ? 1u : 0u) << r;
+                        }
                     } else if (fast == 0) {
 #pragma unroll
                         for (int r = 0; r < 8; ++r) {
@@ -464,7 +465,7 @@ __global__ void __launch_bounds__(kBlock, K2Cfg<CFG>::kMinB) k2_filter_tma(const
                             } else {   // the unpaired last point
                                 q = __ldg(reinterpret_cast<const float2*>(p.pts) + 2u * full_pairs);
                             }
-                            kp = classify_queued<EDGES>(S, mode, gox, goy, ge2, q.x, q.y);
+                            kp = p.debug == 3 ? true : classify_queued<EDGES>(S, mode, gox, goy, ge2, q.x, q.y);
                         }
                         const unsigned kb = __ballot_sync(kFull, kp);
                         if (kp) {
@@ -485,7 +486,7 @@ __global__ void __launch_bounds__(kBlock, K2Cfg<CFG>::kMinB) k2_filter_tma(const
         if (have && cur.lstart[warp][kK2Sub] > kL) __threadfence_block();   // scratch writes before the signal
         __syncwarp();
         if (lane == 0) {
-            if (have && p.debug != 3) {
+            if (have) {
                 // the last compute warp done with the tile publishes its aggregate
                 // at once: other blocks' look-backs never wait on this block's
                 // emit warp (a late aggregate stalls every later tile's look-back)
