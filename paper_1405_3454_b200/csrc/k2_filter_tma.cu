@@ -186,7 +186,10 @@ __device__ __forceinline__ void emit_t(const K2Params& p, const TileT<kL>& ts, c
 // 2 blocks per SM); CFG 1: 3-stage ring, 128-entry lists.  Overflowing lists
 // spill to global scratch, so the list size only trades smem for traffic.
 template <int CFG> struct K2Cfg;
-template <> struct K2Cfg<0> { static constexpr int kNst = K2_NW == 10 ? 3 : 4; static constexpr unsigned kL = 96; static constexpr int kMinB = 2; };
+#ifndef K2_KL
+#define K2_KL 96
+#endif
+template <> struct K2Cfg<0> { static constexpr int kNst = K2_NW == 10 ? 3 : 4; static constexpr unsigned kL = K2_KL; static constexpr int kMinB = 2; };
 template <> struct K2Cfg<1> { static constexpr int kNst = 3; static constexpr unsigned kL = 128; static constexpr int kMinB = 2; };
 
 // DBG: perf-experiment build with per-warp cycle counters (CUDAPRE_K2_DEBUG=2)
