@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-points", action="store_true",
                     help="write only the survivors' indices (perf experiment; not the benchmark workload)")
+    ap.add_argument("--no-host-step2-check", action="store_true",
+                    help="skip the extra host-Step-2 timing loop reported as host_step2_value")
     ap.add_argument("--host-step2", action="store_true",
                     help="run Step 2 (and, N > 1, the merge) on the host between the kernels, as the paper")
     return ap.parse_args()
@@ -276,6 +278,25 @@ def main():
         _, rep2 = step(rep1)
         lb_rounds[:] = [rep2["lookback_rounds"], rep2["lookback_spins"]]
         assert rep2["survivors"] == surv, (rep2["survivors"], surv)
+    # the same K steps with the paper's host Step 2 between the kernels (D2H of
+    # the picks, host polygon, H2D of the geometry; N > 1: host merge), for
+    # comparison with the device-resident default (identical outputs)
+    host_ms = None
+    if device_path and not args.no_host_step2_check:
+        if group is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+        h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        h0.record()
+        for _ in range(args.steps):
+            step(rep1)
+        h1.record()
+        torch.cuda.synchronize()
+        host_ms = h0.elapsed_time(h1)
+        if group is not None:
+            t = torch.tensor([host_ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            host_ms = float(t.item())
     if group is not None:
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -387,13 +408,15 @@ def main():
                               if 8 * n_local > 126e6 else
                               f"inputs ({8 * n_local / 1e6:.0f} MB) fit in L2: warm-L2 numbers, not a roofline claim"),
                        "parallelism": f"dp{world} (point shards; 912 B NCCL all-gather per step)",
-                       "step2": "device" if device_path else "host"},
+                       "step2": ("device (byte-identical to the host build, SURVEY f3; host_step2_value: the paper's host Step 2)"
+                                 if device_path else "host")},
             "discard_pct": round(100 * (1 - surv_total / n_total), 4),
             "remaining_pct": round(100 * surv_total / n_total, 4),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": clocks.result(),
             "k1_exact_path_points_per_step": int(exact_pts[0]),
             ("host_step2_ms" if not device_path else "step2_device_ms"): round(statistics.median(poly_ms), 4),
+            "host_step2_value": (round(n_total * args.steps / (host_ms / 1e3) / 1e9, 3) if host_ms else None),
             "k2_lookback_rounds_per_step": int(lb_rounds[0]), "k2_lookback_spins_per_step": int(lb_rounds[1]),
         }
         print(json.dumps(line), flush=True)
