@@ -146,3 +146,29 @@ def test_device_merge_of_shards(k):
         assert bytes(cp.result_view(ws).cpu().numpy().tobytes()) == bytes(merged.raw)
         got.append(out_idx[: int(count.item())].cpu().numpy())
     assert np.array_equal(np.concatenate(got), want)
+
+
+@pytest.mark.parametrize("n", [1, 2, 4, 7])
+def test_device_path_tiny_inputs(n):
+    xy = synth.generate("disk", n, seed=n + 40)
+    pts = torch.from_numpy(xy).cuda()
+    want = oracle.cudapre(xy, "A", threads=1)["survivors"]
+    out_idx, out_pts, count = cp.pipeline(pts, "A")
+    torch.cuda.synchronize()
+    m = int(count.item())
+    assert np.array_equal(out_idx[:m].cpu().numpy(), want)
+    g = cp.Graph(pts, "A")
+    g.launch()
+    torch.cuda.synchronize()
+    assert np.array_equal(g.out_idx[: int(g.count.item())].cpu().numpy(), want)
+    g.close()
+
+
+def test_device_path_single_repeated_point_and_empty():
+    xy = np.tile(np.array([[0.25, -0.5]], np.float32), (70_000, 1))   # one distinct point
+    out_idx, _, count = cp.pipeline(torch.from_numpy(xy).cuda(), "A", return_points=False)
+    torch.cuda.synchronize()
+    assert int(count.item()) == len(xy)                                # degenerate ring: all kept
+    with pytest.raises(cp.CudaPreError) as e:
+        cp.pipeline(torch.empty((0, 2), device="cuda"), "A")
+    assert e.value.status == cp.ERR_EMPTY
