@@ -89,4 +89,45 @@ CUDAPRE_HD int orient_sign_f(float ax, float ay, float bx, float by, float cx, f
     return 0;
 }
 
+// The same exact sign, with a float32 filter in front (Shewchuk's orient2d
+// stage A in single precision): det = (ax-cx)(by-cy) - (ay-cy)(bx-cx) has
+// |fl(det) - det| <= (3e + 16e^2)(|dl| + |dr|) for e = 2^-24 without
+// underflow; subnormal differences are exact and a subnormal product is off by
+// <= 2^-150, which the 2^-140 term covers; any overflow fails the finiteness
+// test.  Used where one thread runs many predicates in a row (the Step-2
+// builders): the result is the exact sign either way.
+CUDAPRE_HD float xfsub(float a, float b) {
+#if defined(__CUDA_ARCH__)
+    return __fsub_rn(a, b);
+#else
+    return a - b;
+#endif
+}
+CUDAPRE_HD float xfmul(float a, float b) {
+#if defined(__CUDA_ARCH__)
+    return __fmul_rn(a, b);
+#else
+    return a * b;
+#endif
+}
+CUDAPRE_HD float xfadd(float a, float b) {
+#if defined(__CUDA_ARCH__)
+    return __fadd_rn(a, b);
+#else
+    return a + b;
+#endif
+}
+CUDAPRE_HD int orient_sign_filtered(float ax, float ay, float bx, float by, float cx, float cy) {
+    const float dl = xfmul(xfsub(ax, cx), xfsub(by, cy));
+    const float dr = xfmul(xfsub(ay, cy), xfsub(bx, cx));
+    const float det = xfsub(dl, dr);
+    const float sum = xfadd(dl < 0 ? -dl : dl, dr < 0 ? -dr : dr);
+    const float bound = xfadd(xfmul(0x1p-22f, sum), 0x1p-140f);   // 4e > 3e + 16e^2 + the bound's own roundings
+    if (bound < 0x1p+127f) {   // finite (NaN / inf fail the comparison)
+        if (det > bound) return 1;
+        if (det < -bound) return -1;
+    }
+    return orient_sign_f(ax, ay, bx, by, cx, cy);
+}
+
 }  // namespace cudapre

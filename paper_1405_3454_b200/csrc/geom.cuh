@@ -126,7 +126,7 @@ GEOM_HD double sample_pa(int i) {
 GEOM_HD bool strictly_inside_ring(const float* vx, const float* vy, int nv, float px, float py) {
     for (int j = 0; j < nv; ++j) {
         const int k = j + 1 == nv ? 0 : j + 1;
-        if (orient_sign_f(vx[j], vy[j], vx[k], vy[k], px, py) <= 0) return false;
+        if (orient_sign_filtered(vx[j], vy[j], vx[k], vy[k], px, py) <= 0) return false;
     }
     return true;
 }
@@ -181,24 +181,11 @@ GEOM_HD void merge_header(const cudapre_extremes_t* parts, int count, cudapre_ex
 // Picks -> Andrew's monotone chain (A9, A10): lexicographic (x, y, id)
 // order, distinct coordinates keep the lowest id (-0 == +0), pop while not a
 // strict left turn.  Plus the exact bbox and the vertex mean.
-GEOM_HD void phase_a(const cudapre_extremes_t& ext, Work& w) {
-    Pick P[CUDAPRE_MAX_SLOTS];
-    int m = 0;
-    const int slots = 4 * ext.nang;
-    for (int s = 0; s < slots; ++s)
-        if (ext.idx[s] >= 0) P[m++] = Pick{ext.pt[s].x, ext.pt[s].y, (long long)ext.idx[s]};
-    for (int i = 1; i < m; ++i) {   // insertion sort (total order: ids are distinct or equal picks)
-        const Pick t = P[i];
-        int j = i - 1;
-        while (j >= 0 && pick_less(t, P[j])) {
-            P[j + 1] = P[j];
-            --j;
-        }
-        P[j + 1] = t;
-    }
-    int u = m ? 1 : 0;
-    for (int j = 1; j < m; ++j)
-        if (P[j].x != P[u - 1].x || P[j].y != P[u - 1].y) P[u++] = P[j];
+// (a) the chain over the sorted distinct picks P[0..u) (H: scratch of
+//     2*CUDAPRE_MAX_SLOTS+1 entries); (b) bbox / mean.  phase_a() runs the
+//     whole phase on one thread; the device builder sorts and dedups with a
+//     warp first (a rank sort under the same total order gives the same array).
+GEOM_HD void phase_a_chain(const Pick* P, int u, Pick* H, Work& w) {
     w.n_distinct = u;
     int nv = 0;
     if (u == 1) {
@@ -207,15 +194,14 @@ GEOM_HD void phase_a(const cudapre_extremes_t& ext, Work& w) {
         w.vy[0] = P[0].y;
         nv = 1;
     } else if (u > 1) {
-        Pick H[2 * CUDAPRE_MAX_SLOTS + 1];
         int k = 0;
         for (int j = 0; j < u; ++j) {
-            while (k >= 2 && orient_sign_f(H[k - 2].x, H[k - 2].y, H[k - 1].x, H[k - 1].y, P[j].x, P[j].y) <= 0) --k;
+            while (k >= 2 && orient_sign_filtered(H[k - 2].x, H[k - 2].y, H[k - 1].x, H[k - 1].y, P[j].x, P[j].y) <= 0) --k;
             H[k++] = P[j];
         }
         const int lower = k;
         for (int j = u - 2; j >= 0; --j) {
-            while (k > lower && orient_sign_f(H[k - 2].x, H[k - 2].y, H[k - 1].x, H[k - 1].y, P[j].x, P[j].y) <= 0)
+            while (k > lower && orient_sign_filtered(H[k - 2].x, H[k - 2].y, H[k - 1].x, H[k - 1].y, P[j].x, P[j].y) <= 0)
                 --k;
             H[k++] = P[j];
         }
@@ -235,6 +221,9 @@ GEOM_HD void phase_a(const cudapre_extremes_t& ext, Work& w) {
     w.r2 = -1.0f;
     w.cx = w.cy = 0.0f;
     w.rs_up = 1.0;
+}
+GEOM_HD void phase_a_tail(const cudapre_extremes_t& ext, Work& w) {
+    const int nv = w.nv;
     // exact data bounding box: the angle-0 picks (c0 = 1, s0 = 0)
     const double xmin = ext.pt[0].x, xmax = ext.pt[1].x, ymin = ext.pt[2].y, ymax = ext.pt[3].y;
     w.Mx = dmax(fabs(xmin), fabs(xmax));
@@ -260,6 +249,31 @@ GEOM_HD void phase_a(const cudapre_extremes_t& ext, Work& w) {
     w.oy = oy;
     w.hw = 0.5 * (pxmax - pxmin);
     w.hh = 0.5 * (pymax - pymin);
+}
+// Picks -> Andrew's monotone chain (A9, A10): lexicographic (x, y, id)
+// order, distinct coordinates keep the lowest id (-0 == +0), pop while not a
+// strict left turn.  Plus the exact bbox and the vertex mean.
+GEOM_HD void phase_a(const cudapre_extremes_t& ext, Work& w) {
+    Pick P[CUDAPRE_MAX_SLOTS];
+    int m = 0;
+    const int slots = 4 * ext.nang;
+    for (int s = 0; s < slots; ++s)
+        if (ext.idx[s] >= 0) P[m++] = Pick{ext.pt[s].x, ext.pt[s].y, (long long)ext.idx[s]};
+    for (int i = 1; i < m; ++i) {   // insertion sort (total order: ids are distinct or equal picks)
+        const Pick t = P[i];
+        int j = i - 1;
+        while (j >= 0 && pick_less(t, P[j])) {
+            P[j + 1] = P[j];
+            --j;
+        }
+        P[j + 1] = t;
+    }
+    int u = m ? 1 : 0;
+    for (int j = 1; j < m; ++j)
+        if (P[j].x != P[u - 1].x || P[j].y != P[u - 1].y) P[u++] = P[j];
+    Pick H[2 * CUDAPRE_MAX_SLOTS + 1];
+    phase_a_chain(P, u, H, w);
+    phase_a_tail(ext, w);
 }
 
 // ------------------------------------------------------------------ phase B (per edge)
@@ -300,7 +314,7 @@ GEOM_HD bool box_corner_edge_ok(const Work& w, const float c[4], int q, int j) {
     const float px = (q == 0 || q == 3) ? c[0] : c[1];
     const float py = (q <= 1) ? c[2] : c[3];
     const int k = j + 1 == w.nv ? 0 : j + 1;
-    return orient_sign_f(w.vx[j], w.vy[j], w.vx[k], w.vy[k], px, py) > 0;
+    return orient_sign_filtered(w.vx[j], w.vy[j], w.vx[k], w.vy[k], px, py) > 0;
 }
 
 // ------------------------------------------------------------------ phase D (disk)

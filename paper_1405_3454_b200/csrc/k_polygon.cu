@@ -57,11 +57,44 @@ __global__ void __launch_bounds__(kGeomThreads) k_build_geom(const cudapre_extre
     }
     GT(8);
 
-    if (tid == 0) {
-        phase_a(ext, w);
-        // non-finite or empty Step-1 input (the host API rejects both): keep
-        // everything; the caller sees the flags in the Step-1 result
-        if (ext.nonfinite || ext.n <= 0) w.degenerate = 1;
+    // phase A: warp 0 collects the picks, rank-sorts them under the total
+    // (x, y, id) order (= the host's insertion sort) and keeps the first of
+    // each run of equal coordinates; lane 0 runs the chain
+    __shared__ Pick sp[CUDAPRE_MAX_SLOTS], sd[CUDAPRE_MAX_SLOTS], sh[2 * CUDAPRE_MAX_SLOTS + 1];
+    __shared__ int su;
+    if (tid < 32) {
+        const int slots = 4 * ext.nang;
+        const bool valid = tid < slots && ext.idx[tid] >= 0;
+        const unsigned vb = __ballot_sync(0xffffffffu, valid);
+        const int m = __popc(vb);
+        Pick me = {0.f, 0.f, 0};
+        if (valid) {
+            me = Pick{ext.pt[tid].x, ext.pt[tid].y, (long long)ext.idx[tid]};
+            sp[__popc(vb & ((1u << tid) - 1u))] = me;
+        }
+        __syncwarp();
+        const int i = valid ? __popc(vb & ((1u << tid) - 1u)) : -1;   // this lane's pick position
+        int rank = 0;
+        if (i >= 0)
+            for (int j = 0; j < m; ++j) {
+                const Pick o = sp[j];
+                rank += pick_less(o, me) || (!pick_less(me, o) && j < i);
+            }
+        __syncwarp();
+        if (i >= 0) sp[rank] = me;   // (equal picks are identical: any order is the same array)
+        __syncwarp();
+        const bool first = tid < m && (tid == 0 || sp[tid].x != sp[tid - 1].x || sp[tid].y != sp[tid - 1].y);
+        const unsigned fb = __ballot_sync(0xffffffffu, first);
+        if (first) sd[__popc(fb & ((1u << tid) - 1u))] = sp[tid];
+        __syncwarp();
+        if (tid == 0) {
+            su = __popc(fb);
+            phase_a_chain(sd, su, sh, w);
+            phase_a_tail(ext, w);
+            // non-finite or empty Step-1 input (the host API rejects both): keep
+            // everything; the caller sees the flags in the Step-1 result
+            if (ext.nonfinite || ext.n <= 0) w.degenerate = 1;
+        }
     }
     GT(9);
     __syncthreads();

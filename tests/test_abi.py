@@ -441,3 +441,34 @@ def test_k2_candidate_edges_hold_the_exit_edge(L, oracle_lib, family, angles):
                 assert exits & rng_edges, (family, angles, bb, lo, hi, exits)
                 checked += 1
     assert checked > 1000
+
+
+def test_filtered_orient_in_step2_vs_fractions(L, oracle_lib):
+    """The Step-2 builders use a float32 orientation filter in front of the
+    exact predicate (exact.cuh orient_sign_filtered); on the oracle's hard
+    triples (near-collinear, subnormal, huge) the polygon's ring must equal
+    the exact gift wrap."""
+    rng = np.random.default_rng(12)
+    from tests.test_oracle_pins import _float_triples
+
+    checked = 0
+    for a, b, c in _float_triples(rng, 3000):
+        pts = np.array([a, b, c], np.float32)
+        if not np.isfinite(pts).all():
+            continue
+        r = cp.ExtremesT()
+        r.nang, r.n = 1, 3
+        for k in range(32):
+            r.idx[k] = -1
+        r.c[0], r.s[0] = 1.0, 0.0
+        for slot, i in enumerate((0, 1, 2, 0)):
+            r.idx[slot] = i
+            r.pt[slot].x, r.pt[slot].y = float(pts[i, 0]), float(pts[i, 1])
+        poly = cp.polygon(cp.Extremes(r))
+        want = brute.gift_wrap(pts)
+        if len(want) >= 3:
+            assert poly.vidx.tolist() == want, pts
+            checked += 1
+        else:
+            assert poly.degenerate, pts
+    assert checked > 500
