@@ -188,14 +188,15 @@ def main():
     from paper_1405_3454_b200 import build as pbuild
 
     torch.cuda.set_device(local)
-    if rank == 0:
-        pbuild.build()
-        scuda.build()
     group = None
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         group = dist.group.WORLD
-        dist.barrier()
+    if rank == 0:   # (no-op when the in-tree libraries are up to date)
+        pbuild.build()
+        scuda.build()
+    if group is not None:
+        dist.barrier()   # no rank loads a library rank 0 may be rebuilding
     n_local = n_total // world + (1 if rank < n_total % world else 0)
     base = rank * (n_total // world) + min(rank, n_total % world)
     pts = scuda.generate(family, n_local, seed=seed, base=base, **cfg)
