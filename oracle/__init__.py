@@ -19,6 +19,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "cudapre_oracle.c")
+_SRC3 = os.path.join(_HERE, "cudapre3_oracle.c")   # the 3D extension
 _LIB = os.path.join(_HERE, "liboracle.so")
 CFLAGS = ["-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared", "-pthread"]
 
@@ -27,9 +28,10 @@ _lib = None
 
 def build(force: bool = False) -> str:
     """Compile the oracle with gcc (idempotent)."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+    newest = max(os.path.getmtime(_SRC), os.path.getmtime(_SRC3))
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < newest:
         tmp = _LIB + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, _SRC, "-lm"])
+        subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, _SRC, _SRC3, "-lm"])
         os.replace(tmp, _LIB)
     return _LIB
 
@@ -54,6 +56,20 @@ def _load():
         lib.oracle_filter_mask.restype = None
         lib.oracle_cudapre.argtypes = [vp, i64, vp, vp, i32, i32, vp, vp, vp, vp]
         lib.oracle_cudapre.restype = i32
+        lib.oracle3_orient.argtypes = [vp, vp, vp, vp]
+        lib.oracle3_orient.restype = i32
+        lib.oracle3_extremes.argtypes = [vp, i64, vp, vp, i32, i32, vp, vp]
+        lib.oracle3_extremes.restype = i32
+        lib.oracle3_distinct.argtypes = [vp, vp, i64, vp]
+        lib.oracle3_distinct.restype = i64
+        lib.oracle3_facets.argtypes = [vp, vp, i64, vp, i64]
+        lib.oracle3_facets.restype = i64
+        lib.oracle3_strictly_inside.argtypes = [vp, i64, vp]
+        lib.oracle3_strictly_inside.restype = i32
+        lib.oracle3_filter_mask.argtypes = [vp, i64, vp, i64, i32, vp]
+        lib.oracle3_filter_mask.restype = None
+        lib.oracle3_cudapre.argtypes = [vp, i64, vp, vp, i32, i32, vp, vp, i64, vp, vp]
+        lib.oracle3_cudapre.restype = i32
         _lib = lib
     return _lib
 
@@ -168,5 +184,99 @@ def cudapre(xy, angles="A", threads: int = 1) -> dict:
         "ext_idx": ext,
         "ring": ring[:nvv].copy(),
         "degenerate": nvv < 3,
+        "survivors": np.flatnonzero(keep).astype(np.int64),
+    }
+
+
+# ---------------------------------------------------------------------------
+# The 3D extension (readings B1-B6 in DESIGN.md §3).
+# The arithmetic lives in cudapre3_oracle.c.
+
+MAX_FACETS3 = 4096
+
+
+def _pts3(xyz) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(xyz, dtype=np.float32).reshape(-1, 3))
+
+
+def orient3d(a, b, c, d) -> int:
+    """Exact sign of det[b-a; c-a; d-a] for float inputs (reading B6)."""
+    q = [np.ascontiguousarray(np.asarray(v, np.float32).reshape(3)) for v in (a, b, c, d)]
+    return int(_load().oracle3_orient(*[_ptr(v) for v in q]))
+
+
+def extremes3(xyz, angles="A", threads: int = 1, with_keys: bool = False):
+    """Step 1 in 3D (P:115 with P:33-35; B1, B2): 6*len(angles) indices, slot
+    6k+{minX, maxX, minY, maxY, minZ, maxZ} of the frame rotated by angle k
+    about z; lowest index on ties.  Raises ValueError on empty input."""
+    p = _pts3(xyz)
+    c, s = coeffs(angles)
+    idx = np.empty(6 * len(c), np.int64)
+    key = np.empty(6 * len(c), np.float64)
+    if _load().oracle3_extremes(_ptr(p), len(p), _ptr(c), _ptr(s), len(c), threads, _ptr(idx),
+                                _ptr(key)) != 0:
+        raise ValueError("empty input")
+    return (idx, key) if with_keys else idx
+
+
+def distinct3(xyz, picks) -> np.ndarray:
+    """E: the distinct picks, ascending index, equal coordinates -> lowest index (B3)."""
+    p = _pts3(xyz)
+    pk = np.ascontiguousarray(np.asarray(picks, np.int64))
+    E = np.empty(max(len(pk), 1), np.int64)
+    m = _load().oracle3_distinct(_ptr(p), _ptr(pk), len(pk), _ptr(E))
+    if m < 0:
+        raise ValueError("too many picks")
+    return E[:m].copy()
+
+
+def facets3(xyz, E) -> np.ndarray:
+    """Step 2 in 3D (B3, B4): (nf, 3) point ids of the first supporting triple
+    of each facet plane of conv(E), E on the positive side; nf = 0 means
+    degenerate (|E| < 4 or coplanar)."""
+    p = _pts3(xyz)
+    Ea = np.ascontiguousarray(np.asarray(E, np.int64))
+    out = np.empty((MAX_FACETS3, 3), np.int64)
+    nf = _load().oracle3_facets(_ptr(p), _ptr(Ea), len(Ea), _ptr(out), MAX_FACETS3)
+    if nf < 0:
+        raise ValueError("facet overflow")
+    return out[:nf].copy()
+
+
+def strictly_inside3(fxyz, p) -> bool:
+    """1 iff orient3d(f, p) > 0 for every facet (fxyz: (nf, 3, 3) coordinates)."""
+    f = np.ascontiguousarray(np.asarray(fxyz, np.float32).reshape(-1, 9))
+    q = np.ascontiguousarray(np.asarray(p, np.float32).reshape(3))
+    return bool(_load().oracle3_strictly_inside(_ptr(f), len(f), _ptr(q)))
+
+
+def filter_mask3(xyz, fxyz, threads: int = 1) -> np.ndarray:
+    """Step 3 in 3D (B5): keep[i] = not strictly inside the polyhedron."""
+    p = _pts3(xyz)
+    f = np.ascontiguousarray(np.asarray(fxyz, np.float32).reshape(-1, 9))
+    keep = np.zeros(len(p), np.uint8)
+    _load().oracle3_filter_mask(_ptr(p), len(p), _ptr(f), len(f), threads, _ptr(keep))
+    return keep.astype(bool)
+
+
+def cudapre3(xyz, angles="A", threads: int = 1) -> dict:
+    """The 3D method in order: ``ext_idx`` (Step 1), ``facets`` (Step 2,
+    (nf, 3) ids), ``degenerate``, ``survivors`` (Step 3, ascending int64)."""
+    p = _pts3(xyz)
+    if len(p) == 0:
+        raise ValueError("empty input")
+    c, s = coeffs(angles)
+    ext = np.empty(6 * len(c), np.int64)
+    fac = np.empty((MAX_FACETS3, 3), np.int64)
+    nf = np.zeros(1, np.int64)
+    keep = np.zeros(len(p), np.uint8)
+    if _load().oracle3_cudapre(_ptr(p), len(p), _ptr(c), _ptr(s), len(c), threads, _ptr(ext),
+                               _ptr(fac), MAX_FACETS3, _ptr(nf), _ptr(keep)) != 0:
+        raise ValueError("empty input")
+    k = int(nf[0])
+    return {
+        "ext_idx": ext,
+        "facets": fac[:k].copy(),
+        "degenerate": k == 0,
         "survivors": np.flatnonzero(keep).astype(np.int64),
     }
