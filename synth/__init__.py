@@ -161,6 +161,65 @@ def generate(family: str, n: int, seed: int, base: int = 0, *, lo: float = -1.0,
     return out
 
 
+# ---------------------------------------------------------------------------
+# 3D families (the 3D extension).  Same counter-based
+# stream; a point's first draw (stream 0) gives (u1, u2), its second draw
+# (stream 1) gives (u3, u4).
+#   cube    uniform in [lo, hi)^3                 x = RN(RN(u*w) + lo)
+#   ball    uniform in the unit ball              per-index rejection from [-1,1)^3,
+#                                                 RN(RN(x^2 + y^2) + z^2) <= 1 (float32)
+#   sphere  near-sphere shell r in [1-eps, 1]     direction of a ball sample, radius 1-eps*u4
+FAMILIES3 = ("cube", "ball", "sphere")
+
+
+def _gen3_chunk(family: str, key, idx: np.ndarray, lo: float, hi: float, eps: float) -> np.ndarray:
+    n = len(idx)
+    out = np.zeros((n, 3), np.float32)
+    if family == "cube":
+        u1, u2 = _uniforms(draw(key, idx, 0, 0))
+        u3, _ = _uniforms(draw(key, idx, 0, 1))
+        w = np.float32(hi) - np.float32(lo)
+        for j, u in enumerate((u1, u2, u3)):
+            out[:, j] = u * w + np.float32(lo)
+        return out
+    pending = np.arange(n)
+    for attempt in range(MAX_ATTEMPTS):
+        if len(pending) == 0:
+            break
+        u1, u2 = _uniforms(draw(key, idx[pending], attempt, 0))
+        u3, u4 = _uniforms(draw(key, idx[pending], attempt, 1))
+        x, y, z = _pm1(u1), _pm1(u2), _pm1(u3)
+        s = (x * x + y * y) + z * z        # float32: RN products, RN sums in this order
+        if family == "ball":
+            ok = s <= np.float32(1.0)
+            out[pending[ok]] = np.stack([x[ok], y[ok], z[ok]], 1)
+        elif family == "sphere":
+            ok = (s > np.float32(0.0)) & (s <= np.float32(1.0))
+            xd, yd, zd = (v[ok].astype(np.float64) for v in (x, y, z))
+            d = np.sqrt((xd * xd + yd * yd) + zd * zd)
+            r = 1.0 - eps * u4[ok].astype(np.float64)
+            sc = r / d
+            out[pending[ok]] = np.stack([xd * sc, yd * sc, zd * sc], 1).astype(np.float32)
+        else:
+            raise ValueError(f"unknown 3D family {family!r}")
+        pending = pending[~ok]
+    return out
+
+
+def generate3(family: str, n: int, seed: int, base: int = 0, *, lo: float = -1.0,
+              hi: float = 1.0, eps: float = 1e-3, chunk: int = 1 << 22) -> np.ndarray:
+    """3D points [base, base+n) of the seeded stream, as a float32 (n, 3) array."""
+    if family not in FAMILIES3:
+        raise ValueError(f"unknown 3D family {family!r}")
+    key = seed_key(seed)
+    out = np.empty((n, 3), np.float32)
+    for a in range(0, n, chunk):
+        b = min(n, a + chunk)
+        idx = np.arange(base + a, base + b, dtype=np.int64)
+        out[a:b] = _gen3_chunk(family, key, idx, lo, hi, eps)
+    return out
+
+
 # Named configs (BASELINE.json "configs"; SURVEY §8(d)).
 CONFIGS = {
     "C1": dict(family="square", n=100_000, seed=1, lo=0.0, hi=1.0),
@@ -172,8 +231,16 @@ CONFIGS = {
     "C5": dict(family="disk", n=2_000_000_000, seed=6),
 }
 
+# 3D workloads (f4; not BASELINE configs): 1e9 points = 12 GB of float3.
+CONFIGS3 = {
+    "T1": dict(family="ball", n=1_000_000, seed=21),
+    "T3": dict(family="cube", n=1_000_000_000, seed=22),
+    "T4": dict(family="ball", n=1_000_000_000, seed=23),
+    "T5": dict(family="sphere", n=200_000_000, seed=24, eps=1e-3),
+}
+
 
 def config_kwargs(name: str) -> dict:
-    cfg = dict(CONFIGS[name])
+    cfg = dict(CONFIGS[name] if name in CONFIGS else CONFIGS3[name])
     cfg.pop("n")
     return cfg

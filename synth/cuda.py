@@ -8,7 +8,7 @@ import subprocess
 _HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = os.path.join(_HERE, "gen.cu")
 LIB = os.path.join(_HERE, "libsynth.so")
-_FAM = {"square": 0, "disk": 1, "gauss": 2, "circle": 3}
+_FAM = {"square": 0, "disk": 1, "gauss": 2, "circle": 3, "cube": 10, "ball": 11, "sphere": 12}
 _lib = None
 
 
@@ -38,7 +38,8 @@ def _load():
 
 def generate_into(out, family: str, seed: int, base: int = 0, *, lo: float = -1.0, hi: float = 1.0,
                   eps: float = 1e-3, stream=None):
-    """Fill the CUDA float32 tensor ``out`` (n, 2) with points [base, base+n)."""
+    """Fill the CUDA float32 tensor ``out`` ((n, 2), or (n, 3) for a 3D family)
+    with points [base, base+n)."""
     import torch
 
     s = stream if stream is not None else torch.cuda.current_stream()
@@ -53,4 +54,11 @@ def generate(family: str, n: int, seed: int, base: int = 0, device="cuda", **kw)
     import torch
 
     out = torch.empty((n, 2), dtype=torch.float32, device=device)
+    return generate_into(out, family, seed, base, **kw)
+
+
+def generate3(family: str, n: int, seed: int, base: int = 0, device="cuda", **kw):
+    import torch
+
+    out = torch.empty((n, 3), dtype=torch.float32, device=device)
     return generate_into(out, family, seed, base, **kw)

@@ -105,11 +105,54 @@ __global__ void gen_kernel(int family, long long n, unsigned long long key, long
     }
 }
 
+// 3D families (synth.generate3): 10 cube, 11 ball, 12 sphere
+__global__ void gen3_kernel(int family, long long n, unsigned long long key, long long base, float lo,
+                            float w, double eps, float* out) {
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += stride) {
+        const unsigned long long i = (unsigned long long)(base + j);
+        float r0 = 0.f, r1 = 0.f, r2 = 0.f;
+        if (family == 10) {
+            const unsigned long long z0 = draw(key, i, 0, 0), z1 = draw(key, i, 0, 1);
+            r0 = __fadd_rn(__fmul_rn(u_hi(z0), w), lo);
+            r1 = __fadd_rn(__fmul_rn(u_lo(z0), w), lo);
+            r2 = __fadd_rn(__fmul_rn(u_hi(z1), w), lo);
+        } else {
+            for (int a = 0; a < kMaxAttempts; ++a) {
+                const unsigned long long z0 = draw(key, i, a, 0), z1 = draw(key, i, a, 1);
+                const float x = pm1(u_hi(z0)), y = pm1(u_lo(z0)), z = pm1(u_hi(z1));
+                const float s = __fadd_rn(__fadd_rn(__fmul_rn(x, x), __fmul_rn(y, y)), __fmul_rn(z, z));
+                if (family == 11) {
+                    if (s <= 1.0f) {
+                        r0 = x, r1 = y, r2 = z;
+                        break;
+                    }
+                } else if (s > 0.0f && s <= 1.0f) {
+                    const double xd = x, yd = y, zd = z;
+                    const double d = __dsqrt_rn(
+                        __dadd_rn(__dadd_rn(__dmul_rn(xd, xd), __dmul_rn(yd, yd)), __dmul_rn(zd, zd)));
+                    const double rr = __dsub_rn(1.0, __dmul_rn(eps, (double)u_lo(z1)));
+                    const double sc = __ddiv_rn(rr, d);
+                    r0 = __double2float_rn(__dmul_rn(xd, sc));
+                    r1 = __double2float_rn(__dmul_rn(yd, sc));
+                    r2 = __double2float_rn(__dmul_rn(zd, sc));
+                    break;
+                }
+            }
+        }
+        out[3 * j] = r0;
+        out[3 * j + 1] = r1;
+        out[3 * j + 2] = r2;
+    }
+}
+
 }  // namespace
 
 extern "C" int synth_generate(int family, long long n, unsigned long long seed, long long base,
                               double lo, double hi, double eps, void* d_out, void* stream) {
-    if (family < 0 || family > 3 || n < 0) return (int)cudaErrorInvalidValue;
+    const bool three = family >= 10 && family <= 12;
+    if (!three && (family < 0 || family > 3)) return (int)cudaErrorInvalidValue;
+    if (n < 0) return (int)cudaErrorInvalidValue;
     if (n == 0) return 0;
     unsigned long long key = mix64(seed * kGolden + kSalt);
     const float flo = (float)lo, fhi = (float)hi;
@@ -119,7 +162,11 @@ extern "C" int synth_generate(int family, long long n, unsigned long long seed, 
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     long long blocks = (n + 255) / 256;
     if (blocks > (long long)sms * 16) blocks = (long long)sms * 16;
-    gen_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(family, n, key, base, flo, w, eps,
-                                                                   (float2*)d_out);
+    if (three)
+        gen3_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(family, n, key, base, flo, w, eps,
+                                                                        (float*)d_out);
+    else
+        gen_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(family, n, key, base, flo, w, eps,
+                                                                       (float2*)d_out);
     return (int)cudaGetLastError();
 }
