@@ -342,6 +342,100 @@ cudapre_status cudapre_hull_device(const cudapre_pt* d_pts, const int64_t* d_ids
                                    void* stream, int64_t* h_ring, int64_t ring_capacity,
                                    int64_t* h_ring_len, int64_t* h_remaining);
 
+/* ====================================================================
+ * The 3D extension (DESIGN.md §3 B1-B6, §6.5).
+ * "In 3D, typically six extreme points can be obtained by finding those
+ * points with the min or max x, y, or z coordinates.  More groups of six
+ * extreme points can also be found after rotating the set of points along a
+ * specific axis.  These extreme points can be then used to form a convex
+ * polyhedron.  Those points locating inside the convex polyhedron must be
+ * interior points, and can be directly discarded."
+ * Points are float32 xyz AoS (12 bytes each), caller-owned device memory,
+ * 4-byte aligned (16-byte aligned: vector path).  The workspace is its own
+ * (cudapre3_workspace_bytes), zero-filled once with cudapre_workspace_init.
+ * ==================================================================== */
+#define CUDAPRE3_MAX_SLOTS (6 * CUDAPRE_MAX_ANGLES)   /* 48 */
+#define CUDAPRE3_MAX_FACETS 64                       /* >= 2 * (4 * 8 + 2) - 4 */
+
+typedef struct { float x, y, z; } cudapre_pt3;
+
+/* Step 1 in 3D (B1, B2): rotation about the z axis.  Slot 6k+{0..5} =
+ * {argmin X_k, argmax X_k, argmin Y_k, argmax Y_k, argmin Z, argmax Z} with
+ * X_k, Y_k as in 2D (binary64, no FMA) and Z = z; lowest index on equal
+ * keys.  The Z slots repeat for every k (a rotation about z leaves z as is). */
+typedef struct {
+    int32_t nang;                          /* angles (slots = 6*nang); angle 0 first */
+    int32_t nonfinite;                     /* 1 if a non-finite coordinate was seen */
+    int64_t n;                             /* points reduced (summed over merged parts) */
+    int64_t idx[CUDAPRE3_MAX_SLOTS];       /* global index of each pick, -1 if none */
+    double key[CUDAPRE3_MAX_SLOTS];        /* binary64 key of each pick */
+    cudapre_pt3 pt[CUDAPRE3_MAX_SLOTS];    /* coordinates of each pick */
+    double c[CUDAPRE_MAX_ANGLES];          /* cos / sin of each angle (correctly rounded, A5) */
+    double s[CUDAPRE_MAX_ANGLES];
+    int64_t exact_points;                  /* diagnostic: points through the exact binary64 path */
+} cudapre3_extremes_t;
+
+/* Step 2 in 3D (B3, B4): the polyhedron conv(E), E = the distinct picks
+ * (equal coordinates -> lowest index), ascending index.  Facet f is the
+ * first supporting triple (a < b < c in E's order) of each facet plane,
+ * stored so that E lies on its positive side: a point p is strictly inside
+ * iff orient3d(fv[f], p) > 0 for every f (B5, B6).  nf = 0: degenerate
+ * (|E| < 4 or E coplanar): nothing is inside.                              */
+typedef struct {
+    int32_t nf;                                 /* facet planes, 0 = degenerate */
+    int32_t n_distinct;                         /* |E| */
+    int32_t octants;                            /* 1: per-octant candidate lists around centre */
+    int32_t n_entries;                          /* candidate entries over the 8 octants */
+    int64_t eidx[CUDAPRE3_MAX_SLOTS];           /* E (global ids, ascending) */
+    int64_t fidx[CUDAPRE3_MAX_FACETS][3];       /* supporting triple of each facet plane */
+    cudapre_pt3 fv[CUDAPRE3_MAX_FACETS][3];     /* its coordinates */
+    float centre[3];                            /* strictly inside (octants == 1) */
+    float err_max;                              /* largest plane-test error bound */
+    int32_t oct_count[8];                       /* candidate facets per octant */
+} cudapre3_polyhedron_t;
+
+/* Workspace bytes for a shard of n_local points (3D). */
+size_t cudapre3_workspace_bytes(int64_t n_local);
+
+/* Step 1 in 3D over d_xyz[0, n_local) (one streaming pass, 12 bytes/point):
+ *   d_xyz       device float[3*n_local] (NULL iff n_local == 0), 4-B aligned
+ *   index_base  global index of the first point
+ *   nang, c, s  angle list (host, c[0] = 1, s[0] = 0 required; NULL = preset 0)
+ *   d_out       nullable DEVICE cudapre3_extremes_t receiving the result
+ *   h_out       nullable HOST result; if given the call blocks until valid
+ * Errors: EMPTY_INPUT (n_local == 0; the empty part, every idx = -1, is still
+ * written), NONFINITE_INPUT (result written, flagged), INVALID_ARGUMENT,
+ * WORKSPACE, CUDA.  n_local < 2^32.                                        */
+cudapre_status cudapre3_extremes(const float* d_xyz, int64_t n_local, int64_t index_base, int32_t nang,
+                                 const double* c, const double* s, void* d_ws, size_t ws_bytes,
+                                 void* stream, cudapre3_extremes_t* d_out, cudapre3_extremes_t* h_out);
+
+/* Shard merge (host): per slot the lexicographic (key, global index) extreme. */
+cudapre_status cudapre3_extremes_merge(const cudapre3_extremes_t* h_parts, int32_t count,
+                                       cudapre3_extremes_t* h_out);
+
+/* Step 2 in 3D on the host: the polyhedron of h_ext (global extremes). */
+cudapre_status cudapre3_polyhedron(const cudapre3_extremes_t* h_ext, cudapre3_polyhedron_t* h_poly);
+
+/* Steps 2+3 in 3D: builds the polyhedron from h_ext, then one streaming pass
+ * classifies every local point and stream-compacts the survivors in
+ * ascending global index order.  Point i is DISCARDED iff orient3d(f, p_i)
+ * > 0 exactly for every facet f; degenerate polyhedron: all survive.
+ *   d_surv_idx  device int64[capacity] global indices (required)
+ *   d_surv_xyz  device float[3*capacity] their coordinates (nullable)
+ *   h_count     host: number of survivors (always written on OK / CAPACITY)
+ *   h_poly      nullable host copy of the polyhedron used
+ * Blocks until *h_count is valid.  NONFINITE_INPUT if h_ext is flagged.
+ * CAPACITY if *h_count > capacity (the first `capacity` are written).      */
+cudapre_status cudapre3_filter(const float* d_xyz, int64_t n_local, int64_t index_base,
+                               const cudapre3_extremes_t* h_ext, int64_t* d_surv_idx, float* d_surv_xyz,
+                               int64_t capacity, void* d_ws, size_t ws_bytes, void* stream,
+                               int64_t* h_count, cudapre3_polyhedron_t* h_poly);
+
+/* Exact orient3d sign of float triples (host; tests and callers): sign of
+ * det[b-a; c-a; d-a].                                                       */
+int32_t cudapre3_orient(const float* a, const float* b, const float* c, const float* d);
+
 #ifdef __cplusplus
 }
 #endif

@@ -76,13 +76,39 @@ class ReportT(ctypes.Structure):
 
 EXTREMES_BYTES = ctypes.sizeof(ExtremesT)
 
+MAX_SLOTS3 = 6 * 8     # CUDAPRE3_MAX_SLOTS
+MAX_FACETS3 = 64       # CUDAPRE3_MAX_FACETS
+
+
+class Pt3(ctypes.Structure):
+    _fields_ = [("x", ctypes.c_float), ("y", ctypes.c_float), ("z", ctypes.c_float)]
+
+
+class Extremes3T(ctypes.Structure):
+    _fields_ = [("nang", ctypes.c_int32), ("nonfinite", ctypes.c_int32), ("n", ctypes.c_int64),
+                ("idx", ctypes.c_int64 * MAX_SLOTS3), ("key", ctypes.c_double * MAX_SLOTS3),
+                ("pt", Pt3 * MAX_SLOTS3), ("c", ctypes.c_double * 8), ("s", ctypes.c_double * 8),
+                ("exact_points", ctypes.c_int64)]
+
+
+class Polyhedron3T(ctypes.Structure):
+    _fields_ = [("nf", ctypes.c_int32), ("n_distinct", ctypes.c_int32), ("octants", ctypes.c_int32),
+                ("n_entries", ctypes.c_int32), ("eidx", ctypes.c_int64 * MAX_SLOTS3),
+                ("fidx", (ctypes.c_int64 * 3) * MAX_FACETS3), ("fv", (Pt3 * 3) * MAX_FACETS3),
+                ("centre", ctypes.c_float * 3), ("err_max", ctypes.c_float),
+                ("oct_count", ctypes.c_int32 * 8)]
+
+
 SYMBOLS = ["cudapre_version", "cudapre_last_error", "cudapre_angles_preset",
            "cudapre_workspace_bytes", "cudapre_workspace_init", "cudapre_extremes",
            "cudapre_extremes_merge", "cudapre_polygon", "cudapre_filter", "cudapre_hull",
            "cudapre_run_host", "cudapre_geometry", "cudapre_filter_device", "cudapre_pipeline_device",
            "cudapre_graph_create", "cudapre_graph_launch", "cudapre_graph_destroy",
            "cudapre_polygon_device", "cudapre_filter_geom", "cudapre_hull_device_bytes",
-           "cudapre_hull_device"]
+           "cudapre_hull_device",
+           # the 3D extension
+           "cudapre3_workspace_bytes", "cudapre3_orient", "cudapre3_extremes", "cudapre3_extremes_merge",
+           "cudapre3_polyhedron", "cudapre3_filter"]
 WS_GEOM_OFFSET = 4096            # include/cudapre.h CUDAPRE_WS_GEOM_OFFSET
 WS_POLY_OFFSET = 4096 + 16384    # CUDAPRE_WS_POLY_OFFSET
 WS_RESULT_OFFSET = 176           # CUDAPRE_WS_RESULT_OFFSET
@@ -125,8 +151,15 @@ def lib():
     L.cudapre_hull_device_bytes.argtypes = [i64]
     L.cudapre_hull_device_bytes.restype = sz
     L.cudapre_hull_device.argtypes = [vp, vp, i64, P(PolygonT), vp, sz, vp, vp, i64, P(i64), P(i64)]
+    L.cudapre3_workspace_bytes.argtypes = [i64]
+    L.cudapre3_workspace_bytes.restype = sz
+    L.cudapre3_orient.argtypes = [vp, vp, vp, vp]
+    L.cudapre3_extremes.argtypes = [vp, i64, i64, i32, vp, vp, vp, sz, vp, vp, P(Extremes3T)]
+    L.cudapre3_extremes_merge.argtypes = [P(Extremes3T), i32, P(Extremes3T)]
+    L.cudapre3_polyhedron.argtypes = [P(Extremes3T), P(Polyhedron3T)]
+    L.cudapre3_filter.argtypes = [vp, i64, i64, P(Extremes3T), vp, vp, i64, vp, sz, vp, P(i64), P(Polyhedron3T)]
     for name in SYMBOLS[2:]:
-        if name not in ("cudapre_workspace_bytes", "cudapre_hull_device_bytes"):
+        if name not in ("cudapre_workspace_bytes", "cudapre_hull_device_bytes", "cudapre3_workspace_bytes"):
             getattr(L, name).restype = ctypes.c_int
     _lib = L
     return L
@@ -582,3 +615,161 @@ def run_host(h_pts: np.ndarray, d_pts, d_surv_idx, h_surv_idx: np.ndarray, angle
         ctypes.c_void_p(d_surv_idx.data_ptr()), ctypes.c_void_p(hs), d_surv_idx.shape[0],
         _stream_ptr(stream), ctypes.byref(count), ctypes.byref(rep)))
     return count.value, rep
+
+
+# ====================================================================== 3D
+# The 3D extension: float32 xyz points.
+
+def _points3(pts):
+    torch = _torch()
+    if not isinstance(pts, torch.Tensor) or not pts.is_cuda:
+        raise TypeError("3D points must be a CUDA tensor of shape (n, 3), float32")
+    if pts.dtype != torch.float32 or pts.dim() != 2 or pts.shape[1] != 3 or not pts.is_contiguous():
+        raise TypeError("3D points must be a contiguous (n, 3) float32 tensor")
+    return pts
+
+
+class Workspace3:
+    """Caller-owned device workspace of the 3D path (zero-filled uint8 tensor)."""
+
+    def __init__(self, n_local: int, device=None):
+        torch = _torch()
+        self.nbytes = int(lib().cudapre3_workspace_bytes(int(n_local)))
+        self.capacity_points = int(n_local)
+        self.tensor = torch.zeros(self.nbytes, dtype=torch.uint8, device=device or "cuda")
+
+    @property
+    def ptr(self):
+        return ctypes.c_void_p(self.tensor.data_ptr())
+
+
+_ws3_cache: dict = {}
+
+
+def _workspace3(n: int, device, ws):
+    if ws is not None:
+        return ws
+    torch = _torch()
+    dev = torch.device(device)
+    key = (dev.index if dev.index is not None else torch.cuda.current_device())
+    cur = _ws3_cache.get(key)
+    if cur is None or cur.capacity_points < n:
+        cur = Workspace3(max(n, 1), device=dev)
+        _ws3_cache[key] = cur
+    return cur
+
+
+@dataclass
+class Extremes3:
+    """3D Step-1 result: slot 6k+{minX, maxX, minY, maxY, minZ, maxZ}."""
+    raw: Extremes3T
+
+    @property
+    def nang(self):
+        return self.raw.nang
+
+    @property
+    def n(self):
+        return self.raw.n
+
+    @property
+    def idx(self) -> np.ndarray:
+        return np.ctypeslib.as_array(self.raw.idx)[: 6 * self.raw.nang].copy()
+
+    @property
+    def key(self) -> np.ndarray:
+        return np.ctypeslib.as_array(self.raw.key)[: 6 * self.raw.nang].copy()
+
+    @property
+    def pt(self) -> np.ndarray:
+        a = np.frombuffer(bytes(self.raw.pt), np.float32).reshape(-1, 3)
+        return a[: 6 * self.raw.nang].copy()
+
+
+@dataclass
+class Polyhedron:
+    """3D Step-2 result: facet planes of conv(E) (E on the positive side)."""
+    raw: Polyhedron3T
+
+    @property
+    def nf(self):
+        return self.raw.nf
+
+    @property
+    def degenerate(self):
+        return self.raw.nf == 0
+
+    @property
+    def eidx(self) -> np.ndarray:
+        return np.ctypeslib.as_array(self.raw.eidx)[: self.raw.n_distinct].copy()
+
+    @property
+    def facets(self) -> np.ndarray:
+        return np.ctypeslib.as_array(self.raw.fidx).reshape(-1, 3)[: self.raw.nf].copy()
+
+
+def orient3d(a, b, c, d) -> int:
+    """Exact orient3d sign (det[b-a; c-a; d-a]) of float triples, host side."""
+    q = [np.ascontiguousarray(np.asarray(v, np.float32).reshape(3)) for v in (a, b, c, d)]
+    return int(lib().cudapre3_orient(*[v.ctypes.data_as(ctypes.c_void_p) for v in q]))
+
+
+def extremes3(pts, angles_="A", index_base: int = 0, ws=None, stream=None, device_out=None) -> Extremes3:
+    """3D Step 1 (P:115 with P:33-35) on the local shard."""
+    pts = _points3(pts)
+    n = pts.shape[0]
+    nang, c, s = _angle_arrays(angles_)
+    w = _workspace3(n, pts.device, ws)
+    out = Extremes3T()
+    _check(lib().cudapre3_extremes(
+        ctypes.c_void_p(pts.data_ptr()), n, index_base, nang,
+        c.ctypes.data_as(ctypes.c_void_p), s.ctypes.data_as(ctypes.c_void_p),
+        w.ptr, w.nbytes, _stream_ptr(stream),
+        ctypes.c_void_p(device_out.data_ptr()) if device_out is not None else None, ctypes.byref(out)))
+    return Extremes3(out)
+
+
+def merge3(parts) -> Extremes3:
+    arr = (Extremes3T * len(parts))(*[p.raw if isinstance(p, Extremes3) else p for p in parts])
+    out = Extremes3T()
+    _check(lib().cudapre3_extremes_merge(arr, len(parts), ctypes.byref(out)))
+    return Extremes3(out)
+
+
+def polyhedron3(ext: Extremes3) -> Polyhedron:
+    out = Polyhedron3T()
+    _check(lib().cudapre3_polyhedron(ctypes.byref(ext.raw), ctypes.byref(out)))
+    return Polyhedron(out)
+
+
+def filter3(pts, ext: Extremes3, index_base: int = 0, return_points: bool = True, ws=None,
+            out_idx=None, out_pts=None, stream=None):
+    """3D Steps 2+3: survivors' global indices (ascending, int64 CUDA tensor),
+    optionally their xyz, and the polyhedron used."""
+    torch = _torch()
+    pts = _points3(pts)
+    n = pts.shape[0]
+    w = _workspace3(n, pts.device, ws)
+    if out_idx is None:
+        out_idx = torch.empty(max(n, 1), dtype=torch.int64, device=pts.device)
+    if return_points and out_pts is None:
+        out_pts = torch.empty((max(n, 1), 3), dtype=torch.float32, device=pts.device)
+    cap = out_idx.shape[0]
+    if out_pts is not None:
+        cap = min(cap, out_pts.shape[0])
+    count = ctypes.c_int64()
+    poly = Polyhedron3T()
+    _check(lib().cudapre3_filter(
+        ctypes.c_void_p(pts.data_ptr()), n, index_base, ctypes.byref(ext.raw),
+        ctypes.c_void_p(out_idx.data_ptr()),
+        ctypes.c_void_p(out_pts.data_ptr()) if out_pts is not None else None,
+        cap, w.ptr, w.nbytes, _stream_ptr(stream), ctypes.byref(count), ctypes.byref(poly)))
+    m = count.value
+    return out_idx[:m], (out_pts[:m] if out_pts is not None else None), Polyhedron(poly)
+
+
+def cuda_pre3(pts, angles_="A", index_base: int = 0, return_points: bool = True, ws=None):
+    """The 3D method: Step 1, Step 2 (host), Step 3 on one GPU."""
+    ext = extremes3(pts, angles_, index_base=index_base, ws=ws)
+    idx, sp, poly = filter3(pts, ext, index_base=index_base, return_points=return_points, ws=ws)
+    return idx, sp, {"extremes": ext, "polyhedron": poly}

@@ -41,7 +41,7 @@ cudapre_status fail(cudapre_status st, const char* fmt, ...) {
 // per-thread pinned staging: [0, 4 KiB) small D2H results, [4 KiB, ...) the
 // host-built Step-3 geometry on its way to the workspace
 constexpr size_t kStageGeomOff = 4096;
-constexpr size_t kStageBytes = kStageGeomOff + sizeof(K2Geom);
+constexpr size_t kStageBytes = kStageGeomOff + kWsGeomBytes;   // either dimension's geometry page
 struct Staging {
     void* p = nullptr;
     ~Staging() {
@@ -179,6 +179,14 @@ void k2_params(K2Params& p, const cudapre_pt* d_pts, int64_t n_local, int64_t in
 }
 
 }  // namespace
+
+namespace cudapre {   // hooks for api3.cpp (the 3D ABI)
+cudapre_status api_fail(cudapre_status st, const char* msg) { return fail(st, "%s", msg); }
+cudapre_status api_staging(void** out, size_t* bytes) {
+    *bytes = kStageBytes;
+    return staging(out);
+}
+}  // namespace cudapre
 
 extern "C" {
 

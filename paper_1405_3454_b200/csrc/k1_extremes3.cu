@@ -1,0 +1,340 @@
+// k1_extremes3.cu — Step 1 of the 3D extension (PAPER.md P:115 with
+// P:33-35; DESIGN.md §3 B1-B2, §6.5) as ONE streaming pass over HBM.
+//
+// Slot 6k+{minX, maxX, minY, maxY, minZ, maxZ} of the frame rotated by angle
+// k about z: X_k = RN(RN(x c_k) + RN(y s_k)), Y_k = RN(RN(y c_k) - RN(x s_k))
+// in binary64 without FMA, Z = z; lowest index on ties.  Distinct keys: the
+// 4 angle-0 keys (x, y themselves: RN(x*1 + y*0) = x), the 2 z keys, and 4
+// per further angle.
+//
+// Per point (12 bytes, read once as part of a 48-byte quad):
+//   * angle-0 and z keys: exact float compares, strict improvement (a lane
+//     visits its points in ascending index order);
+//   * rotated keys: the same float32 screen as the 2D kernel (k1_extremes.cu
+//     header: |Xf - X_k| < m = RN32(fma(|x|+|y|, 2^-20,
+//     2^-120)); a point is a candidate for a max slot iff NOT(RN(Xf + m) <
+//     T), for a min slot iff NOT(RN(Xf - m) > T), T a float on the safe side
+//     of the exact key of a point already reduced).  Here T is the warp's
+//     best such bound (redux.sync over the lanes' exact states), refreshed
+//     whenever a lane of the warp took the exact path.  Ties are never
+//     pruned, NaN / Inf are always candidates (the exact path flags them).
+// Lane states -> warp (shuffles) -> block partial -> last-block finalize
+// (ticket) that expands the 4*nang+2 distinct keys into the 6*nang slots.
+#include <cuda_runtime.h>
+
+#include <cfloat>
+#include <cstdint>
+
+#include "internal3.h"
+
+namespace cudapre {
+namespace {
+
+constexpr unsigned kFull = 0xffffffffu;
+constexpr unsigned kNone = 0xffffffffu;
+
+__device__ __forceinline__ unsigned enc_f(float f) {
+    const unsigned b = __float_as_uint(f);
+    return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float dec_f(unsigned e) {
+    return __uint_as_float((e & 0x80000000u) ? (e & 0x7fffffffu) : ~e);
+}
+
+// (k, i) strictly better than (K, I) for the slot direction; lowest index on ties
+__device__ __forceinline__ bool lex_better(double k, unsigned i, double K, unsigned I, bool mx) {
+    return mx ? (k > K || (k == K && i < I)) : (k < K || (k == K && i < I));
+}
+
+struct Quad {
+    float v[12];   // x0 y0 z0 x1 y1 z1 ...
+};
+
+template <bool VEC>
+__device__ __forceinline__ void load_quad(const float* __restrict__ pts, unsigned q, unsigned n, Quad& Q,
+                                          unsigned& valid) {
+    const unsigned i0 = 4u * q;
+    valid = i0 >= n ? 0u : (n - i0 >= 4u ? 4u : n - i0);
+    if (VEC && valid == 4u) {
+        const float4* s = reinterpret_cast<const float4*>(pts) + 3u * q;
+        const float4 a = __ldg(s), b = __ldg(s + 1), c = __ldg(s + 2);
+        Q.v[0] = a.x, Q.v[1] = a.y, Q.v[2] = a.z, Q.v[3] = a.w;
+        Q.v[4] = b.x, Q.v[5] = b.y, Q.v[6] = b.z, Q.v[7] = b.w;
+        Q.v[8] = c.x, Q.v[9] = c.y, Q.v[10] = c.z, Q.v[11] = c.w;
+    } else {
+#pragma unroll
+        for (int j = 0; j < 12; ++j) Q.v[j] = (unsigned)(j / 3) < valid ? __ldg(pts + 3u * i0 + j) : 0.0f;
+    }
+}
+
+template <int NANG>
+struct Lane {
+    static constexpr int R = 4 * (NANG - 1);
+    static constexpr int RR = R > 0 ? R : 1;
+    float ak[6];
+    unsigned ai[6];
+    double rk[RR];
+    unsigned ri[RR];
+    float T[RR];
+};
+
+template <int NANG>
+__device__ __forceinline__ void lane_init(Lane<NANG>& L) {
+#pragma unroll
+    for (int s = 0; s < 6; ++s) {
+        L.ak[s] = (s & 1) ? -INFINITY : INFINITY;
+        L.ai[s] = kNone;
+    }
+#pragma unroll
+    for (int s = 0; s < Lane<NANG>::RR; ++s) {
+        L.rk[s] = (s & 1) ? -INFINITY : INFINITY;
+        L.ri[s] = kNone;
+        L.T[s] = (s & 1) ? -INFINITY : INFINITY;
+    }
+}
+
+// exact update of the rotated keys (cold path, one lane's candidate point)
+template <int NANG>
+__device__ __forceinline__ void exact_rot(Lane<NANG>& L, float x, float y, unsigned i, const K13Params& p,
+                                          unsigned& bad) {
+    if (!isfinite(x) || !isfinite(y)) {
+        bad = 1u;
+        return;
+    }
+    const double xd = x, yd = y;
+#pragma unroll
+    for (int k = 1; k < NANG; ++k) {
+        const double X = __dadd_rn(__dmul_rn(xd, p.c[k]), __dmul_rn(yd, p.s[k]));
+        const double Y = __dsub_rn(__dmul_rn(yd, p.c[k]), __dmul_rn(xd, p.s[k]));
+        const double kv[4] = {X, X, Y, Y};
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const int s = 4 * (k - 1) + r;
+            if ((r & 1) ? kv[r] > L.rk[s] : kv[r] < L.rk[s]) {   // ascending i: strict = lowest index
+                L.rk[s] = kv[r];
+                L.ri[s] = i;
+            }
+        }
+    }
+}
+
+template <int NANG>
+__device__ __forceinline__ void refresh(Lane<NANG>& L) {
+#pragma unroll
+    for (int s = 0; s < Lane<NANG>::R; ++s) {
+        if (s & 1) {
+            L.T[s] = dec_f(__reduce_max_sync(kFull, enc_f(__double2float_rd(L.rk[s]))));
+        } else {
+            L.T[s] = dec_f(__reduce_min_sync(kFull, enc_f(__double2float_ru(L.rk[s]))));
+        }
+    }
+}
+
+// float screen of the pair (x0, y0), (x1, y1): candidate bits (bit 0 / bit 1)
+template <int NANG>
+__device__ __forceinline__ unsigned screen_pair(const Lane<NANG>& L, float x0, float y0, float x1, float y1,
+                                                const K13Params& p) {
+    const float2 xx = make_float2(x0, x1), yy = make_float2(y0, y1);
+    const float2 ab = make_float2(__fadd_rn(fabsf(x0), fabsf(y0)), __fadd_rn(fabsf(x1), fabsf(y1)));
+    const float2 m = __ffma2_rn(ab, make_float2(0x1p-20f, 0x1p-20f), make_float2(0x1p-120f, 0x1p-120f));
+    const float2 nm = __ffma2_rn(ab, make_float2(-0x1p-20f, -0x1p-20f), make_float2(-0x1p-120f, -0x1p-120f));
+    bool c0 = false, c1 = false;
+#pragma unroll
+    for (int k = 1; k < NANG; ++k) {
+        const float2 cf = make_float2(p.cf[k], p.cf[k]);
+        const float2 X = __ffma2_rn(xx, cf, __fmul2_rn(yy, make_float2(p.sf[k], p.sf[k])));
+        const float2 Y = __ffma2_rn(yy, cf, __fmul2_rn(xx, make_float2(p.nsf[k], p.nsf[k])));
+        const float2 Xl = __fadd2_rn(X, nm), Xh = __fadd2_rn(X, m);
+        const float2 Yl = __fadd2_rn(Y, nm), Yh = __fadd2_rn(Y, m);
+        const int b = 4 * (k - 1);
+        c0 |= !(Xl.x > L.T[b + 0]) | !(Xh.x < L.T[b + 1]) | !(Yl.x > L.T[b + 2]) | !(Yh.x < L.T[b + 3]);
+        c1 |= !(Xl.y > L.T[b + 0]) | !(Xh.y < L.T[b + 1]) | !(Yl.y > L.T[b + 2]) | !(Yh.y < L.T[b + 3]);
+    }
+    return (c0 ? 1u : 0u) | (c1 ? 2u : 0u);
+}
+
+template <int NANG>
+__device__ __forceinline__ void fold_quad(Lane<NANG>& L, const Quad& Q, unsigned valid, unsigned i0,
+                                          const K13Params& p, unsigned& bad, unsigned& nexact) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        if ((unsigned)e < valid) {
+            const float x = Q.v[3 * e], y = Q.v[3 * e + 1], z = Q.v[3 * e + 2];
+            const unsigned i = i0 + e;
+            if (x < L.ak[0]) L.ak[0] = x, L.ai[0] = i;
+            if (x > L.ak[1]) L.ak[1] = x, L.ai[1] = i;
+            if (y < L.ak[2]) L.ak[2] = y, L.ai[2] = i;
+            if (y > L.ak[3]) L.ak[3] = y, L.ai[3] = i;
+            if (z < L.ak[4]) L.ak[4] = z, L.ai[4] = i;
+            if (z > L.ak[5]) L.ak[5] = z, L.ai[5] = i;
+            bad |= (fabsf(x) <= FLT_MAX && fabsf(y) <= FLT_MAX && fabsf(z) <= FLT_MAX) ? 0u : 1u;
+        }
+    }
+    if (NANG > 1) {
+        unsigned cand = screen_pair<NANG>(L, Q.v[0], Q.v[1], Q.v[3], Q.v[4], p) |
+                        (screen_pair<NANG>(L, Q.v[6], Q.v[7], Q.v[9], Q.v[10], p) << 2);
+        cand &= (1u << valid) - 1u;
+        if (__any_sync(kFull, cand != 0u)) {
+#pragma unroll 1
+            for (unsigned c = cand; c; c &= c - 1u) {
+                const int e = __ffs(c) - 1;
+                exact_rot<NANG>(L, Q.v[3 * e], Q.v[3 * e + 1], i0 + e, p, bad);
+                ++nexact;
+            }
+            refresh<NANG>(L);
+        }
+    }
+}
+
+template <int NANG, bool VEC>
+__global__ void __launch_bounds__(kK13Threads, 2) k1_extremes3(const __grid_constant__ K13Params p) {
+    constexpr int R = Lane<NANG>::R;
+    constexpr int D = 6 + R;   // distinct keys
+    __shared__ double s_key[kK13Threads / 32][D];
+    __shared__ unsigned s_idx[kK13Threads / 32][D];
+    __shared__ bool s_last;
+
+    Lane<NANG> L;
+    lane_init<NANG>(L);
+    unsigned bad = 0, nexact = 0;
+    const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    const unsigned nq = (p.n + 3u) / 4u;
+    const unsigned gwarps = gridDim.x * (kK13Threads / 32);
+    const unsigned gw = blockIdx.x * (kK13Threads / 32) + warp;
+    // warp-uniform loop: each warp takes kK13Quads*32 consecutive quads per step
+    for (unsigned qb = gw * (32u * kK13Quads); qb < nq; qb += gwarps * (32u * kK13Quads)) {
+        Quad Q[kK13Quads];
+        unsigned valid[kK13Quads];
+#pragma unroll
+        for (int u = 0; u < kK13Quads; ++u)
+            load_quad<VEC>(p.pts, qb + u * 32u + lane, p.n, Q[u], valid[u]);
+#pragma unroll
+        for (int u = 0; u < kK13Quads; ++u)
+            fold_quad<NANG>(L, Q[u], valid[u], 4u * (qb + u * 32u + lane), p, bad, nexact);
+    }
+
+    // lane -> warp (lexicographic), distinct key d: 0..5 axis, 6.. rotated
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+        double k = d < 6 ? (double)L.ak[d < 6 ? d : 0] : L.rk[d >= 6 ? d - 6 : 0];
+        unsigned i = d < 6 ? L.ai[d < 6 ? d : 0] : L.ri[d >= 6 ? d - 6 : 0];
+        const bool mx = (d & 1) != 0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double k2 = __shfl_xor_sync(kFull, k, o);
+            const unsigned i2 = __shfl_xor_sync(kFull, i, o);
+            if (i2 != kNone && (i == kNone || lex_better(k2, i2, k, i, mx))) k = k2, i = i2;
+        }
+        if (lane == 0) {
+            s_key[warp][d] = k;
+            s_idx[warp][d] = i;
+        }
+    }
+    bad = __reduce_or_sync(kFull, bad);
+    nexact = __reduce_add_sync(kFull, nexact);
+    if (lane == 0) {
+        if (bad) atomicOr(&p.ws->k1_nonfinite, 1u);
+        if (nexact) atomicAdd(&p.ws->k1_exact, nexact);
+    }
+    __syncthreads();
+    if (threadIdx.x < D) {   // warp -> block partial
+        const int d = threadIdx.x;
+        double k = s_key[0][d];
+        unsigned i = s_idx[0][d];
+        for (int w = 1; w < kK13Threads / 32; ++w)
+            if (s_idx[w][d] != kNone && (i == kNone || lex_better(s_key[w][d], s_idx[w][d], k, i, d & 1)))
+                k = s_key[w][d], i = s_idx[w][d];
+        p.partials[(size_t)blockIdx.x * kMax3Slots + d] = K13Partial{k, i, 0u};
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(&p.ws->k1_ticket, 1u) == gridDim.x - 1u;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    // last block: partials -> result (6*nang slots)
+    cudapre3_extremes_t* out = &p.ws->result;
+    if (threadIdx.x < D) {
+        const int d = threadIdx.x;
+        double k = 0.0;
+        unsigned i = kNone;
+        for (unsigned b = 0; b < gridDim.x; ++b) {
+            const K13Partial* q = &p.partials[(size_t)b * kMax3Slots + d];
+            const double qk = __ldcg(&q->key);
+            const unsigned qi = __ldcg(&q->idx);
+            if (qi != kNone && (i == kNone || lex_better(qk, qi, k, i, d & 1))) k = qk, i = qi;
+        }
+        s_idx[0][d] = i;
+    }
+    __syncthreads();
+    if (threadIdx.x < 6 * p.nang) {
+        const int slot = threadIdx.x, kk = slot / 6, r = slot % 6;
+        const int d = r >= 4 ? r : (kk == 0 ? r : 6 + 4 * (kk - 1) + r);
+        const unsigned i = s_idx[0][d];
+        if (i == kNone) {
+            out->idx[slot] = -1;
+            out->key[slot] = 0.0;
+            out->pt[slot] = cudapre_pt3{0.f, 0.f, 0.f};
+        } else {
+            const float x = p.pts[3ull * i], y = p.pts[3ull * i + 1], z = p.pts[3ull * i + 2];
+            const double xd = x, yd = y;
+            double key;
+            if (r >= 4) {
+                key = (double)z;
+            } else if (r < 2) {
+                key = __dadd_rn(__dmul_rn(xd, p.c[kk]), __dmul_rn(yd, p.s[kk]));
+            } else {
+                key = __dsub_rn(__dmul_rn(yd, p.c[kk]), __dmul_rn(xd, p.s[kk]));
+            }
+            out->idx[slot] = p.base + (long long)i;
+            out->key[slot] = key;
+            out->pt[slot] = cudapre_pt3{x, y, z};
+        }
+    }
+    if (threadIdx.x == 0) {
+        out->nang = p.nang;
+        out->nonfinite = (int)atomicExch(&p.ws->k1_nonfinite, 0u);
+        out->n = p.n;
+        out->exact_points = atomicExch(&p.ws->k1_exact, 0u);
+        p.ws->k1_ticket = 0u;
+    }
+    if (threadIdx.x < CUDAPRE_MAX_ANGLES) {
+        out->c[threadIdx.x] = threadIdx.x < (unsigned)p.nang ? p.c[threadIdx.x] : 0.0;
+        out->s[threadIdx.x] = threadIdx.x < (unsigned)p.nang ? p.s[threadIdx.x] : 0.0;
+    }
+}
+
+template <int NANG>
+int launch_n(const K13Params& p, void* stream) {
+    const unsigned nq = (p.n + 3u) / 4u;
+    const unsigned per_block = kK13Threads * kK13Quads;
+    unsigned blocks = (nq + per_block - 1) / per_block;
+    const unsigned cap = (unsigned)device_sm_count() * 2u;
+    if (blocks > cap) blocks = cap;
+    if (blocks > (unsigned)kMaxK13Blocks) blocks = kMaxK13Blocks;
+    if (blocks == 0) blocks = 1;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (p.vec)
+        k1_extremes3<NANG, true><<<blocks, kK13Threads, 0, s>>>(p);
+    else
+        k1_extremes3<NANG, false><<<blocks, kK13Threads, 0, s>>>(p);
+    return (int)cudaGetLastError();
+}
+
+}  // namespace
+
+int launch_extremes3(const K13Params& p, void* stream, int* launches) {
+    int rc;
+    switch (p.nang) {
+        case 1: rc = launch_n<1>(p, stream); break;
+        case 2: rc = launch_n<2>(p, stream); break;
+        case 3: rc = launch_n<3>(p, stream); break;
+        case 4: rc = launch_n<4>(p, stream); break;
+        case 8: rc = launch_n<8>(p, stream); break;
+        default: return (int)cudaErrorInvalidValue;
+    }
+    *launches += 1;
+    return rc;
+}
+
+}  // namespace cudapre

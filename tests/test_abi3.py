@@ -1,0 +1,118 @@
+"""Host logic of the 3D extension, no GPU: the product's exact
+orient3d (FP filter + expansion) against exact rationals, its host Step 2
+(cudapre3_polyhedron) against the oracle's facets, the shard merge, the
+struct layout, and the 3D generators' determinism."""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_1405_3454_b200 as cp
+import synth
+from tests.test_oracle3_pins import _quads, orient3d_frac
+
+
+def test_struct_sizes_match_the_header_layout():
+    # Extremes3T: 16 + 48*8 + 48*8 + 48*12 + 64 + 64 + 8; Polyhedron3T: 16 + 384 + 64*24 + 64*36 + 16 + 32
+    assert ctypes.sizeof(cp.Extremes3T) == 16 + 384 + 384 + 576 + 128 + 8
+    assert ctypes.sizeof(cp.Polyhedron3T) == 16 + 384 + 1536 + 2304 + 16 + 32
+
+
+def test_orient3d_exact_vs_fractions():
+    rng = np.random.default_rng(77)
+    zeros = 0
+    for a, b, c, d in _quads(rng, 4000):
+        want = orient3d_frac(a, b, c, d)
+        zeros += want == 0
+        assert cp.orient3d(a, b, c, d) == want, (a, b, c, d)
+        assert cp.orient3d(a, c, b, d) == -want
+    assert zeros > 50
+
+
+def test_orient3d_filter_boundary_cases():
+    """Cases the binary64 filter cannot decide go through the expansion:
+    exact zeros far from the origin, huge and tiny magnitudes."""
+    big, tiny = np.float32(3e38), np.float32(2 ** -149)
+    o = np.zeros(3, np.float32)
+    cases = [
+        (o, [big, 0, 0], [0, big, 0], [0, 0, big]),
+        (o, [tiny, 0, 0], [0, tiny, 0], [0, 0, tiny]),
+        ([-big, tiny, 1], [big, -big, tiny], [tiny, big, -big], [1, tiny, big]),
+    ]
+    a = np.full(3, 2 ** 20, np.float32)
+    for k in range(200):   # points exactly on / next to the plane x + y + z = 3 * 2^20 + ...
+        e = np.float32(2 ** -3) * (k % 5 - 2)
+        cases.append((a, a + np.float32([1, 0, 0]), a + np.float32([0, 1, 0]), a + np.float32([e, e, 0])))
+    for q in cases:
+        assert cp.orient3d(*q) == orient3d_frac(*q)
+
+
+def _ext3_from_oracle(xyz, angles):
+    """A cudapre3_extremes_t filled from the oracle's Step 1 (host only)."""
+    idx, key = oracle.extremes3(xyz, angles, with_keys=True)
+    c, s = oracle.coeffs(angles)
+    r = cp.Extremes3T()
+    r.nang = len(c)
+    r.n = len(xyz)
+    for j in range(cp.MAX_SLOTS3):
+        r.idx[j] = -1
+    for j, (i, k) in enumerate(zip(idx, key)):
+        r.idx[j] = int(i)
+        r.key[j] = float(k)
+        r.pt[j] = cp.Pt3(*[float(v) for v in xyz[i]])
+    for k in range(len(c)):
+        r.c[k], r.s[k] = c[k], s[k]
+    return cp.Extremes3(r)
+
+
+@pytest.mark.parametrize("family", ["cube", "ball", "sphere"])
+@pytest.mark.parametrize("angles", ["A", "AT", "C", "D"])
+def test_host_polyhedron_matches_oracle_facets(family, angles):
+    xyz = synth.generate3(family, 20_000, seed=3)
+    ext = _ext3_from_oracle(xyz, angles)
+    poly = cp.polyhedron3(ext)
+    E = oracle.distinct3(xyz, ext.idx)
+    assert poly.eidx.tolist() == E.tolist()
+    assert poly.facets.tolist() == oracle.facets3(xyz, E).tolist()
+    assert poly.nf >= 4
+    assert poly.raw.octants == 1
+    assert poly.raw.n_entries >= poly.nf       # every facet meets some octant
+
+
+def test_host_polyhedron_degenerate_and_ties():
+    flat = np.c_[synth.generate("disk", 3000, seed=2), np.zeros(3000)].astype(np.float32)
+    poly = cp.polyhedron3(_ext3_from_oracle(flat, "A"))
+    assert poly.degenerate and poly.nf == 0
+    lattice = np.random.default_rng(1).integers(-2, 3, (5000, 3)).astype(np.float32)   # coplanar faces, ties
+    ext = _ext3_from_oracle(lattice, "A")
+    poly = cp.polyhedron3(ext)
+    E = oracle.distinct3(lattice, ext.idx)
+    assert poly.facets.tolist() == oracle.facets3(lattice, E).tolist()
+
+
+def test_merge3_equals_unsharded_oracle():
+    xyz = np.round(synth.generate3("ball", 30_001, seed=4) * 16).astype(np.float32)   # heavy ties
+    whole = oracle.extremes3(xyz, "A")
+    parts = []
+    bounds = [0, 7_000, 7_001, 19_000, 30_001]
+    for lo, hi in zip(bounds[:-1], bounds[1:]):
+        e = _ext3_from_oracle(xyz[lo:hi], "A")
+        for j in range(24):
+            e.raw.idx[j] += lo
+        parts.append(e)
+    m = cp.merge3(parts)
+    assert m.idx.tolist() == whole.tolist()
+    assert m.n == len(xyz)
+
+
+def test_generate3_is_deterministic_and_sliceable():
+    a = synth.generate3("sphere", 5000, seed=9)
+    b = synth.generate3("sphere", 2000, seed=9, base=3000)
+    assert np.array_equal(a[3000:], b)
+    r = np.sqrt((a.astype(np.float64) ** 2).sum(1))
+    assert (r <= 1.0 + 1e-6).all() and (r >= 1 - 1e-3 - 1e-6).all()
+    c = synth.generate3("ball", 5000, seed=9)
+    assert ((c.astype(np.float64) ** 2).sum(1) <= 1.0 + 1e-6).all()

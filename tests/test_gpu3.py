@@ -1,0 +1,135 @@
+"""GPU parity of the 3D extension: K1-3D picks, the
+host polyhedron and K2-3D survivors must equal the oracle's exactly, at
+sizes that span many tiles with ragged tails, for aligned and misaligned
+inputs, ties, degenerate and extreme-magnitude inputs; at large sizes the
+picks are compared exactly and the classification on a sample."""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_1405_3454_b200 as cp
+import synth
+import synth.cuda
+
+pytestmark = pytest.mark.gpu
+
+THREADS = max(1, min(64, os.cpu_count() or 1))
+
+
+def _run(xyz, angles="A", index_base=0, view_offset=0):
+    if view_offset:
+        full = torch.from_numpy(np.ascontiguousarray(np.concatenate([np.zeros((view_offset, 3), np.float32),
+                                                                       xyz]))).cuda()
+        pts = full[view_offset:]
+    else:
+        pts = torch.from_numpy(np.ascontiguousarray(xyz)).cuda()
+    ext = cp.extremes3(pts, angles, index_base=index_base)
+    idx, sp, poly = cp.filter3(pts, ext, index_base=index_base)
+    torch.cuda.synchronize()
+    return ext, idx.cpu().numpy(), sp.cpu().numpy(), poly
+
+
+def _check(xyz, angles="A", **kw):
+    ext, idx, sp, poly = _run(xyz, angles, **kw)
+    base = kw.get("index_base", 0)
+    want = oracle.cudapre3(xyz, angles, threads=THREADS)
+    assert (ext.idx - base).tolist() == want["ext_idx"].tolist()
+    assert (poly.facets - base).tolist() == want["facets"].tolist()
+    assert np.array_equal(idx - base, want["survivors"])
+    assert np.array_equal(sp, xyz[want["survivors"]])
+    return ext, idx, poly
+
+
+@pytest.mark.parametrize("family", ["cube", "ball", "sphere"])
+@pytest.mark.parametrize("angles", ["A", "AT", "C", "D"])
+@pytest.mark.parametrize("n", [5, 1_001, 300_007])
+def test_parity_families_angles_sizes(family, angles, n):
+    _check(synth.generate3(family, n, seed=n % 53 + 1), angles)
+
+
+@pytest.mark.parametrize("n", [2_000_003, 4_194_305])
+def test_parity_many_tiles(n):
+    _check(synth.generate3("ball", n, seed=7))
+
+
+def test_misaligned_and_index_base():
+    xyz = synth.generate3("cube", 500_001, seed=2)
+    _check(xyz, view_offset=1)                 # 12-byte offset: scalar loads
+    _check(xyz, index_base=123_456_789_012)
+
+
+def test_ties_lattice_duplicates_offsets():
+    rng = np.random.default_rng(8)
+    cases = [
+        rng.integers(-3, 4, (200_001, 3)).astype(np.float32),                       # coplanar faces, ties
+        np.round(synth.generate3("ball", 300_001, seed=1) * 16).astype(np.float32),  # heavy ties
+        (synth.generate3("ball", 200_001, seed=3) + np.float32(1e4)).astype(np.float32),   # large offset
+        (synth.generate3("cube", 100_001, seed=4).astype(np.float64) * 1e-30).astype(np.float32),
+        (synth.generate3("cube", 100_001, seed=5).astype(np.float64) * 1e30).astype(np.float32),
+        np.tile(np.float32([[0.5, -0.25, 2.0]]), (70_001, 1)),                       # one distinct point
+    ]
+    for xyz in cases:
+        _check(xyz)
+
+
+def test_degenerate_coplanar_keeps_everything():
+    xy = synth.generate("disk", 100_003, seed=6)
+    xyz = np.c_[xy, np.float32(0.5) * xy[:, 0]].astype(np.float32)   # exactly on the plane z = x / 2
+    ext, idx, poly = _check(xyz)
+    assert poly.degenerate and len(idx) == len(xyz)
+
+
+def test_errors():
+    with pytest.raises(cp.CudaPreError) as e:
+        cp.extremes3(torch.empty((0, 3), device="cuda"))
+    assert e.value.status == cp.ERR_EMPTY
+    xyz = synth.generate3("ball", 10_000, seed=1)
+    xyz[777, 2] = np.nan
+    with pytest.raises(cp.CudaPreError) as e:
+        cp.extremes3(torch.from_numpy(xyz).cuda())
+    assert e.value.status == cp.ERR_NONFINITE
+
+
+def test_workspace_reuse_across_sizes():
+    ws = cp.Workspace3(3_000_000)
+    for n, seed in ((3_000_000, 1), (10_001, 2), (2_500_000, 3), (1, 4), (3_000_000, 5)):
+        xyz = synth.generate3("ball", n, seed=seed)
+        pts = torch.from_numpy(xyz).cuda()
+        ext = cp.extremes3(pts, "A", ws=ws)
+        idx, _, _ = cp.filter3(pts, ext, ws=ws, return_points=False)
+        want = oracle.cudapre3(xyz, "A", threads=THREADS)
+        assert np.array_equal(idx.cpu().numpy(), want["survivors"])
+
+
+def test_cuda_generator_matches_numpy():
+    for fam in synth.FAMILIES3:
+        a = synth.cuda.generate3(fam, 300_001, seed=11, base=5).cpu().numpy()
+        b = synth.generate3(fam, 300_001, seed=11, base=5)
+        assert np.array_equal(a.view(np.uint32), b.view(np.uint32)), fam
+
+
+def test_large_sampled():
+    """Bench-scale input generated on the device: picks equal the oracle's
+    exactly; survivors ascend; the classification of 50k sampled points
+    equals the oracle's against the oracle's own polyhedron."""
+    n = 200_000_000
+    pts = synth.cuda.generate3("ball", n, seed=23)
+    ext = cp.extremes3(pts, "A")
+    idx, _, poly = cp.filter3(pts, ext, return_points=False)
+    torch.cuda.synchronize()
+    host = pts.cpu().numpy()
+    want_ext = oracle.extremes3(host, "A", threads=THREADS)
+    assert ext.idx.tolist() == want_ext.tolist()
+    E = oracle.distinct3(host, want_ext)
+    F = oracle.facets3(host, E)
+    assert poly.facets.tolist() == F.tolist()
+    got = idx.cpu().numpy()
+    assert np.all(np.diff(got) > 0)
+    rng = np.random.default_rng(0)
+    sample = np.sort(rng.choice(n, 50_000, replace=False))
+    keep = oracle.filter_mask3(host[sample], host[F], threads=THREADS)
+    assert np.array_equal(np.isin(sample, got), keep)
+    del host
