@@ -384,14 +384,16 @@ typedef struct {
 typedef struct {
     int32_t nf;                                 /* facet planes, 0 = degenerate */
     int32_t n_distinct;                         /* |E| */
-    int32_t octants;                            /* 1: per-octant candidate lists around centre */
-    int32_t n_entries;                          /* candidate entries over the 8 octants */
+    int32_t cells;                              /* 1: per-direction-cell candidate lists around centre */
+    int32_t n_entries;                          /* candidate facets summed over the 384 cells */
     int64_t eidx[CUDAPRE3_MAX_SLOTS];           /* E (global ids, ascending) */
     int64_t fidx[CUDAPRE3_MAX_FACETS][3];       /* supporting triple of each facet plane */
     cudapre_pt3 fv[CUDAPRE3_MAX_FACETS][3];     /* its coordinates */
-    float centre[3];                            /* strictly inside (octants == 1) */
+    float centre[3];                            /* strictly inside (cells == 1) */
     float err_max;                              /* largest plane-test error bound */
-    int32_t oct_count[8];                       /* candidate facets per octant */
+    int32_t max_candidates;                     /* largest candidate list of a cell */
+    int32_t long_cells;                         /* cells whose list exceeds the kernel's 3 slots */
+    int32_t pad[6];
 } cudapre3_polyhedron_t;
 
 /* Workspace bytes for a shard of n_local points (3D). */

@@ -92,11 +92,11 @@ class Extremes3T(ctypes.Structure):
 
 
 class Polyhedron3T(ctypes.Structure):
-    _fields_ = [("nf", ctypes.c_int32), ("n_distinct", ctypes.c_int32), ("octants", ctypes.c_int32),
+    _fields_ = [("nf", ctypes.c_int32), ("n_distinct", ctypes.c_int32), ("cells", ctypes.c_int32),
                 ("n_entries", ctypes.c_int32), ("eidx", ctypes.c_int64 * MAX_SLOTS3),
                 ("fidx", (ctypes.c_int64 * 3) * MAX_FACETS3), ("fv", (Pt3 * 3) * MAX_FACETS3),
                 ("centre", ctypes.c_float * 3), ("err_max", ctypes.c_float),
-                ("oct_count", ctypes.c_int32 * 8)]
+                ("max_candidates", ctypes.c_int32), ("long_cells", ctypes.c_int32), ("pad", ctypes.c_int32 * 6)]
 
 
 SYMBOLS = ["cudapre_version", "cudapre_last_error", "cudapre_angles_preset",

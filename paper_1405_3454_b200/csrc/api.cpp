@@ -41,7 +41,7 @@ cudapre_status fail(cudapre_status st, const char* fmt, ...) {
 // per-thread pinned staging: [0, 4 KiB) small D2H results, [4 KiB, ...) the
 // host-built Step-3 geometry on its way to the workspace
 constexpr size_t kStageGeomOff = 4096;
-constexpr size_t kStageBytes = kStageGeomOff + kWsGeomBytes;   // either dimension's geometry page
+constexpr size_t kStageBytes = kStageGeomOff + 65536;   // either dimension's geometry page (2D 32 KiB, 3D 64 KiB)
 struct Staging {
     void* p = nullptr;
     ~Staging() {

@@ -24,35 +24,105 @@ struct P3 {
     int64_t id;
 };
 
-// Does the triangle (a, b, c) (coordinates relative to the centre) meet the
-// closed octant {sigma_i x_i >= -tau}?  Sutherland-Hodgman clip by the three
-// half-spaces; conservative by tau (never misses a true intersection).
-bool tri_meets_octant(const double* a, const double* b, const double* c, int oct, double tau) {
-    double poly[16][3], tmp[16][3];
-    int n = 3;
-    for (int k = 0; k < 3; ++k) poly[0][k] = a[k], poly[1][k] = b[k], poly[2][k] = c[k];
-    for (int ax = 0; ax < 3 && n > 0; ++ax) {
-        const double sg = ((oct >> ax) & 1) ? -1.0 : 1.0;   // bit set: x_ax < centre
-        int m = 0;
-        for (int i = 0; i < n; ++i) {
-            const double* P = poly[i];
-            const double* Q = poly[(i + 1) % n];
-            const double dp = sg * P[ax] + tau, dq = sg * Q[ax] + tau;
-            if (dp >= 0) {
-                for (int k = 0; k < 3; ++k) tmp[m][k] = P[k];
-                ++m;
-            }
-            if ((dp >= 0) != (dq >= 0)) {
-                const double t = dp / (dp - dq);
-                for (int k = 0; k < 3; ++k) tmp[m][k] = P[k] + t * (Q[k] - P[k]);
-                ++m;
-            }
+// Clip the convex polygon poly[0..n) (in place) by the half-space
+// h[0] x + h[1] y + h[2] z + h[3] >= 0.  Returns the new vertex count.
+int clip(double (*poly)[3], int n, const double* h) {
+    double out[24][3];
+    int m = 0;
+    for (int i = 0; i < n && m < 22; ++i) {
+        const double* P = poly[i];
+        const double* Q = poly[(i + 1) % n];
+        const double dp = h[0] * P[0] + h[1] * P[1] + h[2] * P[2] + h[3];
+        const double dq = h[0] * Q[0] + h[1] * Q[1] + h[2] * Q[2] + h[3];
+        if (dp >= 0) {
+            for (int k = 0; k < 3; ++k) out[m][k] = P[k];
+            ++m;
         }
-        n = m;
-        for (int i = 0; i < n; ++i)
-            for (int k = 0; k < 3; ++k) poly[i][k] = tmp[i][k];
+        if ((dp >= 0) != (dq >= 0)) {
+            const double t = dp / (dp - dq);
+            for (int k = 0; k < 3; ++k) out[m][k] = P[k] + t * (Q[k] - P[k]);
+            ++m;
+        }
     }
-    return n > 0;
+    for (int i = 0; i < m; ++i)
+        for (int k = 0; k < 3; ++k) poly[i][k] = out[i][k];
+    return m;
+}
+
+// Mark in cmask every direction cell that the triangle (A, B, C) (relative to
+// the centre) may be seen through: per cube face (axis a, sign s) clip it to
+// the face's pyramid widened by the guard, project the rest centrally to
+// (u, v) = (d_b, d_c) / (s d_a) — the projection of a convex polygon in
+// front of the centre is convex — and mark every cell whose rectangle,
+// widened by the guard (the border cells unbounded outwards: the kernel
+// clamps), meets it.  The guard covers the kernel's rounding of the cell
+// index; clipping is done in binary64, far below the guard.
+void mark_cells(const double* A, const double* B, const double* C, double tau, int bit, unsigned long long* cmask) {
+    static const int U[3] = {1, 2, 0}, V[3] = {2, 0, 1};
+    const double w = 1.0 + 4 * kCellGuard;
+    for (int a = 0; a < 3; ++a)
+        for (int sg = 0; sg < 2; ++sg) {
+            const double s = sg ? -1.0 : 1.0;
+            double poly[24][3];
+            for (int k = 0; k < 3; ++k) poly[0][k] = A[k], poly[1][k] = B[k], poly[2][k] = C[k];
+            int n = 3;
+            double h[4];
+            // s d_a >= 0;  w s d_a -+ d_u >= 0;  w s d_a -+ d_v >= 0   (each relaxed by tau)
+            h[0] = h[1] = h[2] = 0;
+            h[a] = s;
+            h[3] = tau;
+            n = clip(poly, n, h);
+            for (int t = 0; t < 4 && n > 0; ++t) {
+                const int c = (t < 2) ? U[a] : V[a];
+                h[0] = h[1] = h[2] = 0;
+                h[a] = w * s;
+                h[c] = (t & 1) ? 1.0 : -1.0;
+                h[3] = tau;
+                n = clip(poly, n, h);
+            }
+            if (n == 0) continue;
+            double ulo = 1e300, uhi = -1e300, vlo = 1e300, vhi = -1e300;
+            double uv[24][2];
+            bool far = false;
+            for (int i = 0; i < n; ++i) {
+                const double m = s * poly[i][a];
+                if (!(m > tau)) {   // at the apex: the polygon reaches the centre's neighbourhood
+                    far = true;
+                    break;
+                }
+                uv[i][0] = poly[i][U[a]] / m, uv[i][1] = poly[i][V[a]] / m;
+                ulo = std::min(ulo, uv[i][0]), uhi = std::max(uhi, uv[i][0]);
+                vlo = std::min(vlo, uv[i][1]), vhi = std::max(vhi, uv[i][1]);
+            }
+            const int face = 2 * a + sg;
+            auto cell_of = [](double x) {
+                const double f = std::floor((x + 1.0) * (kCellG / 2.0));
+                return (int)std::min<double>(kCellG - 1, std::max<double>(0.0, f));
+            };
+            if (far) {
+                for (int c = 0; c < kCellG * kCellG; ++c) cmask[face * kCellG * kCellG + c] |= 1ull << bit;
+                continue;
+            }
+            const int iu0 = cell_of(ulo - kCellGuard), iu1 = cell_of(uhi + kCellGuard);
+            for (int iu = iu0; iu <= iu1; ++iu) {
+                // the polygon within this row's u-strip (widened by the guard; the
+                // border rows unbounded outwards: the kernel clamps) is convex, so
+                // its v-extent is exactly the v-range of the row's cells it meets
+                const double cu0 = iu == 0 ? -1e300 : -1.0 + 2.0 * iu / kCellG - kCellGuard;
+                const double cu1 = iu == kCellG - 1 ? 1e300 : -1.0 + 2.0 * (iu + 1) / kCellG + kCellGuard;
+                double q[24][3];
+                for (int i = 0; i < n; ++i) q[i][0] = uv[i][0], q[i][1] = uv[i][1], q[i][2] = 0.0;
+                int k = n;
+                const double h0[4] = {1, 0, 0, -cu0}, h1[4] = {-1, 0, 0, cu1};
+                if (iu != 0) k = clip(q, k, h0);
+                if (k > 0 && iu != kCellG - 1) k = clip(q, k, h1);
+                if (k == 0) continue;
+                double v0 = 1e300, v1 = -1e300;
+                for (int i = 0; i < k; ++i) v0 = std::min(v0, q[i][1]), v1 = std::max(v1, q[i][1]);
+                const int iv0 = cell_of(v0 - kCellGuard), iv1 = cell_of(v1 + kCellGuard);
+                for (int iv = iv0; iv <= iv1; ++iv) cmask[(face * kCellG + iu) * kCellG + iv] |= 1ull << bit;
+            }
+    }
 }
 
 }  // namespace
@@ -159,7 +229,7 @@ int build_polyhedron3(const cudapre3_extremes_t& ext, cudapre3_polyhedron_t* pol
     }
     P.err_max = emax;
 
-    // centre: mean of E, rounded to float; octant lists only if it is
+    // centre: mean of E, rounded to float; direction cells only if it is
     // strictly inside every facet (exact check)
     double cx = 0, cy = 0, cz = 0;
     for (const P3& e : E) cx += e.v[0], cy += e.v[1], cz += e.v[2];
@@ -168,62 +238,69 @@ int build_polyhedron3(const cudapre3_extremes_t& ext, cudapre3_polyhedron_t* pol
     for (int f = 0; f < nf && inside; ++f)
         inside = orient3d_sign_f(E[F[f][0]].v, E[F[f][1]].v, E[F[f][2]].v, o) > 0;
     g->ox = o[0], g->oy = o[1], g->oz = o[2];
-    g->octants = inside ? 1 : 0;
-    P.octants = g->octants;
+    g->cells = inside ? 1 : 0;
+    P.cells = g->cells;
     P.centre[0] = o[0], P.centre[1] = o[1], P.centre[2] = o[2];
-
-    int nent = 0;
+    g->all = nf == 64 ? ~0ull : ((1ull << nf) - 1ull);
+    std::vector<unsigned long long> cmask(kCells, 0ull);
+    for (int f = 0; f < nf; ++f) {
+        g->pl[f] = pl[f];
+        g->pe[f] = pe[f];
+    }
     if (!inside) {
-        for (int f = 0; f < nf; ++f) {
-            g->pl[nent] = pl[f];
-            g->pe[nent] = pe[f];
-            g->pf[nent] = (unsigned char)f;
-            ++nent;
-        }
-        g->oct_start[0] = 0;
-        for (int k = 1; k <= 8; ++k) g->oct_start[k] = nent;
-        for (int k = 0; k < 8; ++k) P.oct_count[k] = nf;
+        for (int c = 0; c < kCells; ++c) cmask[c] = g->all;
     } else {
-        // face of facet f = conv(points of E on its plane) = union of the
+        // face of facet f = conv(points of E on its plane) = the union of the
         // triangles of those points; relative to the centre, in binary64
-        std::vector<std::vector<int>> on(nf);
         double ext_max = 0;
         for (const P3& e : E)
             for (int k = 0; k < 3; ++k) ext_max = std::max(ext_max, std::fabs((double)e.v[k] - o[k]));
         const double tau = ext_max * 0x1p-30 + 0x1p-140;
-        for (int f = 0; f < nf; ++f)
+        for (int f = 0; f < nf; ++f) {
+            std::vector<int> on;
             for (int j = 0; j < m; ++j)
                 if (j == F[f][0] || j == F[f][1] || j == F[f][2] ||
                     orient3d_sign_f(E[F[f][0]].v, E[F[f][1]].v, E[F[f][2]].v, E[j].v) == 0)
-                    on[f].push_back(j);
-        for (int oct = 0; oct < 8; ++oct) {
-            g->oct_start[oct] = nent;
-            for (int f = 0; f < nf; ++f) {
-                bool meets = false;
-                const std::vector<int>& V = on[f];
-                for (size_t i = 0; i < V.size() && !meets; ++i)
-                    for (size_t j = i + 1; j < V.size() && !meets; ++j)
-                        for (size_t k = j + 1; k < V.size() && !meets; ++k) {
-                            double A[3], B[3], C[3];
-                            for (int c = 0; c < 3; ++c) {
-                                A[c] = (double)E[V[i]].v[c] - o[c];
-                                B[c] = (double)E[V[j]].v[c] - o[c];
-                                C[c] = (double)E[V[k]].v[c] - o[c];
-                            }
-                            meets = tri_meets_octant(A, B, C, oct, tau);
+                    on.push_back(j);
+            for (size_t i = 0; i < on.size(); ++i)
+                for (size_t j = i + 1; j < on.size(); ++j)
+                    for (size_t k = j + 1; k < on.size(); ++k) {
+                        double A[3], B[3], C[3];
+                        for (int c = 0; c < 3; ++c) {
+                            A[c] = (double)E[on[i]].v[c] - o[c];
+                            B[c] = (double)E[on[j]].v[c] - o[c];
+                            C[c] = (double)E[on[k]].v[c] - o[c];
                         }
-                if (!meets) continue;
-                g->pl[nent] = pl[f];
-                g->pe[nent] = pe[f];
-                g->pf[nent] = (unsigned char)f;
-                ++nent;
-            }
-            P.oct_count[oct] = nent - g->oct_start[oct];
+                        mark_cells(A, B, C, tau, f, cmask.data());
+                    }
         }
-        g->oct_start[8] = nent;
     }
-    g->nent = nent;
+    g->pl[kDummyFacet] = make_float4(0.f, 0.f, 0.f, 1.f);
+    g->pe[kDummyFacet] = 0.f;
+    int nent = 0, mx = 0, nlong = 0;
+    for (int c = 0; c < kCells; ++c) {
+        const int k = __builtin_popcountll(cmask[c]);
+        nent += k;
+        mx = std::max(mx, k);
+        unsigned w = (unsigned)std::min(k, 255) << 24;
+        if (k > kCellSlots) {   // long list: its mask (or every facet once lmask is full)
+            ++P.long_cells;
+            if (nlong < kMaxLong) {
+                g->lmask[nlong] = cmask[c];
+                w |= (unsigned)nlong++;
+            } else {
+                w |= kNoLong;
+            }
+        } else {
+            int slot = 0;
+            for (unsigned long long b = cmask[c]; b; b &= b - 1, ++slot)
+                w |= (unsigned)__builtin_ctzll(b) << (8 * slot);
+            for (; slot < kCellSlots; ++slot) w |= (unsigned)kDummyFacet << (8 * slot);
+        }
+        g->clist[c] = w;
+    }
     P.n_entries = nent;
+    P.max_candidates = mx;
     if (poly) *poly = P;
     return 0;
 }

@@ -13,7 +13,6 @@ namespace cudapre {
 
 constexpr int kMax3Slots = CUDAPRE3_MAX_SLOTS;     // 6 per angle
 constexpr int kMax3Facets = CUDAPRE3_MAX_FACETS;   // facet planes of conv(<= 34 points)
-constexpr int kMax3Entries = 8 * kMax3Facets;      // octant candidate lists, all octants
 
 // ---------------------------------------------------------------- launch shape
 constexpr int kK13Threads = 256;              // K1-3D block
@@ -22,7 +21,7 @@ constexpr int kMaxK13Blocks = 148 * 8;
 constexpr int kK23Threads = 256;              // K2-3D block
 constexpr int kK23TileQuads = 2 * kK23Threads;              // 512 quads
 constexpr int kK23TilePts = 4 * kK23TileQuads;              // 2048 points (24 KiB) per tile
-constexpr int kK23BlocksPerSM = 4;
+constexpr int kK23BlocksPerSM = 3;
 constexpr int kStatus3Stride = 16;            // one 8-byte status word per 128-byte line
 
 // ---------------------------------------------------------------- workspace
@@ -42,7 +41,7 @@ struct alignas(16) Ws3Header {
 };
 static_assert(sizeof(Ws3Header) <= 4096, "3D header too large");
 constexpr size_t kWs3HeaderBytes = 4096;
-constexpr size_t kWs3GeomBytes = 32768;
+constexpr size_t kWs3GeomBytes = 65536;
 
 struct K13Partial {
     double key;
@@ -58,22 +57,41 @@ inline size_t ws3_bytes_for(int64_t n) {
 }
 
 // Step-3 geometry (host-built, copied to the geometry page; K2-3D stages it
-// in shared memory).  Octant o of a point p is (p.x < ox) | (p.y < oy) << 1 |
-// (p.z < oz) << 2 (exact float compares); its candidate facets are entries
-// [oct_start[o], oct_start[o+1]).  Entry t: plane test g = fma(A, x, fma(B,
-// y, fma(C, z, D))) with |g - orient3d(facet, p)| <= E over the data bounding
-// box; fid = the facet, whose supporting triple fv[fid] decides exactly.
+// in shared memory).  Direction cells around the centre o (strictly inside):
+// d = RN(p - o); the major axis a of |d| (ties: x before y before z) and its
+// sign give the cube face f = 2a + (d_a < 0); with (u, v) the two other
+// components in the order (y, z), (z, x), (x, y) for a = x, y, z, the cell is
+// (f, iu, iv), iu = clamp(floor((u / |d_a| + 1) G / 2), 0, G - 1) (same for
+// v), computed with one approximate reciprocal.  The candidates of a cell are
+// the facets whose face meets the cell's direction pyramid widened by
+// kCellGuard; clist[cell] holds up to kCellSlots of them as
+// bytes (unused: kDummyFacet, whose plane test always says "inside") and the
+// count in the top byte; a longer list (count > kCellSlots) keeps in its low
+// bits an index into lmask[] (the candidate mask), or kNoLong = every facet.  Facet
+// j: plane test g = fma(A, x, fma(B, y, fma(C, z, D))) with |g -
+// orient3d(facet, p)| <= E over the data bounding box; fv[j] its supporting
+// triple for the exact decision.
+constexpr int kCellG = 32;                      // cells per cube-face side
+constexpr int kCells = 6 * kCellG * kCellG;     // 6144
+constexpr int kMaxLong = 1024;                  // long lists with their own mask
+constexpr unsigned kNoLong = 0xffffffu;
+constexpr int kCellSlots = 3;
+constexpr int kDummyFacet = kMax3Facets;        // plane (0, 0, 0, 1), E = 0
+constexpr double kCellGuard = 0x1p-12;          // widening of every cell, in (u, v) units
+
 struct alignas(16) K3Geom {
     int nf;          // facet planes
     int mode;        // 0 = filter, 1 = keep everything (degenerate polyhedron)
-    int nent;        // candidate entries (sum over octants)
-    int octants;     // 1 if the centre is strictly inside (lists per octant), 0 = every list = all facets
-    float ox, oy, oz, pad;
-    int oct_start[12];
-    float4 pl[kMax3Entries];          // (A, B, C, D)
-    float pe[kMax3Entries];           // E
-    unsigned char pf[kMax3Entries];   // facet id
-    float fv[kMax3Facets][9];         // facet triple coordinates (a, b, c)
+    int cells;       // 1 if the centre is strictly inside (cell lists), 0 = every cell = all facets
+    int pad0;
+    float ox, oy, oz, pad1;
+    unsigned long long all;                // mask of every facet
+    unsigned long long pad2;
+    unsigned clist[kCells];                // candidate lists (bytes) + count
+    unsigned long long lmask[kMaxLong];    // candidate masks of long lists
+    float4 pl[kMax3Facets + 1];            // (A, B, C, D); [kDummyFacet] = (0, 0, 0, 1)
+    float pe[kMax3Facets + 1];             // E; [kDummyFacet] = 0
+    float fv[kMax3Facets][9];              // facet triple coordinates (a, b, c)
 };
 static_assert(sizeof(K3Geom) <= kWs3GeomBytes, "3D geometry page");
 

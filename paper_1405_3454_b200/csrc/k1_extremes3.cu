@@ -10,14 +10,14 @@
 // Per point (12 bytes, read once as part of a 48-byte quad):
 //   * angle-0 and z keys: exact float compares, strict improvement (a lane
 //     visits its points in ascending index order);
-//   * rotated keys: the same float32 screen as the 2D kernel (k1_extremes.cu
-//     header: |Xf - X_k| < m = RN32(fma(|x|+|y|, 2^-20,
-//     2^-120)); a point is a candidate for a max slot iff NOT(RN(Xf + m) <
-//     T), for a min slot iff NOT(RN(Xf - m) > T), T a float on the safe side
-//     of the exact key of a point already reduced).  Here T is the warp's
-//     best such bound (redux.sync over the lanes' exact states), refreshed
-//     whenever a lane of the warp took the exact path.  Ties are never
-//     pruned, NaN / Inf are always candidates (the exact path flags them).
+//   * every key is screened against the warp's threshold T (a float on the
+//     safe side of the exact key of a point already reduced: redux.sync over
+//     the lanes' exact states, refreshed whenever a lane took the exact path);
+//     axis keys exactly (x, y, z are the keys), rotated keys with the 2D
+//     kernel's margin (k1_extremes.cu header: |Xf - X_k| <
+//     m = RN32(fma(|x|+|y|, 2^-20, 2^-120))), here the quad's largest m
+//     folded into the thresholds once per quad.  Ties are never pruned,
+//     NaN / Inf are always candidates (the exact path flags them).
 // Lane states -> warp (shuffles) -> block partial -> last-block finalize
 // (ticket) that expands the 4*nang+2 distinct keys into the 6*nang slots.
 #include <cuda_runtime.h>
@@ -46,6 +46,11 @@ __device__ __forceinline__ bool lex_better(double k, unsigned i, double K, unsig
     return mx ? (k > K || (k == K && i < I)) : (k < K || (k == K && i < I));
 }
 
+// L2 prefetch of [p, p + bytes) (cp.async.bulk.prefetch; 16-B aligned, bytes % 16 == 0)
+__device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
 struct Quad {
     float v[12];   // x0 y0 z0 x1 y1 z1 ...
 };
@@ -64,6 +69,10 @@ __device__ __forceinline__ void load_quad(const float* __restrict__ pts, unsigne
     } else {
 #pragma unroll
         for (int j = 0; j < 12; ++j) Q.v[j] = (unsigned)(j / 3) < valid ? __ldg(pts + 3u * i0 + j) : 0.0f;
+        if (valid > 0u)   // pad the tail with copies of the quad's first point (no effect on any key)
+#pragma unroll
+            for (int j = 3; j < 12; ++j)
+                if ((unsigned)(j / 3) >= valid) Q.v[j] = Q.v[j % 3];
     }
 }
 
@@ -71,11 +80,12 @@ template <int NANG>
 struct Lane {
     static constexpr int R = 4 * (NANG - 1);
     static constexpr int RR = R > 0 ? R : 1;
-    float ak[6];
+    static constexpr int D = 6 + R;   // distinct keys: x, x, y, y, z, z, then 4 per further angle
+    float ak[6];        // exact float keys of the axis slots (min x, max x, min y, max y, min z, max z)
     unsigned ai[6];
-    double rk[RR];
+    double rk[RR];      // exact binary64 keys of the rotated slots
     unsigned ri[RR];
-    float T[RR];
+    float T[D];         // warp thresholds (float, on the safe side of a reduced point's exact key)
 };
 
 template <int NANG>
@@ -89,18 +99,24 @@ __device__ __forceinline__ void lane_init(Lane<NANG>& L) {
     for (int s = 0; s < Lane<NANG>::RR; ++s) {
         L.rk[s] = (s & 1) ? -INFINITY : INFINITY;
         L.ri[s] = kNone;
-        L.T[s] = (s & 1) ? -INFINITY : INFINITY;
     }
+#pragma unroll
+    for (int s = 0; s < Lane<NANG>::D; ++s) L.T[s] = (s & 1) ? -INFINITY : INFINITY;
 }
 
-// exact update of the rotated keys (cold path, one lane's candidate point)
+// exact update of every key of one point (cold path; a lane's points arrive in
+// ascending index order, so strict improvement keeps the lowest index)
 template <int NANG>
-__device__ __forceinline__ void exact_rot(Lane<NANG>& L, float x, float y, unsigned i, const K13Params& p,
-                                          unsigned& bad) {
-    if (!isfinite(x) || !isfinite(y)) {
+__device__ __forceinline__ void exact_point(Lane<NANG>& L, float x, float y, float z, unsigned i,
+                                            const K13Params& p, unsigned& bad) {
+    if (!(fabsf(x) <= FLT_MAX && fabsf(y) <= FLT_MAX && fabsf(z) <= FLT_MAX)) {
         bad = 1u;
         return;
     }
+    const float av[6] = {x, x, y, y, z, z};
+#pragma unroll
+    for (int s = 0; s < 6; ++s)
+        if ((s & 1) ? av[s] > L.ak[s] : av[s] < L.ak[s]) L.ak[s] = av[s], L.ai[s] = i;
     const double xd = x, yd = y;
 #pragma unroll
     for (int k = 1; k < NANG; ++k) {
@@ -110,79 +126,72 @@ __device__ __forceinline__ void exact_rot(Lane<NANG>& L, float x, float y, unsig
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
             const int s = 4 * (k - 1) + r;
-            if ((r & 1) ? kv[r] > L.rk[s] : kv[r] < L.rk[s]) {   // ascending i: strict = lowest index
-                L.rk[s] = kv[r];
-                L.ri[s] = i;
-            }
+            if ((r & 1) ? kv[r] > L.rk[s] : kv[r] < L.rk[s]) L.rk[s] = kv[r], L.ri[s] = i;
         }
     }
 }
 
+// warp thresholds from the lanes' exact states: max slots take the largest
+// float <= some lane's key, min slots the smallest float >= some lane's key
 template <int NANG>
 __device__ __forceinline__ void refresh(Lane<NANG>& L) {
 #pragma unroll
+    for (int s = 0; s < 6; ++s)
+        L.T[s] = dec_f((s & 1) ? __reduce_max_sync(kFull, enc_f(L.ak[s])) : __reduce_min_sync(kFull, enc_f(L.ak[s])));
+#pragma unroll
     for (int s = 0; s < Lane<NANG>::R; ++s) {
         if (s & 1) {
-            L.T[s] = dec_f(__reduce_max_sync(kFull, enc_f(__double2float_rd(L.rk[s]))));
+            L.T[6 + s] = dec_f(__reduce_max_sync(kFull, enc_f(__double2float_rd(L.rk[s]))));
         } else {
-            L.T[s] = dec_f(__reduce_min_sync(kFull, enc_f(__double2float_ru(L.rk[s]))));
+            L.T[6 + s] = dec_f(__reduce_min_sync(kFull, enc_f(__double2float_ru(L.rk[s]))));
         }
     }
 }
 
-// float screen of the pair (x0, y0), (x1, y1): candidate bits (bit 0 / bit 1)
-template <int NANG>
-__device__ __forceinline__ unsigned screen_pair(const Lane<NANG>& L, float x0, float y0, float x1, float y1,
-                                                const K13Params& p) {
-    const float2 xx = make_float2(x0, x1), yy = make_float2(y0, y1);
-    const float2 ab = make_float2(__fadd_rn(fabsf(x0), fabsf(y0)), __fadd_rn(fabsf(x1), fabsf(y1)));
-    const float2 m = __ffma2_rn(ab, make_float2(0x1p-20f, 0x1p-20f), make_float2(0x1p-120f, 0x1p-120f));
-    const float2 nm = __ffma2_rn(ab, make_float2(-0x1p-20f, -0x1p-20f), make_float2(-0x1p-120f, -0x1p-120f));
-    bool c0 = false, c1 = false;
-#pragma unroll
-    for (int k = 1; k < NANG; ++k) {
-        const float2 cf = make_float2(p.cf[k], p.cf[k]);
-        const float2 X = __ffma2_rn(xx, cf, __fmul2_rn(yy, make_float2(p.sf[k], p.sf[k])));
-        const float2 Y = __ffma2_rn(yy, cf, __fmul2_rn(xx, make_float2(p.nsf[k], p.nsf[k])));
-        const float2 Xl = __fadd2_rn(X, nm), Xh = __fadd2_rn(X, m);
-        const float2 Yl = __fadd2_rn(Y, nm), Yh = __fadd2_rn(Y, m);
-        const int b = 4 * (k - 1);
-        c0 |= !(Xl.x > L.T[b + 0]) | !(Xh.x < L.T[b + 1]) | !(Yl.x > L.T[b + 2]) | !(Yh.x < L.T[b + 3]);
-        c1 |= !(Xl.y > L.T[b + 0]) | !(Xh.y < L.T[b + 1]) | !(Yl.y > L.T[b + 2]) | !(Yh.y < L.T[b + 3]);
-    }
-    return (c0 ? 1u : 0u) | (c1 ? 2u : 0u);
-}
-
+// One quad: screen all four points — the axis keys exactly in float, the
+// rotated keys against thresholds widened by the quad's largest margin
+// mq = max_e RN32(fma(|x_e|+|y_e|, 2^-20, 2^-120)) >= each point's m (a point
+// whose exact key ties or beats T has Xf < T + m <= T + mq, so Xf <= RN(T +
+// mq): never pruned).  A candidate sends the whole quad through the exact
+// path.  Unordered compares make NaN / Inf candidates, which the exact path
+// flags.
 template <int NANG>
 __device__ __forceinline__ void fold_quad(Lane<NANG>& L, const Quad& Q, unsigned valid, unsigned i0,
                                           const K13Params& p, unsigned& bad, unsigned& nexact) {
+    bool c = false;
+    float am = 0.0f;
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-        if ((unsigned)e < valid) {
-            const float x = Q.v[3 * e], y = Q.v[3 * e + 1], z = Q.v[3 * e + 2];
-            const unsigned i = i0 + e;
-            if (x < L.ak[0]) L.ak[0] = x, L.ai[0] = i;
-            if (x > L.ak[1]) L.ak[1] = x, L.ai[1] = i;
-            if (y < L.ak[2]) L.ak[2] = y, L.ai[2] = i;
-            if (y > L.ak[3]) L.ak[3] = y, L.ai[3] = i;
-            if (z < L.ak[4]) L.ak[4] = z, L.ai[4] = i;
-            if (z > L.ak[5]) L.ak[5] = z, L.ai[5] = i;
-            bad |= (fabsf(x) <= FLT_MAX && fabsf(y) <= FLT_MAX && fabsf(z) <= FLT_MAX) ? 0u : 1u;
-        }
+        const float x = Q.v[3 * e], y = Q.v[3 * e + 1], z = Q.v[3 * e + 2];
+        c |= !(x > L.T[0]) | !(x < L.T[1]) | !(y > L.T[2]) | !(y < L.T[3]) | !(z > L.T[4]) | !(z < L.T[5]);
+        am = fmaxf(am, __fadd_rn(fabsf(x), fabsf(y)));
     }
     if (NANG > 1) {
-        unsigned cand = screen_pair<NANG>(L, Q.v[0], Q.v[1], Q.v[3], Q.v[4], p) |
-                        (screen_pair<NANG>(L, Q.v[6], Q.v[7], Q.v[9], Q.v[10], p) << 2);
-        cand &= (1u << valid) - 1u;
-        if (__any_sync(kFull, cand != 0u)) {
-#pragma unroll 1
-            for (unsigned c = cand; c; c &= c - 1u) {
-                const int e = __ffs(c) - 1;
-                exact_rot<NANG>(L, Q.v[3 * e], Q.v[3 * e + 1], i0 + e, p, bad);
-                ++nexact;
+        const float mq = __fmaf_rn(am, 0x1p-20f, 0x1p-120f);
+#pragma unroll
+        for (int k = 1; k < NANG; ++k) {
+            const float* T = &L.T[6 + 4 * (k - 1)];
+            const float t0 = __fadd_rn(T[0], mq), t1 = __fsub_rn(T[1], mq);
+            const float t2 = __fadd_rn(T[2], mq), t3 = __fsub_rn(T[3], mq);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const float x = Q.v[3 * e], y = Q.v[3 * e + 1];
+                const float X = __fmaf_rn(x, p.cf[k], __fmul_rn(y, p.sf[k]));
+                const float Y = __fmaf_rn(y, p.cf[k], __fmul_rn(x, p.nsf[k]));
+                c |= !(X > t0) | !(X < t1) | !(Y > t2) | !(Y < t3);
             }
-            refresh<NANG>(L);
         }
+    }
+    c &= valid != 0u;
+    if (__any_sync(kFull, c)) {
+        if (c) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e)   // static indices: the quad stays in registers
+                if ((unsigned)e < valid)
+                    exact_point<NANG>(L, Q.v[3 * e], Q.v[3 * e + 1], Q.v[3 * e + 2], i0 + e, p, bad);
+            nexact += valid;
+        }
+        refresh<NANG>(L);
     }
 }
 
@@ -201,8 +210,26 @@ __global__ void __launch_bounds__(kK13Threads, 2) k1_extremes3(const __grid_cons
     const unsigned nq = (p.n + 3u) / 4u;
     const unsigned gwarps = gridDim.x * (kK13Threads / 32);
     const unsigned gw = blockIdx.x * (kK13Threads / 32) + warp;
-    // warp-uniform loop: each warp takes kK13Quads*32 consecutive quads per step
-    for (unsigned qb = gw * (32u * kK13Quads); qb < nq; qb += gwarps * (32u * kK13Quads)) {
+    // warp-uniform loop: each warp takes kK13Quads*32 consecutive quads per
+    // step; lane 0 prefetches the warp's range kAhead steps ahead into L2
+    // (16-B aligned input only), which doubles the bytes in flight at no
+    // register cost
+    constexpr unsigned kStep = 32u * kK13Quads;
+    constexpr int kAhead = 2;
+    const unsigned gstep = gwarps * kStep;
+    if (VEC && lane == 0)
+        for (int a = 1; a < kAhead; ++a) {
+            const unsigned qa = gw * kStep + a * gstep;
+            if (qa + kStep <= p.n / 4u) prefetch_l2(p.pts + 12ull * qa, 48u * kStep);
+        }
+    for (unsigned qb = gw * kStep; qb < nq; qb += gstep) {
+        if (VEC && lane == 0) {
+            const unsigned qa = qb + kAhead * gstep;
+            if (qa < qb) {
+            } else if (qa + kStep <= p.n / 4u) {
+                prefetch_l2(p.pts + 12ull * qa, 48u * kStep);
+            }
+        }
         Quad Q[kK13Quads];
         unsigned valid[kK13Quads];
 #pragma unroll

@@ -7,19 +7,25 @@
 // Classification (exact semantics): p is DISCARDED iff orient3d(f, p) > 0
 // for every facet plane f.  With the centre o strictly inside (checked
 // exactly on the host), the ray from o through p leaves the polyhedron
-// through a facet whose face contains the ray's direction, and that
-// direction lies in p's closed octant around o — an exact float compare per
-// axis.  So p is strictly inside iff it is strictly inside every facet whose
-// face meets its octant: the host lists those per octant (conservatively,
-// DESIGN.md §6.5), and the kernel tests only them:
+// through a facet whose face contains the ray's direction; p is strictly
+// inside iff it is strictly inside that facet.  The direction d = RN(p - o)
+// selects one of 1536 cube-map cells (major axis, sign, and the two other
+// components over the major one on a 16 x 16 grid; one approximate
+// reciprocal), and the host lists, per cell, every facet whose face meets the
+// cell's direction pyramid widened by a guard far larger than the kernel's
+// rounding — about 2 of ~32 on average.  Lists of up to 3
+// are tested branch-free (unused slots: a plane that always says "inside"),
+// longer ones walk the cell's facet mask:
 //   g = fma(A, x, fma(B, y, fma(C, z, D))), |g - orient3d| <= E over the
-//   data bounding box:   g < -E on any entry -> keep;  g > E on all -> discard;
-//   otherwise the exact orient3d (exact3.cuh) on the undecided entries.
+//   data bounding box:   g < -E on any candidate -> keep;  g > E on all ->
+//   discard;  otherwise the exact orient3d (exact3.cuh) on the undecided ones.
+// A direction too short for the reciprocal (or NaN) takes every facet.
 // Compaction: persistent blocks take 2048-point tiles (24 KiB) from an atomic
 // ticket; each thread classifies two quads (8 points); a packed two-half
 // block scan orders the survivors; warp 0 resolves the tile's exclusive
 // prefix by a decoupled look-back over epoch-tagged status words (one per
-// 128-byte line); survivors' int64 index (+ xyz) are written in order.
+// 128-byte line), deferred by one tile so that it never waits; survivors'
+// int64 index (+ xyz, kept in registers) are written in order.
 #include <cuda_runtime.h>
 
 #include <cfloat>
@@ -38,17 +44,17 @@ constexpr unsigned kEpochMask = 0x3fffffffu;
 constexpr int kWarps = kK23Threads / 32;
 
 struct Smem3 {
-    float4 pl[kMax3Entries];
-    float pe[kMax3Entries];
-    unsigned char pf[kMax3Entries];
+    unsigned clist[kCells];
+    float4 pl[kMax3Facets + 1];
+    float pe[kMax3Facets + 1];
     float fv[kMax3Facets][9];
-    int beg[8], end[8];
+    unsigned long long all;
     float ox, oy, oz;
     int mode;
     unsigned wsum[kWarps];
-    unsigned wbase[kWarps];
-    unsigned tile;
-    unsigned total;
+    unsigned wbase[2][kWarps];
+    unsigned tile[2];
+    unsigned total[2];
     unsigned long long ex;
 };
 
@@ -113,37 +119,71 @@ __device__ unsigned long long resolve(const K23Params& p, unsigned tile, unsigne
     return ex;
 }
 
-// the exact decision over the candidate entries [b, e) (rare path)
-__device__ __noinline__ bool keep_exact(const Smem3& g, float x, float y, float z, int b, int e,
+__device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ float rcp_approx(float a) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(a));
+    return r;
+}
+
+// the exact decision over the candidate facets (rare path)
+__device__ __noinline__ bool keep_exact(const Smem3& g, float x, float y, float z, unsigned long long mask,
                                         unsigned* nexact) {
     if (!(fabsf(x) <= FLT_MAX && fabsf(y) <= FLT_MAX && fabsf(z) <= FLT_MAX)) return true;
     ++*nexact;
     const float q[3] = {x, y, z};
-    for (int t = b; t < e; ++t) {
+    for (; mask; mask &= mask - 1ull) {
+        const int t = __ffsll((long long)mask) - 1;
         const float4 P = g.pl[t];
         const float v = __fmaf_rn(P.x, x, __fmaf_rn(P.y, y, __fmaf_rn(P.z, z, P.w)));
         const float E = g.pe[t];
         if (v < -E) return true;
         if (v > E) continue;
-        const float* f = g.fv[g.pf[t]];
+        const float* f = g.fv[t];
         if (orient3d_sign_f(f, f + 3, f + 6, q) <= 0) return true;
     }
     return false;
 }
 
-__device__ __forceinline__ bool keep_pt(const Smem3& g, float x, float y, float z, unsigned* nexact) {
-    const int o = (x < g.ox ? 1 : 0) | (y < g.oy ? 2 : 0) | (z < g.oz ? 4 : 0);
-    const int b = g.beg[o], e = g.end[o];
-    bool unsure = false;
-    for (int t = b; t < e; ++t) {
-        const float4 P = g.pl[t];
-        const float v = __fmaf_rn(P.x, x, __fmaf_rn(P.y, y, __fmaf_rn(P.z, z, P.w)));
-        const float E = g.pe[t];
-        if (v < -E) return true;
-        unsure |= !(v > E);
+__device__ __forceinline__ bool keep_pt(const Smem3& g, const K3Geom* __restrict__ G, float x, float y, float z,
+                                        unsigned* nexact) {
+    const float dx = __fsub_rn(x, g.ox), dy = __fsub_rn(y, g.oy), dz = __fsub_rn(z, g.oz);
+    const float ax = fabsf(dx), ay = fabsf(dy), az = fabsf(dz);
+    const bool xm = ax >= ay && ax >= az;
+    const bool ym = !xm && ay >= az;
+    const float m = xm ? dx : (ym ? dy : dz);
+    const float u = xm ? dy : (ym ? dz : dx);
+    const float v = xm ? dz : (ym ? dx : dy);
+    const float am = fabsf(m);
+    const float r = __fmul_rn(rcp_approx(am), 0.5f * kCellG);
+    const float fu = fminf(fmaxf(__fmaf_rn(u, r, 0.5f * kCellG), 0.0f), kCellG - 0.5f);
+    const float fv = fminf(fmaxf(__fmaf_rn(v, r, 0.5f * kCellG), 0.0f), kCellG - 0.5f);
+    const int face = (xm ? 0 : (ym ? 2 : 4)) + (m < 0.0f ? 1 : 0);
+    const int cell = (face * kCellG + (int)fu) * kCellG + (int)fv;
+    const bool ok = am >= 0x1p-100f;   // false for NaN and for directions too short for the reciprocal
+    const unsigned w = g.clist[ok ? cell : 0];
+    if (!ok || (w >> 24) > (unsigned)kCellSlots) {   // long list (or no cell): walk the mask
+        const unsigned li = w & 0xffffffu;
+        return keep_exact(g, x, y, z, (ok && li != kNoLong) ? __ldg(&G->lmask[li]) : g.all, nexact);
     }
+    bool out = false, unsure = false;
+    unsigned long long cand = 0;
+#pragma unroll
+    for (int k = 0; k < kCellSlots; ++k) {   // branch-free: unused slots test the dummy plane
+        const unsigned t = (w >> (8 * k)) & 0xffu;
+        const float4 P = g.pl[t];
+        const float E = g.pe[t];
+        const float val = __fmaf_rn(P.x, x, __fmaf_rn(P.y, y, __fmaf_rn(P.z, z, P.w)));
+        out |= val < -E;
+        unsure |= !(val > E);
+        cand |= (t < (unsigned)kMax3Facets) ? (1ull << t) : 0ull;
+    }
+    if (out) return true;
     if (!unsure) return false;
-    return keep_exact(g, x, y, z, b, e, nexact);
+    return keep_exact(g, x, y, z, cand, nexact);
 }
 
 template <bool VEC>
@@ -162,8 +202,10 @@ __device__ __forceinline__ unsigned load_quad(const float* __restrict__ pts, uns
     return valid;
 }
 
-__device__ __forceinline__ void emit(const K23Params& p, const float (&v)[12], unsigned bits, unsigned i0,
+// Write one quad's survivors (coordinates v) from position pos on.
+__device__ __forceinline__ void emit(const K23Params& p, const float (&v)[12], unsigned bits, unsigned q,
                                      unsigned long long pos) {
+    const unsigned i0 = 4u * q;
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
         if ((bits >> e) & 1u) {
@@ -184,86 +226,113 @@ __global__ void __launch_bounds__(kK23Threads, kK23BlocksPerSM) k2_filter3(const
     __shared__ Smem3 g;
     const unsigned tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
     const K3Geom* G = p.g;
-    const int nent = G->nent;
-    for (int t = tid; t < nent; t += kK23Threads) {
-        g.pl[t] = G->pl[t];
-        g.pe[t] = G->pe[t];
-        g.pf[t] = G->pf[t];
-    }
-    for (int t = tid; t < G->nf * 9; t += kK23Threads) g.fv[t / 9][t % 9] = G->fv[t / 9][t % 9];
-    if (tid < 8) {
-        g.beg[tid] = G->oct_start[tid];
-        g.end[tid] = G->oct_start[tid + 1];
-        if (!G->octants) {   // one list for every octant
-            g.beg[tid] = 0;
-            g.end[tid] = G->oct_start[1];
+    for (int t = tid; t < kCells; t += kK23Threads) g.clist[t] = G->clist[t];
+    const int nf = G->nf;
+    for (int t = tid; t <= kMax3Facets; t += kK23Threads)
+        if (t < nf || t == kDummyFacet) {
+            g.pl[t] = G->pl[t];
+            g.pe[t] = G->pe[t];
         }
-    }
+    for (int t = tid; t < nf * 9; t += kK23Threads) g.fv[t / 9][t % 9] = G->fv[t / 9][t % 9];
     if (tid == 0) {
         g.ox = G->ox, g.oy = G->oy, g.oz = G->oz;
         g.mode = G->mode;
+        g.all = G->all;
     }
     const unsigned epoch = *(volatile unsigned*)&p.ws->epoch;
     unsigned nexact = 0;
     __syncthreads();
     const bool keep_all = g.mode != 0;
 
+    // Deferred look-back (as the 2D kernel): tile k's aggregate is published
+    // right after its scan, but its prefix is resolved only after tile k+1 has
+    // been classified, when every predecessor has long published its own
+    // aggregate — no spinning.  Tile k's keep bits and in-warp offsets stay in
+    // registers; its warp bases and total in shared memory (double-buffered).
+    // L2 prefetch one wave ahead: the tile gridDim.x after the claimed one is
+    // about the one some block claims next (no ticket is held early).
+    const unsigned full_tiles = p.n / kK23TilePts;
+    bool have_prev = false;
+    unsigned prev_tile = 0, pb0 = 0, pb1 = 0, pexcl = 0;
+    float pv0[12], pv1[12];   // the previous tile's quads (emitted one tile later)
+    int par = 0;
     for (;;) {
-        if (tid == 0) g.tile = atomicAdd(&p.ws->k2_ticket, 1u);
+        if (tid == 0) {
+            const unsigned t = atomicAdd(&p.ws->k2_ticket, 1u);
+            g.tile[par] = t;
+            const unsigned ahead = t + gridDim.x;
+            if (VEC && ahead < full_tiles) prefetch_l2(p.pts + 3ull * kK23TilePts * ahead, 12u * kK23TilePts);
+        }
         __syncthreads();
-        const unsigned tile = g.tile;
-        if (tile >= p.num_tiles) break;
+        const unsigned tile = g.tile[par];
+        const bool live = tile < p.num_tiles;
+        unsigned b0 = 0, b1 = 0, c = 0, incl = 0;
         const unsigned q0 = tile * kK23TileQuads + tid, q1 = q0 + kK23Threads;
         float v0[12], v1[12];
-        const unsigned n0 = load_quad<VEC>(p.pts, q0, p.n, v0);
-        const unsigned n1 = load_quad<VEC>(p.pts, q1, p.n, v1);
-        unsigned b0 = 0, b1 = 0;
+        if (live) {
+            const unsigned n0 = load_quad<VEC>(p.pts, q0, p.n, v0);
+            const unsigned n1 = load_quad<VEC>(p.pts, q1, p.n, v1);
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            if ((unsigned)e < n0 && (keep_all || keep_pt(g, v0[3 * e], v0[3 * e + 1], v0[3 * e + 2], &nexact)))
-                b0 |= 1u << e;
-            if ((unsigned)e < n1 && (keep_all || keep_pt(g, v1[3 * e], v1[3 * e + 1], v1[3 * e + 2], &nexact)))
-                b1 |= 1u << e;
-        }
-        // packed scan: low half = first 256 quads, high half = second 256
-        const unsigned c = (unsigned)__popc(b0) | ((unsigned)__popc(b1) << 16);
-        unsigned incl = c;
+            for (int e = 0; e < 4; ++e) {
+                if ((unsigned)e < n0 && (keep_all || keep_pt(g, G, v0[3 * e], v0[3 * e + 1], v0[3 * e + 2], &nexact)))
+                    b0 |= 1u << e;
+                if ((unsigned)e < n1 && (keep_all || keep_pt(g, G, v1[3 * e], v1[3 * e + 1], v1[3 * e + 2], &nexact)))
+                    b1 |= 1u << e;
+            }
+            // packed scan: low half = first 256 quads, high half = second 256
+            c = (unsigned)__popc(b0) | ((unsigned)__popc(b1) << 16);
+            incl = c;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const unsigned t = __shfl_up_sync(kFull, incl, o);
-            if (lane >= (unsigned)o) incl += t;
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned t = __shfl_up_sync(kFull, incl, o);
+                if (lane >= (unsigned)o) incl += t;
+            }
+            if (lane == 31) g.wsum[warp] = incl;
         }
-        if (lane == 31) g.wsum[warp] = incl;
         __syncthreads();
         if (warp == 0) {
-            const unsigned ws = lane < kWarps ? g.wsum[lane] : 0u;
-            unsigned wi = ws;
+            if (live) {
+                const unsigned ws = lane < kWarps ? g.wsum[lane] : 0u;
+                unsigned wi = ws;
 #pragma unroll
-            for (int o = 1; o < kWarps; o <<= 1) {
-                const unsigned t = __shfl_up_sync(kFull, wi, o);
-                if (lane >= (unsigned)o) wi += t;
+                for (int o = 1; o < kWarps; o <<= 1) {
+                    const unsigned t = __shfl_up_sync(kFull, wi, o);
+                    if (lane >= (unsigned)o) wi += t;
+                }
+                const unsigned tot = __shfl_sync(kFull, wi, kWarps - 1);
+                if (lane < kWarps) g.wbase[par][lane] = wi - ws;
+                if (lane == 0) {
+                    g.total[par] = tot;
+                    const unsigned total = (tot & 0xffffu) + (tot >> 16);
+                    publish(p, tile, tile == 0 ? kFlagP : kFlagA, total, epoch);
+                    if (tile == 0 && tile == p.num_tiles - 1) p.ws->count = total;
+                }
             }
-            const unsigned tot = __shfl_sync(kFull, wi, kWarps - 1);
-            if (lane < kWarps) g.wbase[lane] = wi - ws;
-            const unsigned total = (tot & 0xffffu) + (tot >> 16);
-            if (lane == 0) {
-                g.total = tot;
-                publish(p, tile, tile == 0 ? kFlagP : kFlagA, total, epoch);
-            }
-            const unsigned long long ex = tile == 0 ? 0ull : resolve(p, tile, epoch, lane);
-            if (lane == 0) {
-                if (tile != 0) publish(p, tile, kFlagP, ex + total, epoch);
-                g.ex = ex;
-                if (tile == p.num_tiles - 1) p.ws->count = ex + total;
+            if (have_prev) {
+                const unsigned tot = g.total[par ^ 1];
+                const unsigned total = (tot & 0xffffu) + (tot >> 16);
+                const unsigned long long ex = prev_tile == 0 ? 0ull : resolve(p, prev_tile, epoch, lane);
+                if (lane == 0) {
+                    if (prev_tile != 0) publish(p, prev_tile, kFlagP, ex + total, epoch);
+                    g.ex = ex;
+                    if (prev_tile == p.num_tiles - 1) p.ws->count = ex + total;
+                }
             }
         }
         __syncthreads();
-        const unsigned long long ex = g.ex;
-        const unsigned wb = g.wbase[warp], lo_tot = g.total & 0xffffu;
-        const unsigned excl = incl - c;
-        emit(p, v0, b0, 4u * q0, ex + (wb & 0xffffu) + (excl & 0xffffu));
-        emit(p, v1, b1, 4u * q1, ex + lo_tot + (wb >> 16) + (excl >> 16));
-        __syncthreads();   // g.tile / wsum reuse
+        if (have_prev) {
+            const unsigned long long ex = g.ex;
+            const unsigned wb = g.wbase[par ^ 1][warp], lo_tot = g.total[par ^ 1] & 0xffffu;
+            const unsigned pq0 = prev_tile * kK23TileQuads + tid;
+            emit(p, pv0, pb0, pq0, ex + (wb & 0xffffu) + (pexcl & 0xffffu));
+            emit(p, pv1, pb1, pq0 + kK23Threads, ex + lo_tot + (wb >> 16) + (pexcl >> 16));
+        }
+        if (!live) break;
+        have_prev = true;
+        prev_tile = tile, pb0 = b0, pb1 = b1, pexcl = incl - c;
+#pragma unroll
+        for (int j = 0; j < 12; ++j) pv0[j] = v0[j], pv1[j] = v1[j];
+        par ^= 1;
     }
     nexact = __reduce_add_sync(kFull, nexact);
     if (lane == 0 && nexact) atomicAdd(&p.ws->k2_exact, nexact);

@@ -78,8 +78,9 @@ def test_host_polyhedron_matches_oracle_facets(family, angles):
     assert poly.eidx.tolist() == E.tolist()
     assert poly.facets.tolist() == oracle.facets3(xyz, E).tolist()
     assert poly.nf >= 4
-    assert poly.raw.octants == 1
-    assert poly.raw.n_entries >= poly.nf       # every facet meets some octant
+    assert poly.raw.cells == 1
+    assert poly.raw.n_entries >= poly.nf       # every facet meets some cell
+    assert 1 <= poly.raw.max_candidates <= poly.nf
 
 
 def test_host_polyhedron_degenerate_and_ties():
