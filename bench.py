@@ -1,6 +1,7 @@
 """Benchmark: filtered points/s of the CudaPre hot path (Steps 1-3) on B200.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config C5] [--impl ours|reference]
+    python bench.py --config T4      # the 3D extension, synth.CONFIGS3
     python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 ... bench.py --gpus N
 
 One step = one pass of the whole hot path over the workload resident in HBM:
@@ -128,6 +129,226 @@ def sized_sample(pts_dev, target_s: float, threads: int, angles: str, cap: int):
     return n, rate
 
 
+METRIC3 = "3D extension (P:115): filtered points/sec (Gpts/s) and % of HBM roofline; discard %"
+K13_BYTES_PER_PT = 12         # K1-3D reads each float3 once
+K23_BYTES_PER_PT = 12         # K2-3D reads each float3 once ...
+K23_BYTES_PER_SURVIVOR = 20   # ... and writes int64 index + float3 point per survivor
+
+
+def oracle3_rate(pts_host: np.ndarray, threads: int, angles: str):
+    import oracle
+
+    oracle.build()
+    t0 = time.perf_counter()
+    oracle.cudapre3(pts_host, angles, threads=threads)
+    dt = time.perf_counter() - t0
+    return len(pts_host) / dt, dt
+
+
+def sized_sample3(pts_dev, target_s: float, threads: int, angles: str, cap: int):
+    pilot = min(cap, 200_000)
+    rate, _ = oracle3_rate(pts_dev[:pilot].cpu().numpy(), threads, angles)
+    return int(min(cap, max(pilot, rate * target_s))), rate
+
+
+def main3(args, world, rank, local):
+    """The 3D extension (configs synth.CONFIGS3, not BASELINE
+    configs): one step = K1-3D (+ D2H of the picks; N > 1: all-gather + host
+    merge), host Step 2 (polyhedron + cell lists, H2D), K2-3D writing each
+    survivor's int64 index and float3 point (+ D2H of the count)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1405_3454_b200 as cp
+    import synth
+    import synth.cuda as scuda
+    from paper_1405_3454_b200 import build as pbuild
+
+    cfg = dict(synth.CONFIGS3[args.config])
+    n_total = args.n or cfg.pop("n")
+    cfg.pop("n", None)
+    family, seed = cfg.pop("family"), cfg.pop("seed")
+    threads = os.cpu_count() or 1
+    torch.cuda.set_device(local)
+    if args.impl == "reference":   # the 3D oracle on a bounded sample, rank 0 only
+        if rank != 0:
+            return
+        scuda.build()
+        sample_cap = min(n_total, 20_000_000)
+        dev = scuda.generate3(family, sample_cap, seed=seed, **cfg)
+        n_s, _ = sized_sample3(dev, 2.0, threads, args.angles, sample_cap)
+        host = dev[:n_s].cpu().numpy()
+        del dev
+        import oracle
+
+        for _ in range(args.warmup):
+            oracle.cudapre3(host, args.angles, threads=threads)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            oracle.cudapre3(host, args.angles, threads=threads)
+        dt = time.perf_counter() - t0
+        v = n_s * args.steps / dt / 1e9
+        print(json.dumps({
+            "metric": METRIC3, "value": v, "unit": "Gpts/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": {"workload": f"{args.config}: {n_total} pts {family} seed {seed}",
+                       "sample_points_per_step": n_s},
+            "cpu_baseline": {"value": v, "unit": "Gpts/s", "cores": threads, "kind": "oracle",
+                             "sample": f"first {n_s} points of {args.config} per step"},
+            "e2e": {"value": v, "unit": "Gpts/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}), flush=True)
+        return
+
+    group = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        group = dist.group.WORLD
+    if rank == 0:
+        pbuild.build()
+        scuda.build()
+    if group is not None:
+        dist.barrier()
+    n_local = n_total // world + (1 if rank < n_total % world else 0)
+    base = rank * (n_total // world) + min(rank, n_total % world)
+    pts = scuda.generate3(family, n_local, seed=seed, base=base, **cfg)
+    ws = cp.Workspace3(n_local)
+    out_idx = torch.empty(n_local, dtype=torch.int64, device="cuda")
+    out_pts = None if args.no_points else torch.empty((n_local, 3), dtype=torch.float32, device="cuda")
+    ext_dev = torch.empty(ctypes_sizeof(cp.Extremes3T), dtype=torch.uint8, device="cuda")
+    torch.cuda.synchronize()
+    k1_ms, k2_ms, info = [], [], {}
+
+    def step(timed=True):
+        ext = cp.extremes3(pts, args.angles, index_base=base, ws=ws, device_out=ext_dev,
+                           timing=k1_ms if timed else None)
+        if group is not None:   # cross-rank combine of the Step-1 blocks (as 2D a3)
+            g = torch.empty(world * ext_dev.numel(), dtype=torch.uint8, device="cuda")
+            dist.all_gather_into_tensor(g, ext_dev, group=group)
+            raw = g.cpu().numpy().tobytes()
+            sz = ext_dev.numel()
+            ext = cp.merge3([cp.Extremes3T.from_buffer_copy(raw[r * sz:(r + 1) * sz]) for r in range(world)])
+        idx, _, poly = cp.filter3(pts, ext, index_base=base, ws=ws, out_idx=out_idx, out_pts=out_pts,
+                                  return_points=out_pts is not None, timing=k2_ms if timed else None)
+        info.update(surv=idx.shape[0], nf=poly.nf, exact=ext.raw.exact_points,
+                    mean_cand=poly.raw.n_entries / (6 * 32 * 32), long_cells=poly.raw.long_cells)
+
+    for _ in range(args.warmup):
+        step(False)
+    clocks = ClockSampler(torch.cuda.current_device())
+    if group is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with clocks:
+        start.record()
+        for _ in range(args.steps):
+            step()
+        end.record()
+        torch.cuda.synchronize()
+    ms = start.elapsed_time(end)
+    surv = info["surv"]
+    if group is not None:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        s_ = torch.tensor([surv], device="cuda", dtype=torch.int64)
+        dist.all_reduce(s_)
+        surv_total = int(s_.item())
+    else:
+        surv_total = surv
+    value = n_total * args.steps / (ms / 1e3) / 1e9
+
+    pk = peaks()
+    peak = pk["hbm_gbs"] if pk else 6650.0
+    k1, k2 = statistics.mean(k1_ms), statistics.mean(k2_ms)
+    k1_bytes = K13_BYTES_PER_PT * n_local
+    k2_bytes = K23_BYTES_PER_PT * n_local + (K23_BYTES_PER_SURVIVOR if out_pts is not None else 8) * surv
+    kernels = {"k1_extremes3": (k1, k1_bytes), "k2_filter3": (k2, k2_bytes)}
+    dom = max(kernels, key=lambda k: kernels[k][0])
+    d_ms, d_bytes = kernels[dom]
+    achieved = d_bytes / (d_ms / 1e3) / 1e9
+    traffic = None
+    try:
+        ent = json.load(open(os.path.join(ROOT, "profiles", "traffic.json"))).get(args.config, {}).get(dom)
+        if ent and int(ent.get("n_local", -1)) == n_local:
+            traffic = ent["dram_bytes_per_launch"]
+    except (OSError, ValueError):
+        pass
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": traffic, "kernel": dom,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, measured)" if pk else "fallback",
+                "per_kernel_ms": {k: round(v[0], 4) for k, v in kernels.items()},
+                "per_kernel_GBps": {k: round(v[1] / (v[0] / 1e3) / 1e9, 1) for k, v in kernels.items()},
+                "pipeline_GBps": round((k1_bytes + k2_bytes) * args.steps / (ms / 1e3) / 1e9, 1)}
+
+    e2e = None
+    if not args.no_e2e and group is None:
+        e_steps = max(1, min(args.steps, 3))
+        try:
+            h_pts = torch.empty((n_local, 3), dtype=torch.float32).pin_memory()
+            h_surv = torch.empty(n_local, dtype=torch.int64).pin_memory()
+        except RuntimeError:
+            h_pts = torch.empty((n_local, 3), dtype=torch.float32)
+            h_surv = torch.empty(n_local, dtype=torch.int64)
+        h_pts.copy_(pts)
+
+        def e2e_step():
+            pts.copy_(h_pts, non_blocking=True)
+            ext = cp.extremes3(pts, args.angles, index_base=base, ws=ws)
+            idx, _, _ = cp.filter3(pts, ext, index_base=base, ws=ws, out_idx=out_idx, return_points=False)
+            h_surv[: idx.shape[0]].copy_(idx)
+            return idx.shape[0]
+
+        e2e_step()
+        torch.cuda.synchronize()
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record()
+        for _ in range(e_steps):
+            m = e2e_step()
+        t1.record()
+        torch.cuda.synchronize()
+        e_ms = t0.elapsed_time(t1)
+        e2e = {"value": n_total * e_steps / (e_ms / 1e3) / 1e9, "unit": "Gpts/s",
+               "h2d_bytes_per_step": 12 * n_local, "d2h_bytes_per_step": 8 * m + ctypes_sizeof(cp.Extremes3T) + 8,
+               "steps": e_steps, "pinned": bool(h_pts.is_pinned())}
+        del h_pts, h_surv
+
+    cpu = None
+    if world == 1 and rank == 0 and not args.no_cpu_baseline:
+        n_s, _ = sized_sample3(pts, 12.0, threads, args.angles, min(n_local, 20_000_000))
+        rate, dt = oracle3_rate(pts[:n_s].cpu().numpy(), threads, args.angles)
+        cpu = {"value": rate / 1e9, "unit": "Gpts/s", "cores": threads, "kind": "oracle",
+               "sample": f"first {n_s} points of {args.config} (3D oracle Steps 1-3, {dt:.1f} s)"}
+
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC3, "value": round(value, 3), "unit": "Gpts/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32+f64",
+            "data": "synthetic",
+            "config": {"workload": f"{args.config}: {n_total} pts {family} (seed {seed}), float3 AoS, "
+                                   f"contiguous shards of {n_local}", "n_total": n_total, "angles": args.angles,
+                       "l2": f"inputs larger than L2 ({12 * n_local / 1e9:.2f} GB vs 126 MB), no flush",
+                       "parallelism": f"dp{world} (point shards)", "step2": "host (polyhedron + direction cells)"},
+            "discard_pct": round(100 * (1 - surv_total / n_total), 4),
+            "remaining_pct": round(100 * surv_total / n_total, 4),
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": 2 * args.steps, "clocks": clocks.result(),
+            "facets": info["nf"], "mean_cell_candidates": round(info["mean_cand"], 3),
+            "k1_exact_path_points_per_step": int(info["exact"]),
+            "host_step2_and_transfers_ms": round(ms / args.steps - k1 - k2, 4),
+        }), flush=True)
+    if group is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def ctypes_sizeof(t):
+    import ctypes
+
+    return ctypes.sizeof(t)
+
+
 def main():
     args = parse()
     import torch
@@ -138,6 +359,9 @@ def main():
     if world != args.gpus and world > 1:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     import synth
+
+    if args.config in synth.CONFIGS3:
+        return main3(args, world, rank, local)
 
     cfg = dict(synth.CONFIGS[args.config])
     n_total = args.n or cfg.pop("n")

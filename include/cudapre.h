@@ -405,12 +405,15 @@ size_t cudapre3_workspace_bytes(int64_t n_local);
  *   nang, c, s  angle list (host, c[0] = 1, s[0] = 0 required; NULL = preset 0)
  *   d_out       nullable DEVICE cudapre3_extremes_t receiving the result
  *   h_out       nullable HOST result; if given the call blocks until valid
+ *   h_ms_kernel nullable: device time of the K1-3D launch (CUDA events on
+ *               `stream`; the call then blocks)
  * Errors: EMPTY_INPUT (n_local == 0; the empty part, every idx = -1, is still
  * written), NONFINITE_INPUT (result written, flagged), INVALID_ARGUMENT,
  * WORKSPACE, CUDA.  n_local < 2^32.                                        */
 cudapre_status cudapre3_extremes(const float* d_xyz, int64_t n_local, int64_t index_base, int32_t nang,
                                  const double* c, const double* s, void* d_ws, size_t ws_bytes,
-                                 void* stream, cudapre3_extremes_t* d_out, cudapre3_extremes_t* h_out);
+                                 void* stream, cudapre3_extremes_t* d_out, cudapre3_extremes_t* h_out,
+                                 double* h_ms_kernel);
 
 /* Shard merge (host): per slot the lexicographic (key, global index) extreme. */
 cudapre_status cudapre3_extremes_merge(const cudapre3_extremes_t* h_parts, int32_t count,
@@ -427,12 +430,13 @@ cudapre_status cudapre3_polyhedron(const cudapre3_extremes_t* h_ext, cudapre3_po
  *   d_surv_xyz  device float[3*capacity] their coordinates (nullable)
  *   h_count     host: number of survivors (always written on OK / CAPACITY)
  *   h_poly      nullable host copy of the polyhedron used
+ *   h_ms_kernel nullable: device time of the K2-3D launch (CUDA events)
  * Blocks until *h_count is valid.  NONFINITE_INPUT if h_ext is flagged.
  * CAPACITY if *h_count > capacity (the first `capacity` are written).      */
 cudapre_status cudapre3_filter(const float* d_xyz, int64_t n_local, int64_t index_base,
                                const cudapre3_extremes_t* h_ext, int64_t* d_surv_idx, float* d_surv_xyz,
                                int64_t capacity, void* d_ws, size_t ws_bytes, void* stream,
-                               int64_t* h_count, cudapre3_polyhedron_t* h_poly);
+                               int64_t* h_count, cudapre3_polyhedron_t* h_poly, double* h_ms_kernel);
 
 /* Exact orient3d sign of float triples (host; tests and callers): sign of
  * det[b-a; c-a; d-a].                                                       */

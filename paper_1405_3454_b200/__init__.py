@@ -154,10 +154,10 @@ def lib():
     L.cudapre3_workspace_bytes.argtypes = [i64]
     L.cudapre3_workspace_bytes.restype = sz
     L.cudapre3_orient.argtypes = [vp, vp, vp, vp]
-    L.cudapre3_extremes.argtypes = [vp, i64, i64, i32, vp, vp, vp, sz, vp, vp, P(Extremes3T)]
+    L.cudapre3_extremes.argtypes = [vp, i64, i64, i32, vp, vp, vp, sz, vp, vp, P(Extremes3T), vp]
     L.cudapre3_extremes_merge.argtypes = [P(Extremes3T), i32, P(Extremes3T)]
     L.cudapre3_polyhedron.argtypes = [P(Extremes3T), P(Polyhedron3T)]
-    L.cudapre3_filter.argtypes = [vp, i64, i64, P(Extremes3T), vp, vp, i64, vp, sz, vp, P(i64), P(Polyhedron3T)]
+    L.cudapre3_filter.argtypes = [vp, i64, i64, P(Extremes3T), vp, vp, i64, vp, sz, vp, P(i64), P(Polyhedron3T), vp]
     for name in SYMBOLS[2:]:
         if name not in ("cudapre_workspace_bytes", "cudapre_hull_device_bytes", "cudapre3_workspace_bytes"):
             getattr(L, name).restype = ctypes.c_int
@@ -714,18 +714,24 @@ def orient3d(a, b, c, d) -> int:
     return int(lib().cudapre3_orient(*[v.ctypes.data_as(ctypes.c_void_p) for v in q]))
 
 
-def extremes3(pts, angles_="A", index_base: int = 0, ws=None, stream=None, device_out=None) -> Extremes3:
-    """3D Step 1 (P:115 with P:33-35) on the local shard."""
+def extremes3(pts, angles_="A", index_base: int = 0, ws=None, stream=None, device_out=None,
+              timing: list | None = None) -> Extremes3:
+    """3D Step 1 (P:115 with P:33-35) on the local shard.  ``timing``: a list
+    the K1-3D launch's device milliseconds are appended to."""
     pts = _points3(pts)
     n = pts.shape[0]
     nang, c, s = _angle_arrays(angles_)
     w = _workspace3(n, pts.device, ws)
     out = Extremes3T()
+    ms = ctypes.c_double()
     _check(lib().cudapre3_extremes(
         ctypes.c_void_p(pts.data_ptr()), n, index_base, nang,
         c.ctypes.data_as(ctypes.c_void_p), s.ctypes.data_as(ctypes.c_void_p),
         w.ptr, w.nbytes, _stream_ptr(stream),
-        ctypes.c_void_p(device_out.data_ptr()) if device_out is not None else None, ctypes.byref(out)))
+        ctypes.c_void_p(device_out.data_ptr()) if device_out is not None else None, ctypes.byref(out),
+        ctypes.byref(ms) if timing is not None else None))
+    if timing is not None:
+        timing.append(ms.value)
     return Extremes3(out)
 
 
@@ -743,9 +749,10 @@ def polyhedron3(ext: Extremes3) -> Polyhedron:
 
 
 def filter3(pts, ext: Extremes3, index_base: int = 0, return_points: bool = True, ws=None,
-            out_idx=None, out_pts=None, stream=None):
+            out_idx=None, out_pts=None, stream=None, timing: list | None = None):
     """3D Steps 2+3: survivors' global indices (ascending, int64 CUDA tensor),
-    optionally their xyz, and the polyhedron used."""
+    optionally their xyz, and the polyhedron used.  ``timing``: a list the
+    K2-3D launch's device milliseconds are appended to."""
     torch = _torch()
     pts = _points3(pts)
     n = pts.shape[0]
@@ -759,11 +766,15 @@ def filter3(pts, ext: Extremes3, index_base: int = 0, return_points: bool = True
         cap = min(cap, out_pts.shape[0])
     count = ctypes.c_int64()
     poly = Polyhedron3T()
+    ms = ctypes.c_double()
     _check(lib().cudapre3_filter(
         ctypes.c_void_p(pts.data_ptr()), n, index_base, ctypes.byref(ext.raw),
         ctypes.c_void_p(out_idx.data_ptr()),
         ctypes.c_void_p(out_pts.data_ptr()) if out_pts is not None else None,
-        cap, w.ptr, w.nbytes, _stream_ptr(stream), ctypes.byref(count), ctypes.byref(poly)))
+        cap, w.ptr, w.nbytes, _stream_ptr(stream), ctypes.byref(count), ctypes.byref(poly),
+        ctypes.byref(ms) if timing is not None else None))
+    if timing is not None:
+        timing.append(ms.value)
     m = count.value
     return out_idx[:m], (out_pts[:m] if out_pts is not None else None), Polyhedron(poly)
 

@@ -57,6 +57,28 @@ cudapre_status check_ws3(void* d_ws, size_t ws_bytes, int64_t n) {
     return CUDAPRE_OK;
 }
 
+// CUDA events around one launch (per host thread, created on first use)
+struct Timer3 {
+    static thread_local cudaEvent_t ev[2];
+    cudaError_t start(cudaStream_t s) {
+        if (!ev[0]) {
+            cudaError_t e = cudaEventCreate(&ev[0]);
+            if (e == cudaSuccess) e = cudaEventCreate(&ev[1]);
+            if (e != cudaSuccess) return e;
+        }
+        return cudaEventRecord(ev[0], s);
+    }
+    cudaError_t stop(cudaStream_t s, double* ms) {
+        cudaError_t e = cudaEventRecord(ev[1], s);
+        if (e == cudaSuccess) e = cudaEventSynchronize(ev[1]);
+        float f = 0.f;
+        if (e == cudaSuccess) e = cudaEventElapsedTime(&f, ev[0], ev[1]);
+        *ms = f;
+        return e;
+    }
+};
+thread_local cudaEvent_t Timer3::ev[2] = {nullptr, nullptr};
+
 void empty_result3(cudapre3_extremes_t* r, int nang, const double* c, const double* s) {
     std::memset(r, 0, sizeof(*r));
     r->nang = nang;
@@ -76,7 +98,7 @@ int32_t cudapre3_orient(const float* a, const float* b, const float* c, const fl
 
 cudapre_status cudapre3_extremes(const float* d_xyz, int64_t n_local, int64_t index_base, int32_t nang,
                                  const double* c, const double* s, void* d_ws, size_t ws_bytes, void* stream,
-                                 cudapre3_extremes_t* d_out, cudapre3_extremes_t* h_out) {
+                                 cudapre3_extremes_t* d_out, cudapre3_extremes_t* h_out, double* h_ms_kernel) {
     api_fail(CUDAPRE_OK, "");
     double c0[CUDAPRE_MAX_ANGLES], s0[CUDAPRE_MAX_ANGLES];
     if (!c || !s) {
@@ -96,6 +118,7 @@ cudapre_status cudapre3_extremes(const float* d_xyz, int64_t n_local, int64_t in
     cudapre_status st = check_pts3(d_xyz, n_local);
     if (st) return st;
     cudaStream_t strm = (cudaStream_t)stream;
+    if (h_ms_kernel) *h_ms_kernel = 0.0;
     if (n_local == 0) {
         cudapre3_extremes_t r;
         empty_result3(&r, nang, c, s);
@@ -125,7 +148,10 @@ cudapre_status cudapre3_extremes(const float* d_xyz, int64_t n_local, int64_t in
         p.nsf[k] = -(float)s[k];
     }
     int launches = 0;
+    Timer3 tm;
+    if (h_ms_kernel) CUDA_TRY3(tm.start(strm));
     CUDA_TRY3(launch_extremes3(p, stream, &launches));
+    if (h_ms_kernel) CUDA_TRY3(tm.stop(strm, h_ms_kernel));
     if (d_out) CUDA_TRY3(cudaMemcpyAsync(d_out, &p.ws->result, sizeof(cudapre3_extremes_t),
                                          cudaMemcpyDeviceToDevice, strm));
     if (h_out) {
@@ -165,7 +191,7 @@ cudapre_status cudapre3_polyhedron(const cudapre3_extremes_t* h_ext, cudapre3_po
 cudapre_status cudapre3_filter(const float* d_xyz, int64_t n_local, int64_t index_base,
                                const cudapre3_extremes_t* h_ext, int64_t* d_surv_idx, float* d_surv_xyz,
                                int64_t capacity, void* d_ws, size_t ws_bytes, void* stream, int64_t* h_count,
-                               cudapre3_polyhedron_t* h_poly) {
+                               cudapre3_polyhedron_t* h_poly, double* h_ms_kernel) {
     api_fail(CUDAPRE_OK, "");
     if (!h_ext || !h_count) return fail3(CUDAPRE_ERR_INVALID_ARGUMENT, "h_ext / h_count is NULL");
     if (h_ext->nonfinite) return fail3(CUDAPRE_ERR_NONFINITE_INPUT, "the extremes saw a non-finite coordinate");
@@ -185,6 +211,7 @@ cudapre_status cudapre3_filter(const float* d_xyz, int64_t n_local, int64_t inde
     if (rc) return fail3((cudapre_status)rc, "polyhedron build failed");
     cudaStream_t strm = (cudaStream_t)stream;
     *h_count = 0;
+    if (h_ms_kernel) *h_ms_kernel = 0.0;
     if (n_local == 0) return CUDAPRE_OK;
     CUDA_TRY3(cudaMemcpyAsync(ws3_geom(d_ws), g, sizeof(K3Geom), cudaMemcpyHostToDevice, strm));
     K23Params p;
@@ -201,7 +228,10 @@ cudapre_status cudapre3_filter(const float* d_xyz, int64_t n_local, int64_t inde
     p.status = ws3_status(d_ws);
     p.num_tiles = (unsigned)ws3_tiles(n_local);
     int launches = 0;
+    Timer3 tm;
+    if (h_ms_kernel) CUDA_TRY3(tm.start(strm));
     CUDA_TRY3(launch_filter3(p, stream, &launches));
+    if (h_ms_kernel) CUDA_TRY3(tm.stop(strm, h_ms_kernel));
     CUDA_TRY3(cudaMemcpyAsync(stage, &p.ws->count, sizeof(unsigned long long), cudaMemcpyDeviceToHost, strm));
     CUDA_TRY3(cudaStreamSynchronize(strm));
     unsigned long long cnt;
