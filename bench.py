@@ -222,11 +222,7 @@ def main3(args, world, rank, local):
         ext = cp.extremes3(pts, args.angles, index_base=base, ws=ws, device_out=ext_dev,
                            timing=k1_ms if timed else None)
         if group is not None:   # cross-rank combine of the Step-1 blocks (as 2D a3)
-            g = torch.empty(world * ext_dev.numel(), dtype=torch.uint8, device="cuda")
-            dist.all_gather_into_tensor(g, ext_dev, group=group)
-            raw = g.cpu().numpy().tobytes()
-            sz = ext_dev.numel()
-            ext = cp.merge3([cp.Extremes3T.from_buffer_copy(raw[r * sz:(r + 1) * sz]) for r in range(world)])
+            ext = cp.exchange3(ext, group, device_buf=ext_dev)
         idx, _, poly = cp.filter3(pts, ext, index_base=base, ws=ws, out_idx=out_idx, out_pts=out_pts,
                                   return_points=out_pts is not None, timing=k2_ms if timed else None)
         info.update(surv=idx.shape[0], nf=poly.nf, exact=ext.raw.exact_points,

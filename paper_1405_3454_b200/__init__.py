@@ -735,6 +735,28 @@ def extremes3(pts, angles_="A", index_base: int = 0, ws=None, stream=None, devic
     return Extremes3(out)
 
 
+def exchange3(local, group, device_buf=None) -> Extremes3:
+    """Cross-rank combine in 3D: all-gather every rank's Step-1 struct (NCCL:
+    from the device buffer K1-3D wrote via ``device_out``; gloo: host bytes)
+    and merge them with the library's lexicographic rule."""
+    torch = _torch()
+    import torch.distributed as dist
+
+    raw_local = local.raw if isinstance(local, Extremes3) else local
+    nbytes = ctypes.sizeof(Extremes3T)
+    world = dist.get_world_size(group)
+    if device_buf is not None:
+        gathered = torch.empty(world * nbytes, dtype=torch.uint8, device=device_buf.device)
+        dist.all_gather_into_tensor(gathered, device_buf, group=group)
+        host = gathered.cpu().numpy().tobytes()
+    else:
+        mine = torch.frombuffer(bytearray(bytes(raw_local)), dtype=torch.uint8)
+        bufs = [torch.empty(nbytes, dtype=torch.uint8) for _ in range(world)]
+        dist.all_gather(bufs, mine, group=group)
+        host = b"".join(bytes(b.numpy().tobytes()) for b in bufs)
+    return merge3([Extremes3T.from_buffer_copy(host[r * nbytes:(r + 1) * nbytes]) for r in range(world)])
+
+
 def merge3(parts) -> Extremes3:
     arr = (Extremes3T * len(parts))(*[p.raw if isinstance(p, Extremes3) else p for p in parts])
     out = Extremes3T()

@@ -65,3 +65,51 @@ def test_two_rank_exchange_matches_single(cuts, oracle_lib):
         assert n == N
         assert idx == want["ext_idx"].tolist(), rank
         assert ring == want["ring"].tolist(), rank
+
+
+def _worker3(rank, world, port, cuts, out_q):
+    import sys
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import paper_1405_3454_b200 as cp
+    import synth
+    from tests.test_abi3 import _ext3_from_oracle
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    try:
+        lo, hi = cuts[rank], cuts[rank + 1]
+        xyz = np.round(synth.generate3("ball", hi - lo, seed=6, base=lo) * 32).astype(np.float32)   # ties
+        local = _ext3_from_oracle(xyz, "A")
+        for j in range(24):
+            if local.raw.idx[j] >= 0:
+                local.raw.idx[j] += lo
+        merged = cp.exchange3(local, dist.group.WORLD)
+        poly = cp.polyhedron3(merged)
+        out_q.put((rank, merged.idx.tolist(), poly.facets.tolist(), merged.n))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("cuts", [[0, 17_000, N], [0, 1, N]])
+def test_two_rank_exchange3_matches_single(cuts, oracle_lib):
+    """3D: the all-gathered, merged Step-1 structs equal the oracle's
+    single-set picks on every rank, and so do the facets built from them."""
+    import synth
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker3, args=(r, 2, port, cuts, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    xyz = np.round(synth.generate3("ball", N, seed=6) * 32).astype(np.float32)
+    want = oracle_lib.cudapre3(xyz, "A")
+    for rank, idx, facets, n in res:
+        assert n == N
+        assert idx == want["ext_idx"].tolist(), rank
+        assert facets == want["facets"].tolist(), rank
