@@ -21,7 +21,7 @@ constexpr int kMaxK13Blocks = 148 * 8;
 constexpr int kK23Threads = 256;              // K2-3D block
 constexpr int kK23TileQuads = 2 * kK23Threads;              // 512 quads
 constexpr int kK23TilePts = 4 * kK23TileQuads;              // 2048 points (24 KiB) per tile
-constexpr int kK23BlocksPerSM = 3;
+constexpr int kK23BlocksPerSM = 3;   // ~60 KiB of shared memory each (cell lists + staging)
 constexpr int kStatus3Stride = 16;            // one 8-byte status word per 128-byte line
 
 // ---------------------------------------------------------------- workspace

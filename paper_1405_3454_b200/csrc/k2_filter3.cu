@@ -25,7 +25,8 @@
 // block scan orders the survivors; warp 0 resolves the tile's exclusive
 // prefix by a decoupled look-back over epoch-tagged status words (one per
 // 128-byte line), deferred by one tile so that it never waits; survivors'
-// int64 index (+ xyz, kept in registers) are written in order.
+// int64 index (+ xyz) are staged in shared memory and written in order with
+// coalesced stores.
 #include <cuda_runtime.h>
 
 #include <cfloat>
@@ -56,6 +57,9 @@ struct Smem3 {
     unsigned tile[2];
     unsigned total[2];
     unsigned long long ex;
+    // the previous tile's survivors, compacted in order: tile-local index + xyz
+    unsigned sidx[kK23TilePts];
+    float spts[3 * kK23TilePts];
 };
 
 __device__ __forceinline__ void st_status(unsigned long long* a, unsigned long long v) {
@@ -202,20 +206,14 @@ __device__ __forceinline__ unsigned load_quad(const float* __restrict__ pts, uns
     return valid;
 }
 
-// Write one quad's survivors (coordinates v) from position pos on.
-__device__ __forceinline__ void emit(const K23Params& p, const float (&v)[12], unsigned bits, unsigned q,
-                                     unsigned long long pos) {
-    const unsigned i0 = 4u * q;
+// Stage one quad's survivors (coordinates v) at tile-local positions from pos on.
+__device__ __forceinline__ void stage(Smem3& g, const float (&v)[12], unsigned bits, unsigned local_q,
+                                      unsigned pos) {
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
         if ((bits >> e) & 1u) {
-            if (pos < p.capacity) {
-                p.out_idx[pos] = p.base + (long long)(i0 + e);
-                if (p.out_pts) {
-                    float* o = p.out_pts + 3ull * pos;
-                    o[0] = v[3 * e], o[1] = v[3 * e + 1], o[2] = v[3 * e + 2];
-                }
-            }
+            g.sidx[pos] = 4u * local_q + e;
+            g.spts[3 * pos] = v[3 * e], g.spts[3 * pos + 1] = v[3 * e + 1], g.spts[3 * pos + 2] = v[3 * e + 2];
             ++pos;
         }
     }
@@ -223,7 +221,8 @@ __device__ __forceinline__ void emit(const K23Params& p, const float (&v)[12], u
 
 template <bool VEC>
 __global__ void __launch_bounds__(kK23Threads, kK23BlocksPerSM) k2_filter3(const __grid_constant__ K23Params p) {
-    __shared__ Smem3 g;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Smem3& g = *reinterpret_cast<Smem3*>(smem_raw);
     const unsigned tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
     const K3Geom* G = p.g;
     for (int t = tid; t < kCells; t += kK23Threads) g.clist[t] = G->clist[t];
@@ -247,14 +246,14 @@ __global__ void __launch_bounds__(kK23Threads, kK23BlocksPerSM) k2_filter3(const
     // Deferred look-back (as the 2D kernel): tile k's aggregate is published
     // right after its scan, but its prefix is resolved only after tile k+1 has
     // been classified, when every predecessor has long published its own
-    // aggregate — no spinning.  Tile k's keep bits and in-warp offsets stay in
-    // registers; its warp bases and total in shared memory (double-buffered).
+    // aggregate — no spinning.  Tile k's survivors wait compacted in shared
+    // memory (tile-local index + xyz) and are then written with fully
+    // coalesced stores; its total lives in shared memory (double-buffered).
     // L2 prefetch one wave ahead: the tile gridDim.x after the claimed one is
     // about the one some block claims next (no ticket is held early).
     const unsigned full_tiles = p.n / kK23TilePts;
     bool have_prev = false;
-    unsigned prev_tile = 0, pb0 = 0, pb1 = 0, pexcl = 0;
-    float pv0[12], pv1[12];   // the previous tile's quads (emitted one tile later)
+    unsigned prev_tile = 0;
     int par = 0;
     for (;;) {
         if (tid == 0) {
@@ -320,18 +319,29 @@ __global__ void __launch_bounds__(kK23Threads, kK23BlocksPerSM) k2_filter3(const
             }
         }
         __syncthreads();
-        if (have_prev) {
+        if (have_prev) {   // the previous tile's survivors: coalesced stores from the staging area
             const unsigned long long ex = g.ex;
-            const unsigned wb = g.wbase[par ^ 1][warp], lo_tot = g.total[par ^ 1] & 0xffffu;
-            const unsigned pq0 = prev_tile * kK23TileQuads + tid;
-            emit(p, pv0, pb0, pq0, ex + (wb & 0xffffu) + (pexcl & 0xffffu));
-            emit(p, pv1, pb1, pq0 + kK23Threads, ex + lo_tot + (wb >> 16) + (pexcl >> 16));
+            const unsigned tot = g.total[par ^ 1];
+            const unsigned total = (tot & 0xffffu) + (tot >> 16);
+            const long long gbase = p.base + (long long)prev_tile * kK23TilePts;
+            const unsigned long long cap = p.capacity > ex ? p.capacity - ex : 0ull;
+            const unsigned lim = (unsigned)(cap < total ? cap : total);
+            for (unsigned j = tid; j < lim; j += kK23Threads) p.out_idx[ex + j] = gbase + g.sidx[j];
+            if (p.out_pts) {
+                float* o = p.out_pts + 3ull * ex;
+                for (unsigned j = tid; j < 3u * lim; j += kK23Threads) o[j] = g.spts[j];
+            }
         }
         if (!live) break;
+        __syncthreads();   // the staging area is free
+        {
+            const unsigned wb = g.wbase[par][warp], lo_tot = g.total[par] & 0xffffu;
+            const unsigned excl = incl - c;
+            stage(g, v0, b0, tid, (wb & 0xffffu) + (excl & 0xffffu));
+            stage(g, v1, b1, tid + kK23Threads, lo_tot + (wb >> 16) + (excl >> 16));
+        }
         have_prev = true;
-        prev_tile = tile, pb0 = b0, pb1 = b1, pexcl = incl - c;
-#pragma unroll
-        for (int j = 0; j < 12; ++j) pv0[j] = v0[j], pv1[j] = v1[j];
+        prev_tile = tile;
         par ^= 1;
     }
     nexact = __reduce_add_sync(kFull, nexact);
@@ -354,10 +364,16 @@ int launch_filter3(const K23Params& p, void* stream, int* launches) {
     if (blocks > p.num_tiles) blocks = p.num_tiles;
     if (blocks == 0) blocks = 1;
     cudaStream_t s = (cudaStream_t)stream;
+    static bool attr = false;
+    if (!attr) {   // the staging area takes the block past the 48 KB static limit
+        cudaFuncSetAttribute(k2_filter3<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem3));
+        cudaFuncSetAttribute(k2_filter3<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem3));
+        attr = true;
+    }
     if (p.vec)
-        k2_filter3<true><<<blocks, kK23Threads, 0, s>>>(p);
+        k2_filter3<true><<<blocks, kK23Threads, sizeof(Smem3), s>>>(p);
     else
-        k2_filter3<false><<<blocks, kK23Threads, 0, s>>>(p);
+        k2_filter3<false><<<blocks, kK23Threads, sizeof(Smem3), s>>>(p);
     *launches += 1;
     return (int)cudaGetLastError();
 }
