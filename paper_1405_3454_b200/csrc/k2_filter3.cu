@@ -133,27 +133,11 @@ __device__ __forceinline__ float rcp_approx(float a) {
     return r;
 }
 
-// the exact decision over the candidate facets (rare path)
-__device__ __noinline__ bool keep_exact(const Smem3& g, float x, float y, float z, unsigned long long mask,
-                                        unsigned* nexact) {
-    if (!(fabsf(x) <= FLT_MAX && fabsf(y) <= FLT_MAX && fabsf(z) <= FLT_MAX)) return true;
-    ++*nexact;
-    const float q[3] = {x, y, z};
-    for (; mask; mask &= mask - 1ull) {
-        const int t = __ffsll((long long)mask) - 1;
-        const float4 P = g.pl[t];
-        const float v = __fmaf_rn(P.x, x, __fmaf_rn(P.y, y, __fmaf_rn(P.z, z, P.w)));
-        const float E = g.pe[t];
-        if (v < -E) return true;
-        if (v > E) continue;
-        const float* f = g.fv[t];
-        if (orient3d_sign_f(f, f + 3, f + 6, q) <= 0) return true;
-    }
-    return false;
-}
-
-__device__ __forceinline__ bool keep_pt(const Smem3& g, const K3Geom* __restrict__ G, float x, float y, float z,
-                                        unsigned* nexact) {
+// Fast test of one point: 0 = discard, 1 = keep, 2 = slow (a long candidate
+// list, an undecided plane test, or no cell); `mask` then holds the
+// candidate facets for the warp-cooperative pass.
+__device__ __forceinline__ int classify_fast(const Smem3& g, const K3Geom* __restrict__ G, float x, float y,
+                                             float z, unsigned long long& mask) {
     const float dx = __fsub_rn(x, g.ox), dy = __fsub_rn(y, g.oy), dz = __fsub_rn(z, g.oz);
     const float ax = fabsf(dx), ay = fabsf(dy), az = fabsf(dz);
     const bool xm = ax >= ay && ax >= az;
@@ -169,9 +153,10 @@ __device__ __forceinline__ bool keep_pt(const Smem3& g, const K3Geom* __restrict
     const int cell = (face * kCellG + (int)fu) * kCellG + (int)fv;
     const bool ok = am >= 0x1p-100f;   // false for NaN and for directions too short for the reciprocal
     const unsigned w = g.clist[ok ? cell : 0];
-    if (!ok || (w >> 24) > (unsigned)kCellSlots) {   // long list (or no cell): walk the mask
+    if (!ok || (w >> 24) > (unsigned)kCellSlots) {   // long list (or no cell)
         const unsigned li = w & 0xffffffu;
-        return keep_exact(g, x, y, z, (ok && li != kNoLong) ? __ldg(&G->lmask[li]) : g.all, nexact);
+        mask = (ok && li != kNoLong) ? __ldg(&G->lmask[li]) : g.all;
+        return 2;
     }
     bool out = false, unsure = false;
     unsigned long long cand = 0;
@@ -185,9 +170,37 @@ __device__ __forceinline__ bool keep_pt(const Smem3& g, const K3Geom* __restrict
         unsure |= !(val > E);
         cand |= (t < (unsigned)kMax3Facets) ? (1ull << t) : 0ull;
     }
-    if (out) return true;
-    if (!unsure) return false;
-    return keep_exact(g, x, y, z, cand, nexact);
+    mask = cand;
+    return out ? 1 : (unsure ? 2 : 0);
+}
+
+// The slow decision for one point, by the whole warp (x, y, z, mask uniform):
+// lane j takes the j-th candidate facet — float test, exact orient3d when the
+// float test cannot decide — and the warp votes.  Non-finite points are kept.
+__device__ __noinline__ bool slow_coop(const Smem3& g, float x, float y, float z, unsigned long long mask,
+                                       unsigned lane, unsigned* nexact) {
+    bool out = !(fabsf(x) <= FLT_MAX && fabsf(y) <= FLT_MAX && fabsf(z) <= FLT_MAX);
+    const unsigned lo = (unsigned)mask, hi = (unsigned)(mask >> 32);
+    const int nlo = __popc(lo), n = nlo + __popc(hi);
+    const float q[3] = {x, y, z};
+    for (int base = 0; base < n && !out; base += 32) {
+        const int j = base + (int)lane;
+        if (j < n) {
+            const int t = j < nlo ? (int)__fns(lo, 0, j + 1) : 32 + (int)__fns(hi, 0, j - nlo + 1);
+            const float4 P = g.pl[t];
+            const float E = g.pe[t];
+            const float val = __fmaf_rn(P.x, x, __fmaf_rn(P.y, y, __fmaf_rn(P.z, z, P.w)));
+            if (val < -E) {
+                out = true;
+            } else if (!(val > E)) {
+                ++*nexact;
+                const float* f = g.fv[t];
+                out = orient3d_sign_f(f, f + 3, f + 6, q) <= 0;
+            }
+        }
+        out = __any_sync(kFull, out);
+    }
+    return out;
 }
 
 template <bool VEC>
@@ -271,12 +284,33 @@ __global__ void __launch_bounds__(kK23Threads, kK23BlocksPerSM) k2_filter3(const
         if (live) {
             const unsigned n0 = load_quad<VEC>(p.pts, q0, p.n, v0);
             const unsigned n1 = load_quad<VEC>(p.pts, q1, p.n, v1);
+            if (keep_all) {
+                b0 = (1u << n0) - 1u;
+                b1 = (1u << n1) - 1u;
+            } else {
+                auto classify_quad = [&](const float(&v)[12], unsigned nv) -> unsigned {
+                    unsigned bits = 0;
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                if ((unsigned)e < n0 && (keep_all || keep_pt(g, G, v0[3 * e], v0[3 * e + 1], v0[3 * e + 2], &nexact)))
-                    b0 |= 1u << e;
-                if ((unsigned)e < n1 && (keep_all || keep_pt(g, G, v1[3 * e], v1[3 * e + 1], v1[3 * e + 2], &nexact)))
-                    b1 |= 1u << e;
+                    for (int e = 0; e < 4; ++e) {
+                        unsigned long long mask = 0;
+                        const int st =
+                            (unsigned)e < nv ? classify_fast(g, G, v[3 * e], v[3 * e + 1], v[3 * e + 2], mask) : 0;
+                        bits |= (st == 1 ? 1u : 0u) << e;
+                        // slow points of this element, one at a time by the whole warp
+                        for (unsigned slow = __ballot_sync(kFull, st == 2); slow; slow &= slow - 1u) {
+                            const int src = __ffs(slow) - 1;
+                            const float sx = __shfl_sync(kFull, v[3 * e], src);
+                            const float sy = __shfl_sync(kFull, v[3 * e + 1], src);
+                            const float sz = __shfl_sync(kFull, v[3 * e + 2], src);
+                            const unsigned long long sm = __shfl_sync(kFull, mask, src);
+                            const bool k = slow_coop(g, sx, sy, sz, sm, lane, &nexact);
+                            if ((int)lane == src && k) bits |= 1u << e;
+                        }
+                    }
+                    return bits;
+                };
+                b0 = classify_quad(v0, n0);
+                b1 = classify_quad(v1, n1);
             }
             // packed scan: low half = first 256 quads, high half = second 256
             c = (unsigned)__popc(b0) | ((unsigned)__popc(b1) << 16);
