@@ -9,13 +9,14 @@
 // exactly on the host), the ray from o through p leaves the polyhedron
 // through a facet whose face contains the ray's direction; p is strictly
 // inside iff it is strictly inside that facet.  The direction d = RN(p - o)
-// selects one of 1536 cube-map cells (major axis, sign, and the two other
-// components over the major one on a 16 x 16 grid; one approximate
+// selects one of 6144 cube-map cells (major axis, sign, and the two other
+// components over the major one on a 32 x 32 grid; one approximate
 // reciprocal), and the host lists, per cell, every facet whose face meets the
 // cell's direction pyramid widened by a guard far larger than the kernel's
-// rounding — about 2 of ~32 on average.  Lists of up to 3
-// are tested branch-free (unused slots: a plane that always says "inside"),
-// longer ones walk the cell's facet mask:
+// rounding — about 1.2 of ~32 on average.  Lists of up to
+// 3 are tested branch-free (unused slots: a plane that always says
+// "inside"); longer lists and undecided tests go to a warp-cooperative pass
+// (the whole warp splits one point's candidate facets and votes):
 //   g = fma(A, x, fma(B, y, fma(C, z, D))), |g - orient3d| <= E over the
 //   data bounding box:   g < -E on any candidate -> keep;  g > E on all ->
 //   discard;  otherwise the exact orient3d (exact3.cuh) on the undecided ones.
