@@ -19,9 +19,13 @@ constexpr int kK13Threads = 256;              // K1-3D block
 constexpr int kK13Quads = 2;                  // quads (4 points, 48 B) per thread per iteration
 constexpr int kMaxK13Blocks = 148 * 8;
 constexpr int kK23Threads = 256;              // K2-3D block
-constexpr int kK23TileQuads = 2 * kK23Threads;              // 512 quads
+#ifndef K23_QUADS
+#define K23_QUADS 2
+#endif
+constexpr int kK23Quads = K23_QUADS;                         // quads per thread per tile (2 or 4)
+constexpr int kK23TileQuads = kK23Quads * kK23Threads;
 constexpr int kK23TilePts = 4 * kK23TileQuads;              // 2048 points (24 KiB) per tile
-constexpr int kK23BlocksPerSM = 3;   // ~60 KiB of shared memory each (cell lists + staging)
+constexpr int kK23BlocksPerSM = kK23Quads == 2 ? 3 : 2;     // shared memory: cell lists + staging
 constexpr int kStatus3Stride = 16;            // one 8-byte status word per 128-byte line
 
 // ---------------------------------------------------------------- workspace

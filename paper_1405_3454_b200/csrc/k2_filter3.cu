@@ -21,9 +21,9 @@
 //   data bounding box:   g < -E on any candidate -> keep;  g > E on all ->
 //   discard;  otherwise the exact orient3d (exact3.cuh) on the undecided ones.
 // A direction too short for the reciprocal (or NaN) takes every facet.
-// Compaction: persistent blocks take 2048-point tiles (24 KiB) from an atomic
-// ticket; each thread classifies two quads (8 points); a packed two-half
-// block scan orders the survivors; warp 0 resolves the tile's exclusive
+// Compaction: persistent blocks take tiles of kK23Quads * 1024 points from an
+// atomic ticket; each thread classifies kK23Quads quads; packed (two 16-bit
+// halves per word) block scans order the survivors; warp 0 resolves the tile's exclusive
 // prefix by a decoupled look-back over epoch-tagged status words (one per
 // 128-byte line), deferred by one tile so that it never waits; survivors'
 // int64 index (+ xyz) are staged in shared memory and written in order with
@@ -53,10 +53,10 @@ struct Smem3 {
     unsigned long long all;
     float ox, oy, oz;
     int mode;
-    unsigned wsum[kWarps];
-    unsigned wbase[2][kWarps];
+    unsigned wsum[kK23Quads / 2][kWarps];
+    unsigned wbase[2][kK23Quads / 2][kWarps];
     unsigned tile[2];
-    unsigned total[2];
+    unsigned total[2][kK23Quads / 2];
     unsigned long long ex;
     // the previous tile's survivors, compacted in order: tile-local index + xyz
     unsigned sidx[kK23TilePts];
@@ -279,72 +279,89 @@ __global__ void __launch_bounds__(kK23Threads, kK23BlocksPerSM) k2_filter3(const
         __syncthreads();
         const unsigned tile = g.tile[par];
         const bool live = tile < p.num_tiles;
-        unsigned b0 = 0, b1 = 0, c = 0, incl = 0;
-        const unsigned q0 = tile * kK23TileQuads + tid, q1 = q0 + kK23Threads;
-        float v0[12], v1[12];
+        constexpr int kP = kK23Quads / 2;   // packed scan words: two quad slots each (16-bit halves)
+        unsigned bits[kK23Quads], c[kP], incl[kP];
+        float v[kK23Quads][12];
+#pragma unroll
+        for (int h = 0; h < kK23Quads; ++h) bits[h] = 0;
+#pragma unroll
+        for (int w = 0; w < kP; ++w) c[w] = incl[w] = 0;
         if (live) {
-            const unsigned n0 = load_quad<VEC>(p.pts, q0, p.n, v0);
-            const unsigned n1 = load_quad<VEC>(p.pts, q1, p.n, v1);
+            unsigned nv[kK23Quads];
+#pragma unroll
+            for (int h = 0; h < kK23Quads; ++h)
+                nv[h] = load_quad<VEC>(p.pts, tile * kK23TileQuads + h * kK23Threads + tid, p.n, v[h]);
             if (keep_all) {
-                b0 = (1u << n0) - 1u;
-                b1 = (1u << n1) - 1u;
+#pragma unroll
+                for (int h = 0; h < kK23Quads; ++h) bits[h] = (1u << nv[h]) - 1u;
             } else {
-                auto classify_quad = [&](const float(&v)[12], unsigned nv) -> unsigned {
-                    unsigned bits = 0;
+                auto classify_quad = [&](const float(&q)[12], unsigned n) -> unsigned {
+                    unsigned b = 0;
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
                         unsigned long long mask = 0;
                         const int st =
-                            (unsigned)e < nv ? classify_fast(g, G, v[3 * e], v[3 * e + 1], v[3 * e + 2], mask) : 0;
-                        bits |= (st == 1 ? 1u : 0u) << e;
+                            (unsigned)e < n ? classify_fast(g, G, q[3 * e], q[3 * e + 1], q[3 * e + 2], mask) : 0;
+                        b |= (st == 1 ? 1u : 0u) << e;
                         // slow points of this element, one at a time by the whole warp
                         for (unsigned slow = __ballot_sync(kFull, st == 2); slow; slow &= slow - 1u) {
                             const int src = __ffs(slow) - 1;
-                            const float sx = __shfl_sync(kFull, v[3 * e], src);
-                            const float sy = __shfl_sync(kFull, v[3 * e + 1], src);
-                            const float sz = __shfl_sync(kFull, v[3 * e + 2], src);
+                            const float sx = __shfl_sync(kFull, q[3 * e], src);
+                            const float sy = __shfl_sync(kFull, q[3 * e + 1], src);
+                            const float sz = __shfl_sync(kFull, q[3 * e + 2], src);
                             const unsigned long long sm = __shfl_sync(kFull, mask, src);
                             const bool k = slow_coop(g, sx, sy, sz, sm, lane, &nexact);
-                            if ((int)lane == src && k) bits |= 1u << e;
+                            if ((int)lane == src && k) b |= 1u << e;
                         }
                     }
-                    return bits;
+                    return b;
                 };
-                b0 = classify_quad(v0, n0);
-                b1 = classify_quad(v1, n1);
-            }
-            // packed scan: low half = first 256 quads, high half = second 256
-            c = (unsigned)__popc(b0) | ((unsigned)__popc(b1) << 16);
-            incl = c;
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const unsigned t = __shfl_up_sync(kFull, incl, o);
-                if (lane >= (unsigned)o) incl += t;
+                for (int h = 0; h < kK23Quads; ++h) bits[h] = classify_quad(v[h], nv[h]);
             }
-            if (lane == 31) g.wsum[warp] = incl;
+            // packed scans: word w = quad slots 2w (low half) and 2w+1 (high half)
+#pragma unroll
+            for (int w = 0; w < kP; ++w) {
+                c[w] = (unsigned)__popc(bits[2 * w]) | ((unsigned)__popc(bits[2 * w + 1]) << 16);
+                incl[w] = c[w];
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const unsigned t = __shfl_up_sync(kFull, incl[w], o);
+                    if (lane >= (unsigned)o) incl[w] += t;
+                }
+                if (lane == 31) g.wsum[w][warp] = incl[w];
+            }
         }
         __syncthreads();
         if (warp == 0) {
             if (live) {
-                const unsigned ws = lane < kWarps ? g.wsum[lane] : 0u;
-                unsigned wi = ws;
+                unsigned total = 0;
 #pragma unroll
-                for (int o = 1; o < kWarps; o <<= 1) {
-                    const unsigned t = __shfl_up_sync(kFull, wi, o);
-                    if (lane >= (unsigned)o) wi += t;
+                for (int w = 0; w < kP; ++w) {
+                    const unsigned ws = lane < kWarps ? g.wsum[w][lane] : 0u;
+                    unsigned wi = ws;
+#pragma unroll
+                    for (int o = 1; o < kWarps; o <<= 1) {
+                        const unsigned t = __shfl_up_sync(kFull, wi, o);
+                        if (lane >= (unsigned)o) wi += t;
+                    }
+                    const unsigned tot = __shfl_sync(kFull, wi, kWarps - 1);
+                    if (lane < kWarps) g.wbase[par][w][lane] = wi - ws;
+                    if (lane == 0) g.total[par][w] = tot;
+                    total += (tot & 0xffffu) + (tot >> 16);
                 }
-                const unsigned tot = __shfl_sync(kFull, wi, kWarps - 1);
-                if (lane < kWarps) g.wbase[par][lane] = wi - ws;
                 if (lane == 0) {
-                    g.total[par] = tot;
-                    const unsigned total = (tot & 0xffffu) + (tot >> 16);
                     publish(p, tile, tile == 0 ? kFlagP : kFlagA, total, epoch);
                     if (tile == 0 && tile == p.num_tiles - 1) p.ws->count = total;
                 }
             }
             if (have_prev) {
-                const unsigned tot = g.total[par ^ 1];
-                const unsigned total = (tot & 0xffffu) + (tot >> 16);
+                unsigned total = 0;
+#pragma unroll
+                for (int w = 0; w < kP; ++w) {
+                    const unsigned tot = g.total[par ^ 1][w];
+                    total += (tot & 0xffffu) + (tot >> 16);
+                }
                 const unsigned long long ex = prev_tile == 0 ? 0ull : resolve(p, prev_tile, epoch, lane);
                 if (lane == 0) {
                     if (prev_tile != 0) publish(p, prev_tile, kFlagP, ex + total, epoch);
@@ -356,8 +373,12 @@ __global__ void __launch_bounds__(kK23Threads, kK23BlocksPerSM) k2_filter3(const
         __syncthreads();
         if (have_prev) {   // the previous tile's survivors: coalesced stores from the staging area
             const unsigned long long ex = g.ex;
-            const unsigned tot = g.total[par ^ 1];
-            const unsigned total = (tot & 0xffffu) + (tot >> 16);
+            unsigned total = 0;
+#pragma unroll
+            for (int w = 0; w < kP; ++w) {
+                const unsigned tot = g.total[par ^ 1][w];
+                total += (tot & 0xffffu) + (tot >> 16);
+            }
             const long long gbase = p.base + (long long)prev_tile * kK23TilePts;
             const unsigned long long cap = p.capacity > ex ? p.capacity - ex : 0ull;
             const unsigned lim = (unsigned)(cap < total ? cap : total);
@@ -370,10 +391,15 @@ __global__ void __launch_bounds__(kK23Threads, kK23BlocksPerSM) k2_filter3(const
         if (!live) break;
         __syncthreads();   // the staging area is free
         {
-            const unsigned wb = g.wbase[par][warp], lo_tot = g.total[par] & 0xffffu;
-            const unsigned excl = incl - c;
-            stage(g, v0, b0, tid, (wb & 0xffffu) + (excl & 0xffffu));
-            stage(g, v1, b1, tid + kK23Threads, lo_tot + (wb >> 16) + (excl >> 16));
+            unsigned slot_base = 0;
+#pragma unroll
+            for (int h = 0; h < kK23Quads; ++h) {
+                const int w = h >> 1, sh = 16 * (h & 1);
+                const unsigned wb = (g.wbase[par][w][warp] >> sh) & 0xffffu;
+                const unsigned ex = ((incl[w] - c[w]) >> sh) & 0xffffu;
+                stage(g, v[h], bits[h], h * kK23Threads + tid, slot_base + wb + ex);
+                slot_base += (g.total[par][w] >> sh) & 0xffffu;
+            }
         }
         have_prev = true;
         prev_tile = tile;
