@@ -226,7 +226,7 @@ def main3(args, world, rank, local):
         idx, _, poly = cp.filter3(pts, ext, index_base=base, ws=ws, out_idx=out_idx, out_pts=out_pts,
                                   return_points=out_pts is not None, timing=k2_ms if timed else None)
         info.update(surv=idx.shape[0], nf=poly.nf, exact=ext.raw.exact_points,
-                    mean_cand=poly.raw.n_entries / (6 * 32 * 32), long_cells=poly.raw.long_cells)
+                    mean_cand=poly.raw.n_entries / max(1, poly.raw.n_cells), long_cells=poly.raw.long_cells)
 
     for _ in range(args.warmup):
         step(False)

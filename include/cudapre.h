@@ -393,7 +393,8 @@ typedef struct {
     float err_max;                              /* largest plane-test error bound */
     int32_t max_candidates;                     /* largest candidate list of a cell */
     int32_t long_cells;                         /* cells whose list exceeds the kernel's 3 slots */
-    int32_t pad[6];
+    int32_t n_cells;                            /* direction cells (6 * 32 * 32) */
+    int32_t pad[5];
 } cudapre3_polyhedron_t;
 
 /* Workspace bytes for a shard of n_local points (3D). */

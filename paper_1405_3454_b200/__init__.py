@@ -96,7 +96,8 @@ class Polyhedron3T(ctypes.Structure):
                 ("n_entries", ctypes.c_int32), ("eidx", ctypes.c_int64 * MAX_SLOTS3),
                 ("fidx", (ctypes.c_int64 * 3) * MAX_FACETS3), ("fv", (Pt3 * 3) * MAX_FACETS3),
                 ("centre", ctypes.c_float * 3), ("err_max", ctypes.c_float),
-                ("max_candidates", ctypes.c_int32), ("long_cells", ctypes.c_int32), ("pad", ctypes.c_int32 * 6)]
+                ("max_candidates", ctypes.c_int32), ("long_cells", ctypes.c_int32), ("n_cells", ctypes.c_int32),
+                ("pad", ctypes.c_int32 * 5)]
 
 
 SYMBOLS = ["cudapre_version", "cudapre_last_error", "cudapre_angles_preset",

@@ -301,6 +301,7 @@ int build_polyhedron3(const cudapre3_extremes_t& ext, cudapre3_polyhedron_t* pol
     }
     P.n_entries = nent;
     P.max_candidates = mx;
+    P.n_cells = kCells;
     if (poly) *poly = P;
     return 0;
 }
