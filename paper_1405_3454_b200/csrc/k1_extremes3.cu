@@ -27,6 +27,10 @@
 
 #include "internal3.h"
 
+#ifndef K13_AHEAD
+#define K13_AHEAD 2   // L2 prefetch distance, in warp steps
+#endif
+
 namespace cudapre {
 namespace {
 
@@ -215,7 +219,7 @@ __global__ void __launch_bounds__(kK13Threads, 2) k1_extremes3(const __grid_cons
     // (16-B aligned input only), which doubles the bytes in flight at no
     // register cost
     constexpr unsigned kStep = 32u * kK13Quads;
-    constexpr int kAhead = 2;
+    constexpr int kAhead = K13_AHEAD;
     const unsigned gstep = gwarps * kStep;
     if (VEC && lane == 0)
         for (int a = 1; a < kAhead; ++a) {
