@@ -4,6 +4,7 @@
 // Compiled with -ffp-contract=off.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -237,6 +238,7 @@ int build_polyhedron3(const cudapre3_extremes_t& ext, cudapre3_polyhedron_t* pol
     bool inside = std::isfinite(o[0]) && std::isfinite(o[1]) && std::isfinite(o[2]);
     for (int f = 0; f < nf && inside; ++f)
         inside = orient3d_sign_f(E[F[f][0]].v, E[F[f][1]].v, E[F[f][2]].v, o) > 0;
+    if (std::getenv("CUDAPRE3_NO_CELLS")) inside = false;   // tests: force the every-facet path
     g->ox = o[0], g->oy = o[1], g->oz = o[2];
     g->cells = inside ? 1 : 0;
     P.cells = g->cells;

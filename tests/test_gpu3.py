@@ -133,3 +133,13 @@ def test_large_sampled():
     keep = oracle.filter_mask3(host[sample], host[F], threads=THREADS)
     assert np.array_equal(np.isin(sample, got), keep)
     del host
+
+
+def test_every_facet_path(monkeypatch):
+    """Without direction cells (the host's fallback when the rounded centre is
+    not strictly inside) every point goes through the warp-cooperative pass
+    over all facets: the same survivors."""
+    monkeypatch.setenv("CUDAPRE3_NO_CELLS", "1")
+    for fam, n in (("ball", 300_007), ("cube", 100_003)):
+        ext, idx, poly = _check(synth.generate3(fam, n, seed=31))
+        assert poly.raw.cells == 0
