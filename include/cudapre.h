@@ -11,6 +11,10 @@
  *   Step 3  discard every point inside that convex polygon and
  *           keep the rest, in ascending index order.  -> cudapre_filter
  *   Then    the convex hull of the remaining points -> cudapre_hull
+ *   3D      the extension outlined in P:115 (six extremes per rotation about
+ *           z, a convex polyhedron, discard what is strictly inside) ->
+ *           cudapre3_extremes / cudapre3_polyhedron / cudapre3_filter
+ *           (float3 AoS points; section "The 3D extension" at the end)
  *
  * Citations: "P:nn" = PAPER.md line nn, "S:nn" = SPEC.md line nn, "A#" =
  * the reading numbered # in DESIGN.md §3 (where the paper is silent).
