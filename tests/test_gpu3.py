@@ -143,3 +143,19 @@ def test_every_facet_path(monkeypatch):
     for fam, n in (("ball", 300_007), ("cube", 100_003)):
         ext, idx, poly = _check(synth.generate3(fam, n, seed=31))
         assert poly.raw.cells == 0
+
+
+def test_capacity_error_writes_the_first_survivors():
+    """CAPACITY when the survivors exceed the buffer: the first `capacity`
+    survivors (ascending) are still written, and the error says so."""
+    xyz = synth.generate3("cube", 200_003, seed=12)
+    pts = torch.from_numpy(xyz).cuda()
+    ext = cp.extremes3(pts, "A")
+    want = oracle.cudapre3(xyz, "A", threads=THREADS)["survivors"]
+    cap = len(want) // 3
+    out_idx = torch.full((cap,), -7, dtype=torch.int64, device="cuda")
+    with pytest.raises(cp.CudaPreError) as e:
+        cp.filter3(pts, ext, out_idx=out_idx, return_points=False)
+    assert e.value.status == cp.ERR_CAPACITY
+    torch.cuda.synchronize()
+    assert np.array_equal(out_idx.cpu().numpy(), want[:cap])
