@@ -39,13 +39,31 @@ def main():
     cp.filter_geom(pts, index_base=base, ws=ws, out_idx=d_idx, count=d_count)
     torch.cuda.synchronize()
     assert np.array_equal(d_idx[: int(d_count.item())].cpu().numpy(), idx.cpu().numpy()), "device path"
+    # the 3D extension: K1-3D writes its Step-1 block to a device
+    # buffer, NCCL all-gathers the blocks, the host merges them (cp.exchange3)
+    n3 = N // 3
+    n3_local = n3 // world + (1 if rank < n3 % world else 0)
+    base3 = rank * (n3 // world) + min(rank, n3 % world)
+    xyz = synth.generate3("ball", n3_local, seed=7, base=base3)
+    p3 = torch.from_numpy(xyz).cuda()
+    dev3 = torch.empty(cp.ctypes.sizeof(cp.Extremes3T), dtype=torch.uint8, device="cuda")
+    local3 = cp.extremes3(p3, "A", index_base=base3, device_out=dev3)
+    ext3 = cp.exchange3(local3, dist.group.WORLD, device_buf=dev3)
+    idx3, _, poly3 = cp.filter3(p3, ext3, index_base=base3, return_points=False)
+    parts3 = [None] * world
+    dist.all_gather_object(parts3, idx3.cpu().numpy())
     if rank == 0:
         got = np.concatenate(counts)
         full = synth.generate("disk", N, seed=6)
         want = oracle.cudapre(full, "A", threads=os.cpu_count())
         assert rep["extremes"].idx.tolist() == want["ext_idx"].tolist(), "Step 1"
         assert np.array_equal(got, want["survivors"]), "Step 3"
-        print(f"nccl ok world={world} survivors={len(got)}")
+        full3 = synth.generate3("ball", n3, seed=7)
+        want3 = oracle.cudapre3(full3, "A", threads=os.cpu_count())
+        assert ext3.idx.tolist() == want3["ext_idx"].tolist(), "3D Step 1"
+        assert poly3.facets.tolist() == want3["facets"].tolist(), "3D Step 2"
+        assert np.array_equal(np.concatenate(parts3), want3["survivors"]), "3D Step 3"
+        print(f"nccl ok world={world} survivors={len(got)} 3d={len(want3['survivors'])}")
     dist.barrier()
     dist.destroy_process_group()
 
