@@ -159,3 +159,20 @@ def test_capacity_error_writes_the_first_survivors():
     assert e.value.status == cp.ERR_CAPACITY
     torch.cuda.synchronize()
     assert np.array_equal(out_idx.cpu().numpy(), want[:cap])
+
+
+@pytest.mark.parametrize("sub,deg", [((0, 2), (0.0, 45.0)), ((0, 1, 3), (0.0, 30.0, 60.0)), ((0, 1, 2, 2), (0.0, 30.0, 45.0, 45.0))])
+def test_parity_two_three_and_repeated_angles(sub, deg):
+    """The 2- and 3-angle kernels and a repeated angle (the paper's literal
+    {0, 30, 45, 45}): the product takes slices of its own preset
+    coefficients, the oracle its own table for the same degrees."""
+    _, c, s = cp.angles("A")
+    ang = (c[list(sub)], s[list(sub)])
+    xyz = synth.generate3("ball", 250_003, seed=len(sub) + 40)
+    pts = torch.from_numpy(xyz).cuda()
+    ext = cp.extremes3(pts, ang)
+    idx, _, poly = cp.filter3(pts, ext, return_points=False)
+    want = oracle.cudapre3(xyz, deg, threads=THREADS)
+    assert ext.idx.tolist() == want["ext_idx"].tolist()
+    assert poly.facets.tolist() == want["facets"].tolist()
+    assert np.array_equal(idx.cpu().numpy(), want["survivors"])
