@@ -176,3 +176,13 @@ def test_parity_two_three_and_repeated_angles(sub, deg):
     assert ext.idx.tolist() == want["ext_idx"].tolist()
     assert poly.facets.tolist() == want["facets"].tolist()
     assert np.array_equal(idx.cpu().numpy(), want["survivors"])
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 6, 2047, 2048, 2049, 4095, 4096, 4097, 6143, 6145, 8191, 131_073])
+def test_parity_tile_and_quad_boundaries(n):
+    """Sizes at the 4-point quad and 2048-point tile boundaries (ragged tails,
+    a last tile with one point, exactly full tiles), aligned and misaligned."""
+    xyz = synth.generate3("cube", n, seed=n % 29 + 3)
+    _check(xyz)
+    if n >= 4:
+        _check(xyz, view_offset=1, index_base=5)
