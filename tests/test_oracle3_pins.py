@@ -237,3 +237,23 @@ def test_cudapre3_degenerate_and_empty():
     assert r["degenerate"] and len(r["survivors"]) == 5000     # coplanar input: nothing discarded
     with pytest.raises(ValueError):
         oracle.cudapre3(np.zeros((0, 3), np.float32))
+
+
+def test_discard_fraction_ball_closed_form():
+    """Closed form (P:115 with the default angles): in a uniform ball the
+    picks tend to the 16 equatorial directions at azimuths {0,30,45,60} + k 90
+    degrees and the two poles, so the polyhedron tends to the bipyramid over
+    that 16-gon: volume (2/3) * 2 (1 + 2 sin 15) against 4 pi / 3, i.e.
+    48.308 % discarded.  (A wrong orientation or predicate sign gives ~0 % or
+    ~100 %.)  n = 10^6: the picks' angular deviation ~ n^-1/4 keeps the
+    sampled fraction within ~1 % of the limit."""
+    import math
+
+    area = 2.0 * (1.0 + 2.0 * math.sin(math.radians(15.0)))
+    want = (2.0 / 3.0) * area / (4.0 * math.pi / 3.0)
+    assert abs(want - 0.48308) < 1e-5
+    p = synth.generate3("ball", 1_000_000, seed=23)
+    r = oracle.cudapre3(p, "A", threads=8)
+    got = 1.0 - len(r["survivors"]) / len(p)
+    assert abs(got - want) < 0.01, (got, want)
+    assert len(r["facets"]) == 32          # the bipyramid over a 16-gon: 2 x 16 triangles
