@@ -269,14 +269,17 @@ __global__ void __launch_bounds__(kK23Threads, kK23BlocksPerSM) k2_filter3(const
     bool have_prev = false;
     unsigned prev_tile = 0;
     int par = 0;
+    // the first tile; every later one is claimed by thread 0 right after the
+    // previous tile's aggregate is published (the barrier that follows makes
+    // it visible), so the loop needs no barrier of its own at the top
+    if (tid == 0) {
+        const unsigned t = atomicAdd(&p.ws->k2_ticket, 1u);
+        g.tile[0] = t;
+        const unsigned ahead = t + gridDim.x;
+        if (VEC && ahead < full_tiles) prefetch_l2(p.pts + 3ull * kK23TilePts * ahead, 12u * kK23TilePts);
+    }
+    __syncthreads();
     for (;;) {
-        if (tid == 0) {
-            const unsigned t = atomicAdd(&p.ws->k2_ticket, 1u);
-            g.tile[par] = t;
-            const unsigned ahead = t + gridDim.x;
-            if (VEC && ahead < full_tiles) prefetch_l2(p.pts + 3ull * kK23TilePts * ahead, 12u * kK23TilePts);
-        }
-        __syncthreads();
         const unsigned tile = g.tile[par];
         const bool live = tile < p.num_tiles;
         constexpr int kP = kK23Quads / 2;   // packed scan words: two quad slots each (16-bit halves)
@@ -353,6 +356,10 @@ __global__ void __launch_bounds__(kK23Threads, kK23BlocksPerSM) k2_filter3(const
                 if (lane == 0) {
                     publish(p, tile, tile == 0 ? kFlagP : kFlagA, total, epoch);
                     if (tile == 0 && tile == p.num_tiles - 1) p.ws->count = total;
+                    const unsigned t = atomicAdd(&p.ws->k2_ticket, 1u);   // the next tile
+                    g.tile[par ^ 1] = t;
+                    const unsigned ahead = t + gridDim.x;
+                    if (VEC && ahead < full_tiles) prefetch_l2(p.pts + 3ull * kK23TilePts * ahead, 12u * kK23TilePts);
                 }
             }
             if (have_prev) {
