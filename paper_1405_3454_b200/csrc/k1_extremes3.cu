@@ -221,16 +221,19 @@ __global__ void __launch_bounds__(kK13Threads, 2) k1_extremes3(const __grid_cons
     constexpr unsigned kStep = 32u * kK13Quads;
     constexpr int kAhead = K13_AHEAD;
     const unsigned gstep = gwarps * kStep;
-    const unsigned long long full_quads = p.n / 4u;   // quads with 4 points (vector path)
     if (VEC && lane == 0)
         for (int a = 1; a < kAhead; ++a) {
-            const unsigned long long qa = (unsigned long long)gw * kStep + (unsigned long long)a * gstep;
-            if (qa + kStep <= full_quads) prefetch_l2(p.pts + 12ull * qa, 48u * kStep);
+            const unsigned qa = gw * kStep + a * gstep;
+            if (qa + kStep <= p.n / 4u) prefetch_l2(p.pts + 12ull * qa, 48u * kStep);
         }
     for (unsigned qb = gw * kStep; qb < nq; qb += gstep) {
         if (VEC && lane == 0) {
-            const unsigned long long qa = (unsigned long long)qb + (unsigned long long)kAhead * gstep;
-            if (qa + kStep <= full_quads) prefetch_l2(p.pts + 12ull * qa, 48u * kStep);
+            const unsigned qa = qb + kAhead * gstep;
+            if (qa < qb) {
+                // wrapped past 2^32: beyond the end of the input (n < 2^32), nothing to prefetch
+            } else if (qa + kStep <= p.n / 4u) {
+                prefetch_l2(p.pts + 12ull * qa, 48u * kStep);
+            }
         }
         Quad Q[kK13Quads];
         unsigned valid[kK13Quads];
