@@ -5,31 +5,34 @@
 // its header and DESIGN.md §6.2), organised so that the common path costs as
 // few instructions per point as possible:
 //
-//  * Loads: one elected thread streams 16 KiB sub-tiles global -> shared with
-//    cp.async.bulk (SASS UBLKCP) into a kNst-deep ring guarded by a
-//    transaction-counting "full" mbarrier and a per-warp "empty" mbarrier.
-//    The producer never blocks on a stage it only wants to prefetch
-//    (mbarrier.test_wait), so its warp does not fall behind the others, and it
-//    takes the next super-tile's ticket early (the atomic's latency overlaps
-//    the first sub-tiles).
-//  * Ownership: warp w owns the contiguous 256 points [256w, 256w+256) of each
-//    2048-point sub-tile, lane l the points r*32+l (round r = 0..7, one float2
-//    each).  The groups of the ordered compaction are the 64 (sub-tile, warp)
-//    chunks, in index order.
+//  * Warp roles (kW compute warps + 2): a PRODUCER warp (lane 0) takes
+//    super-tile tickets (the next one while issuing the current one) and
+//    streams 16 KiB sub-tiles global -> shared with cp.async.bulk (SASS
+//    UBLKCP) into a kNst-deep ring guarded by a transaction-counting "full"
+//    mbarrier and an "empty" mbarrier the compute warps release; an EMIT warp
+//    does the ordered compaction's bookkeeping and writes the survivors; the
+//    compute warps only classify.  After set-up there is no block barrier.
+//  * Ownership: compute warp w owns the contiguous 256 points [256w, 256w+256)
+//    of each sub-tile, lane l the points r*32+l (round r = 0..7, one float2
+//    each).  The groups of the ordered compaction are the 8 * kW (sub-tile,
+//    warp) chunks, in index order.
 //  * Pass A: one fast test per point (inner disk or inner box, whichever the
 //    host found larger; a warp-uniform switch).  Points it cannot decide are
-//    queued in INDEX order (one ballot per round), so the per-warp
-//    survivor list comes out sorted and a survivor's rank inside its group is
-//    its list position minus the group's start: no per-group ballots.
+//    queued in INDEX order (one ballot per round), so the per-warp survivor
+//    list comes out sorted and a survivor's rank inside its group is its list
+//    position minus the group's start: no per-group ballots.
 //  * Queue pass: sector table (inner/outer radius of the bucket), then for
 //    the thin undecided band the 1-2 edges the bucket's rays can exit through
-//    (coefficients in shared memory), then the exact predicate.
-//  * Per super-tile: after pass A warp 0 resolves the PREVIOUS super-tile
-//    (decoupled look-back, one tile-time after its aggregate was published)
-//    while warp 1 scans the current one's 64 group counts and publishes its
-//    aggregate; one barrier; all warps write the previous tile's survivors.
-//    Each warp touches only its own lists between barriers, so two barriers
-//    per super-tile suffice.
+//    (coefficients in shared memory), then the exact predicate.  Survivors go
+//    to a per-warp list of the super-tile's buffer (triple-buffered; a list
+//    that overflows spills to the block's global scratch).
+//  * Per super-tile k: each compute warp signals "tile done"; the last one
+//    publishes the tile's aggregate (a packed shared-memory atomic of warps
+//    done and survivor total).  The emit warp then scans the 8 * kW group
+//    counts of k, resolves the PREVIOUS super-tile's prefix (decoupled
+//    look-back one tile-time after its aggregate went out: no spinning),
+//    publishes its inclusive prefix, writes its survivors (index + float2)
+//    and hands its list buffer back ("buf free").
 #include <cuda_runtime.h>
 
 #include <cstdint>
