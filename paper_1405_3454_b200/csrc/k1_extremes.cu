@@ -24,6 +24,14 @@
 //   pruned; NaN/Inf inputs are always candidates (unordered compares).
 //   Angle 0 (c=1, s=0) keys are the coordinates themselves: exact float tests.
 //
+// Before the screen, a per-warp PRE-SCREEN disk (centre and radius derived
+// from the warp's thresholds, rigorous margin: a point strictly inside it
+// cannot tie or beat any slot) lets most points of a dense set skip the 4 *
+// nang screens; the others go to a per-warp queue screened in full 32-lane
+// batches.  Input: 16-B aligned data is streamed by a dedicated producer warp
+// (cp.async.bulk, 4 x 16 KiB ring, full / empty mbarriers) into shared
+// memory, so no register holds data in flight (CUDAPRE_K1_TMA=0: register
+// double-buffered 128-bit loads instead).
 // Thresholds start from a tiny seed kernel (float-only lower/upper bounds of
 // a sample, combined with atomicMax on an order-preserving encoding) so the
 // exact path stays rare from the first iteration on.  Candidates update a
