@@ -443,6 +443,17 @@ cudapre_status cudapre3_filter(const float* d_xyz, int64_t n_local, int64_t inde
                                int64_t capacity, void* d_ws, size_t ws_bytes, void* stream,
                                int64_t* h_count, cudapre3_polyhedron_t* h_poly, double* h_ms_kernel);
 
+/* Test hook (host): the direction cells K2-3D would use for h_ext — for
+ * every cell the mask of candidate facets (bit j = facet j in
+ * cudapre3_polyhedron's order), the centre, and the grid G (6 * G * G
+ * cells; cell = (face * G + iu) * G + iv with face = 2 * axis + (d_axis < 0)
+ * and (u, v) = the other two components in the order (y, z), (z, x),
+ * (x, y)).  n_cells must be >= 6 * G * G (query with h_masks = NULL).
+ * *h_cells = 0 when the centre is not strictly inside (every cell = every
+ * facet) or the polyhedron is degenerate.                                  */
+cudapre_status cudapre3_cells(const cudapre3_extremes_t* h_ext, uint64_t* h_masks, int32_t n_cells,
+                              float* h_centre, int32_t* h_grid, int32_t* h_cells);
+
 /* Exact orient3d sign of float triples (host; tests and callers): sign of
  * det[b-a; c-a; d-a].                                                       */
 int32_t cudapre3_orient(const float* a, const float* b, const float* c, const float* d);

@@ -109,7 +109,7 @@ SYMBOLS = ["cudapre_version", "cudapre_last_error", "cudapre_angles_preset",
            "cudapre_hull_device",
            # the 3D extension
            "cudapre3_workspace_bytes", "cudapre3_orient", "cudapre3_extremes", "cudapre3_extremes_merge",
-           "cudapre3_polyhedron", "cudapre3_filter"]
+           "cudapre3_polyhedron", "cudapre3_filter", "cudapre3_cells"]
 WS_GEOM_OFFSET = 4096            # include/cudapre.h CUDAPRE_WS_GEOM_OFFSET
 WS_POLY_OFFSET = 4096 + 16384    # CUDAPRE_WS_POLY_OFFSET
 WS_RESULT_OFFSET = 176           # CUDAPRE_WS_RESULT_OFFSET
@@ -158,6 +158,7 @@ def lib():
     L.cudapre3_extremes.argtypes = [vp, i64, i64, i32, vp, vp, vp, sz, vp, vp, P(Extremes3T), vp]
     L.cudapre3_extremes_merge.argtypes = [P(Extremes3T), i32, P(Extremes3T)]
     L.cudapre3_polyhedron.argtypes = [P(Extremes3T), P(Polyhedron3T)]
+    L.cudapre3_cells.argtypes = [P(Extremes3T), vp, i32, vp, P(i32), P(i32)]
     L.cudapre3_filter.argtypes = [vp, i64, i64, P(Extremes3T), vp, vp, i64, vp, sz, vp, P(i64), P(Polyhedron3T), vp]
     for name in SYMBOLS[2:]:
         if name not in ("cudapre_workspace_bytes", "cudapre_hull_device_bytes", "cudapre3_workspace_bytes"):
@@ -769,6 +770,20 @@ def polyhedron3(ext: Extremes3) -> Polyhedron:
     out = Polyhedron3T()
     _check(lib().cudapre3_polyhedron(ctypes.byref(ext.raw), ctypes.byref(out)))
     return Polyhedron(out)
+
+
+def cells3(ext: Extremes3):
+    """Test hook: (masks[6 G^2] uint64, centre[3], G, cells_in_use) of the
+    direction cells K2-3D uses for these extremes (cudapre3_cells)."""
+    L = lib()
+    grid, used = ctypes.c_int32(), ctypes.c_int32()
+    _check(L.cudapre3_cells(ctypes.byref(ext.raw), None, 0, None, ctypes.byref(grid), ctypes.byref(used)))
+    n = 6 * grid.value * grid.value
+    masks = np.zeros(n, np.uint64)
+    centre = np.zeros(3, np.float32)
+    _check(L.cudapre3_cells(ctypes.byref(ext.raw), masks.ctypes.data_as(ctypes.c_void_p), n,
+                            centre.ctypes.data_as(ctypes.c_void_p), ctypes.byref(grid), ctypes.byref(used)))
+    return masks, centre, grid.value, bool(used.value)
 
 
 def filter3(pts, ext: Extremes3, index_base: int = 0, return_points: bool = True, ws=None,

@@ -188,6 +188,35 @@ cudapre_status cudapre3_polyhedron(const cudapre3_extremes_t* h_ext, cudapre3_po
     return CUDAPRE_OK;
 }
 
+cudapre_status cudapre3_cells(const cudapre3_extremes_t* h_ext, uint64_t* h_masks, int32_t n_cells,
+                              float* h_centre, int32_t* h_grid, int32_t* h_cells) {
+    api_fail(CUDAPRE_OK, "");
+    if (!h_ext || !h_grid || !h_cells) return fail3(CUDAPRE_ERR_INVALID_ARGUMENT, "NULL argument");
+    *h_grid = kCellG;
+    if (!h_masks) return CUDAPRE_OK;
+    if (n_cells < kCells) return fail3(CUDAPRE_ERR_INVALID_ARGUMENT, "n_cells < %d", kCells);
+    static thread_local K3Geom g;
+    const int rc = build_polyhedron3(*h_ext, nullptr, &g);
+    if (rc) return fail3((cudapre_status)rc, "polyhedron build failed");
+    *h_cells = (g.mode == 0 && g.cells) ? 1 : 0;
+    if (h_centre) h_centre[0] = g.ox, h_centre[1] = g.oy, h_centre[2] = g.oz;
+    for (int c = 0; c < kCells; ++c) {
+        const unsigned w = g.clist[c];
+        unsigned long long m = 0;
+        if ((w >> 24) > (unsigned)kCellSlots) {
+            const unsigned li = w & 0xffffffu;
+            m = li == kNoLong ? g.all : g.lmask[li];
+        } else {
+            for (int k = 0; k < kCellSlots; ++k) {
+                const unsigned t = (w >> (8 * k)) & 0xffu;
+                if (t < (unsigned)kMax3Facets) m |= 1ull << t;
+            }
+        }
+        h_masks[c] = m;
+    }
+    return CUDAPRE_OK;
+}
+
 cudapre_status cudapre3_filter(const float* d_xyz, int64_t n_local, int64_t index_base,
                                const cudapre3_extremes_t* h_ext, int64_t* d_surv_idx, float* d_surv_xyz,
                                int64_t capacity, void* d_ws, size_t ws_bytes, void* stream, int64_t* h_count,

@@ -117,3 +117,66 @@ def test_generate3_is_deterministic_and_sliceable():
     assert (r <= 1.0 + 1e-6).all() and (r >= 1 - 1e-3 - 1e-6).all()
     c = synth.generate3("ball", 5000, seed=9)
     assert ((c.astype(np.float64) ** 2).sum(1) <= 1.0 + 1e-6).all()
+
+
+def _exit_facets(fv, o, d):
+    """Facets through which rays o + t d (rows of d) leave the polyhedron, by
+    binary64 ray casting: per ray the set achieving the smallest exit t
+    (ties: the ray passes through an edge or vertex)."""
+    a, b, c = (fv[:, k, :].astype(np.float64) for k in range(3))
+    n = np.cross(b - a, c - a)                       # inward normals (E on the positive side)
+    oo = np.einsum("fk,fk->f", n, o[None, :] - a)    # orient(o) > 0: o strictly inside
+    nd = d @ n.T                                     # N . d
+    with np.errstate(divide="ignore", invalid="ignore"):
+        t = np.where(nd < 0, oo[None, :] / -nd, np.inf)
+    tmin = t.min(axis=1, keepdims=True)
+    return t <= tmin * (1 + 1e-9) + 1e-300
+
+
+@pytest.mark.parametrize("family", ["ball", "cube", "sphere"])
+@pytest.mark.parametrize("angles", ["A", "D"])
+def test_direction_cells_contain_the_exit_facet(family, angles):
+    """The argument behind K2-3D: a point is strictly inside
+    iff it is strictly inside the facet its ray from the centre leaves
+    through, so every direction cell's candidate list must contain that exit
+    facet — for random directions and for directions on both sides of every
+    cell boundary (where the kernel's rounded cell index may land next door,
+    covered by the guard)."""
+    xyz = synth.generate3(family, 50_000, seed=11)
+    ext = _ext3_from_oracle(xyz, angles)
+    poly = cp.polyhedron3(ext)
+    masks, centre, G, used = cp.cells3(ext)
+    assert used and poly.nf >= 4
+    fv = np.frombuffer(bytes(poly.raw.fv), np.float32).reshape(-1, 3, 3)[: poly.nf]
+    o = centre.astype(np.float64)
+    rng = np.random.default_rng(5)
+    d = rng.normal(size=(60_000, 3))
+    # directions just off the cell boundaries: u, v on the grid lines +- 1e-7
+    face_axis = rng.integers(0, 3, 20_000)
+    sign = rng.choice([-1.0, 1.0], 20_000)
+    grid = -1.0 + 2.0 * rng.integers(0, G + 1, (20_000, 2)) / G
+    uv = grid + rng.choice([-1e-7, 1e-7], (20_000, 2)) + rng.uniform(-1, 1, (20_000, 2)) * [[0, 1]] * 0.5
+    uv = np.clip(uv, -1.0, 1.0)
+    e = np.zeros((20_000, 3))
+    U, V = np.array([1, 2, 0]), np.array([2, 0, 1])
+    e[np.arange(20_000), face_axis] = sign
+    e[np.arange(20_000), U[face_axis]] = uv[:, 0]
+    e[np.arange(20_000), V[face_axis]] = uv[:, 1]
+    d = np.concatenate([d, e])
+    ex = _exit_facets(fv, o, d)
+    # the cell of each direction, exactly as defined (binary64 division)
+    ad = np.abs(d)
+    axis = np.where((ad[:, 0] >= ad[:, 1]) & (ad[:, 0] >= ad[:, 2]), 0, np.where(ad[:, 1] >= ad[:, 2], 1, 2))
+    m = d[np.arange(len(d)), axis]
+    u = d[np.arange(len(d)), U[axis]] / np.abs(m)
+    v = d[np.arange(len(d)), V[axis]] / np.abs(m)
+    # the exact cell, and the cells the kernel's rounded (u, v) (error < 2^-20)
+    # may land in: perturbations of 2^-18 must be covered by the 2^-12 guard
+    for du, dv in ((0, 0), (1, 0), (-1, 0), (0, 1), (0, -1)):
+        uu, vv = u + du * 2.0 ** -18, v + dv * 2.0 ** -18
+        iu = np.clip(np.floor((uu + 1) * G / 2), 0, G - 1).astype(int)
+        iv = np.clip(np.floor((vv + 1) * G / 2), 0, G - 1).astype(int)
+        cell = ((2 * axis + (m < 0)) * G + iu) * G + iv
+        bits = (masks[cell][:, None] >> np.arange(poly.nf, dtype=np.uint64)[None, :]) & np.uint64(1)
+        covered = (ex & bits.astype(bool)).any(axis=1)
+        assert covered.all(), f"{(~covered).sum()} of {len(d)} directions miss their exit facet ({du}, {dv})"
