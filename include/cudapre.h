@@ -454,6 +454,13 @@ cudapre_status cudapre3_filter(const float* d_xyz, int64_t n_local, int64_t inde
 cudapre_status cudapre3_cells(const cudapre3_extremes_t* h_ext, uint64_t* h_masks, int32_t n_cells,
                               float* h_centre, int32_t* h_grid, int32_t* h_cells);
 
+/* Test hook (host): K2-3D's float plane test of each facet, 5 floats per
+ * facet (A, B, C, D, E): g = fma(A, x, fma(B, y, fma(C, z, D))) (float32)
+ * is within E of orient3d(facet, p) for every p in the data bounding box
+ * (E = +inf: the facet always takes the exact predicate).                  */
+cudapre_status cudapre3_planes(const cudapre3_extremes_t* h_ext, float* h_planes, int32_t capacity,
+                               int32_t* h_nf);
+
 /* Exact orient3d sign of float triples (host; tests and callers): sign of
  * det[b-a; c-a; d-a].                                                       */
 int32_t cudapre3_orient(const float* a, const float* b, const float* c, const float* d);

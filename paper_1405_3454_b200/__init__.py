@@ -109,7 +109,7 @@ SYMBOLS = ["cudapre_version", "cudapre_last_error", "cudapre_angles_preset",
            "cudapre_hull_device",
            # the 3D extension
            "cudapre3_workspace_bytes", "cudapre3_orient", "cudapre3_extremes", "cudapre3_extremes_merge",
-           "cudapre3_polyhedron", "cudapre3_filter", "cudapre3_cells"]
+           "cudapre3_polyhedron", "cudapre3_filter", "cudapre3_cells", "cudapre3_planes"]
 WS_GEOM_OFFSET = 4096            # include/cudapre.h CUDAPRE_WS_GEOM_OFFSET
 WS_POLY_OFFSET = 4096 + 16384    # CUDAPRE_WS_POLY_OFFSET
 WS_RESULT_OFFSET = 176           # CUDAPRE_WS_RESULT_OFFSET
@@ -159,6 +159,7 @@ def lib():
     L.cudapre3_extremes_merge.argtypes = [P(Extremes3T), i32, P(Extremes3T)]
     L.cudapre3_polyhedron.argtypes = [P(Extremes3T), P(Polyhedron3T)]
     L.cudapre3_cells.argtypes = [P(Extremes3T), vp, i32, vp, P(i32), P(i32)]
+    L.cudapre3_planes.argtypes = [P(Extremes3T), vp, i32, P(i32)]
     L.cudapre3_filter.argtypes = [vp, i64, i64, P(Extremes3T), vp, vp, i64, vp, sz, vp, P(i64), P(Polyhedron3T), vp]
     for name in SYMBOLS[2:]:
         if name not in ("cudapre_workspace_bytes", "cudapre_hull_device_bytes", "cudapre3_workspace_bytes"):
@@ -784,6 +785,15 @@ def cells3(ext: Extremes3):
     _check(L.cudapre3_cells(ctypes.byref(ext.raw), masks.ctypes.data_as(ctypes.c_void_p), n,
                             centre.ctypes.data_as(ctypes.c_void_p), ctypes.byref(grid), ctypes.byref(used)))
     return masks, centre, grid.value, bool(used.value)
+
+
+def planes3(ext: Extremes3) -> np.ndarray:
+    """Test hook: K2-3D's float plane tests, (nf, 5) = (A, B, C, D, E) per facet."""
+    nf = ctypes.c_int32()
+    out = np.zeros((MAX_FACETS3, 5), np.float32)
+    _check(lib().cudapre3_planes(ctypes.byref(ext.raw), out.ctypes.data_as(ctypes.c_void_p), MAX_FACETS3,
+                                 ctypes.byref(nf)))
+    return out[: nf.value].copy()
 
 
 def filter3(pts, ext: Extremes3, index_base: int = 0, return_points: bool = True, ws=None,

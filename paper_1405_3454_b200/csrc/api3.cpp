@@ -217,6 +217,24 @@ cudapre_status cudapre3_cells(const cudapre3_extremes_t* h_ext, uint64_t* h_mask
     return CUDAPRE_OK;
 }
 
+cudapre_status cudapre3_planes(const cudapre3_extremes_t* h_ext, float* h_planes, int32_t capacity,
+                               int32_t* h_nf) {
+    api_fail(CUDAPRE_OK, "");
+    if (!h_ext || !h_nf) return fail3(CUDAPRE_ERR_INVALID_ARGUMENT, "NULL argument");
+    static thread_local K3Geom g;
+    const int rc = build_polyhedron3(*h_ext, nullptr, &g);
+    if (rc) return fail3((cudapre_status)rc, "polyhedron build failed");
+    *h_nf = g.nf;
+    if (!h_planes) return CUDAPRE_OK;
+    if (capacity < g.nf) return fail3(CUDAPRE_ERR_CAPACITY, "capacity %d < %d facets", capacity, g.nf);
+    for (int f = 0; f < g.nf; ++f) {
+        h_planes[5 * f] = g.pl[f].x, h_planes[5 * f + 1] = g.pl[f].y;
+        h_planes[5 * f + 2] = g.pl[f].z, h_planes[5 * f + 3] = g.pl[f].w;
+        h_planes[5 * f + 4] = g.pe[f];
+    }
+    return CUDAPRE_OK;
+}
+
 cudapre_status cudapre3_filter(const float* d_xyz, int64_t n_local, int64_t index_base,
                                const cudapre3_extremes_t* h_ext, int64_t* d_surv_idx, float* d_surv_xyz,
                                int64_t capacity, void* d_ws, size_t ws_bytes, void* stream, int64_t* h_count,

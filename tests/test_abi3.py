@@ -180,3 +180,39 @@ def test_direction_cells_contain_the_exit_facet(family, angles):
         bits = (masks[cell][:, None] >> np.arange(poly.nf, dtype=np.uint64)[None, :]) & np.uint64(1)
         covered = (ex & bits.astype(bool)).any(axis=1)
         assert covered.all(), f"{(~covered).sum()} of {len(d)} directions miss their exit facet ({du}, {dv})"
+
+
+def _fma32(a, b, c):
+    """RN32(a*b + c) for float32 arrays: a*b is exact in binary64 and the
+    float64 sum is within 2^-53 relative, far below the float32 rounding."""
+    return (a.astype(np.float64) * b.astype(np.float64) + c.astype(np.float64)).astype(np.float32)
+
+
+@pytest.mark.parametrize("family,scale,offset", [("ball", 1.0, 0.0), ("cube", 1.0, 0.0),
+                                                 ("ball", 1e3, 5e3), ("cube", 1e-3, 0.0)])
+def test_plane_test_error_bound(family, scale, offset):
+    """The bound K2-3D's fast decisions rest on: over the data
+    bounding box, |float plane test - orient3d| <= E for every facet —
+    checked on random points, the box corners and the points themselves, with
+    orient3d evaluated in binary64 (its own error ~2^-50 S is far below E)."""
+    xyz = ((synth.generate3(family, 30_000, seed=13).astype(np.float64) * scale) + offset).astype(np.float32)
+    ext = _ext3_from_oracle(xyz, "A")
+    poly = cp.polyhedron3(ext)
+    pl = cp.planes3(ext)
+    assert len(pl) == poly.nf >= 4 and np.isfinite(pl[:, 4]).all()
+    fv = np.frombuffer(bytes(poly.raw.fv), np.float32).reshape(-1, 3, 3)[: poly.nf].astype(np.float64)
+    lo, hi = xyz.min(0), xyz.max(0)
+    rng = np.random.default_rng(2)
+    corners = np.array([[x, y, z] for x in (lo[0], hi[0]) for y in (lo[1], hi[1]) for z in (lo[2], hi[2])],
+                       np.float32)
+    pts = np.concatenate([rng.uniform(lo, hi, (20_000, 3)).astype(np.float32), corners, xyz[:5000]])
+    for f in range(poly.nf):
+        A, B, C, D, E = pl[f]
+        g = _fma32(np.full(len(pts), A, np.float32), pts[:, 0],
+                   _fma32(np.full(len(pts), B, np.float32), pts[:, 1],
+                          _fma32(np.full(len(pts), C, np.float32), pts[:, 2], np.full(len(pts), D, np.float32))))
+        a, b, c = fv[f]
+        exact = (pts.astype(np.float64) - a) @ np.cross(b - a, c - a)
+        err = np.abs(g.astype(np.float64) - exact)
+        assert (err <= E).all(), (f, float(err.max()), float(E))
+        assert float(err.max()) > 0 or E > 0
