@@ -186,3 +186,23 @@ def test_parity_tile_and_quad_boundaries(n):
     _check(xyz)
     if n >= 4:
         _check(xyz, view_offset=1, index_base=5)
+
+
+def test_k1_screen_near_ties_and_exact_ties():
+    """K1-3D's float screen (quad-level margin): 10^6 points
+    on a unit circle in the xy-plane — near every rotated extreme many keys
+    lie within the float margin of each other, so the exact binary64 path
+    decides — plus exact copies of points at higher indices (ties: lowest
+    index wins) and a scaled, offset copy of the whole set."""
+    n = 1_000_000
+    t = np.arange(n, dtype=np.float64) * (2 * np.pi / n)
+    rng = np.random.default_rng(21)
+    base = np.stack([np.cos(t), np.sin(t), rng.uniform(-1, 1, n)], 1).astype(np.float32)
+    dup = base[rng.integers(0, n, 200_000)]
+    for xyz in (np.concatenate([base, dup]),
+                (np.concatenate([base, dup]).astype(np.float64) * 3e5 + 7e5).astype(np.float32)):
+        pts = torch.from_numpy(np.ascontiguousarray(xyz)).cuda()
+        for angles in ("A", "D"):
+            got = cp.extremes3(pts, angles).idx
+            want = oracle.extremes3(xyz, angles, threads=THREADS)
+            assert got.tolist() == want.tolist(), angles
