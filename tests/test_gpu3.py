@@ -206,3 +206,30 @@ def test_k1_screen_near_ties_and_exact_ties():
             got = cp.extremes3(pts, angles).idx
             want = oracle.extremes3(xyz, angles, threads=THREADS)
             assert got.tolist() == want.tolist(), angles
+
+
+@pytest.mark.parametrize("k", [2, 3, 8])
+def test_sharded_pipeline(k):
+    """k contiguous shards (what k ranks hold): per-shard K1-3D with global
+    indices, the merged Step-1 blocks, per-shard K2-3D: the concatenated
+    survivors are the oracle's single-set answer (ties across cuts: heavy
+    rounding)."""
+    xyz = np.round(synth.generate3("ball", 600_007, seed=19) * 64).astype(np.float32)
+    n = len(xyz)
+    cuts = [n * r // k for r in range(k + 1)]
+    parts, shards = [], []
+    for r in range(k):
+        lo, hi = cuts[r], cuts[r + 1]
+        pts = torch.from_numpy(np.ascontiguousarray(xyz[lo:hi])).cuda()
+        ws = cp.Workspace3(hi - lo)
+        parts.append(cp.extremes3(pts, "A", index_base=lo, ws=ws))
+        shards.append((pts, ws, lo))
+    merged = cp.merge3(parts)
+    want = oracle.cudapre3(xyz, "A", threads=THREADS)
+    assert merged.idx.tolist() == want["ext_idx"].tolist()
+    got = []
+    for pts, ws, lo in shards:
+        idx, sp, poly = cp.filter3(pts, merged, index_base=lo, ws=ws)
+        assert poly.facets.tolist() == want["facets"].tolist()
+        got.append(idx.cpu().numpy())
+    assert np.array_equal(np.concatenate(got), want["survivors"])
