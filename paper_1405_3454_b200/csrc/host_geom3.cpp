@@ -64,6 +64,19 @@ void mark_cells(const double* A, const double* B, const double* C, double tau, i
     for (int a = 0; a < 3; ++a)
         for (int sg = 0; sg < 2; ++sg) {
             const double s = sg ? -1.0 : 1.0;
+            {   // trivial reject: all three vertices outside one of the pyramid's half-spaces
+                const double* T3[3] = {A, B, C};
+                bool o0 = true, o1 = true, o2 = true, o3 = true, o4 = true;
+                for (int k = 0; k < 3; ++k) {
+                    const double mk = s * T3[k][a];
+                    o0 &= mk + tau < 0;
+                    o1 &= w * mk - T3[k][U[a]] + tau < 0;
+                    o2 &= w * mk + T3[k][U[a]] + tau < 0;
+                    o3 &= w * mk - T3[k][V[a]] + tau < 0;
+                    o4 &= w * mk + T3[k][V[a]] + tau < 0;
+                }
+                if (o0 || o1 || o2 || o3 || o4) continue;
+            }
             double poly[24][3];
             for (int k = 0; k < 3; ++k) poly[0][k] = A[k], poly[1][k] = B[k], poly[2][k] = C[k];
             int n = 3;
@@ -150,33 +163,36 @@ int build_polyhedron3(const cudapre3_extremes_t& ext, cudapre3_polyhedron_t* pol
     P.n_distinct = m;
     for (int j = 0; j < m; ++j) P.eidx[j] = E[j].id;
 
-    // facets: first supporting triple of each plane, E on the positive side (B4)
+    // facets: first supporting triple of each plane, E on the positive side (B4).
+    // The support test yields the triple's on-plane points (sign 0); a later
+    // supporting triple lies on a kept facet's plane iff its three points are
+    // all in that facet's on-plane set (a supporting plane is determined by
+    // any three non-collinear points on it), so duplicates cost no predicate.
     int nf = 0;
     int F[kMax3Facets][3];
+    unsigned long long onp[kMax3Facets];   // points of E on each kept facet's plane
     for (int a = 0; a < m; ++a)
         for (int b = a + 1; b < m; ++b)
             for (int c = b + 1; c < m; ++c) {
+                const unsigned long long abc = (1ull << a) | (1ull << b) | (1ull << c);
+                bool dup = false;
+                for (int f = 0; f < nf && !dup; ++f) dup = (onp[f] & abc) == abc;
+                if (dup) continue;   // on an earlier facet's plane: never kept (supporting or not)
                 bool pos = false, neg = false;
+                unsigned long long on = abc;
                 for (int d = 0; d < m && !(pos && neg); ++d) {
                     if (d == a || d == b || d == c) continue;
                     const int o = orient3d_sign_f(E[a].v, E[b].v, E[c].v, E[d].v);
                     pos |= o > 0;
                     neg |= o < 0;
+                    if (o == 0) on |= 1ull << d;
                 }
                 if (pos == neg) continue;   // not supporting, or everything on the plane
-                bool same = false;
-                for (int f = 0; f < nf && !same; ++f) {
-                    const float* A = E[F[f][0]].v;
-                    const float* B = E[F[f][1]].v;
-                    const float* C = E[F[f][2]].v;
-                    same = orient3d_sign_f(A, B, C, E[a].v) == 0 && orient3d_sign_f(A, B, C, E[b].v) == 0 &&
-                           orient3d_sign_f(A, B, C, E[c].v) == 0;
-                }
-                if (same) continue;
                 if (nf >= kMax3Facets) return CUDAPRE_ERR_INVALID_ARGUMENT;   // cannot happen for <= 34 points
                 F[nf][0] = a;
                 F[nf][1] = pos ? b : c;
                 F[nf][2] = pos ? c : b;
+                onp[nf] = on;
                 ++nf;
             }
     P.nf = nf;
@@ -261,9 +277,7 @@ int build_polyhedron3(const cudapre3_extremes_t& ext, cudapre3_polyhedron_t* pol
         for (int f = 0; f < nf; ++f) {
             std::vector<int> on;
             for (int j = 0; j < m; ++j)
-                if (j == F[f][0] || j == F[f][1] || j == F[f][2] ||
-                    orient3d_sign_f(E[F[f][0]].v, E[F[f][1]].v, E[F[f][2]].v, E[j].v) == 0)
-                    on.push_back(j);
+                if ((onp[f] >> j) & 1ull) on.push_back(j);
             for (size_t i = 0; i < on.size(); ++i)
                 for (size_t j = i + 1; j < on.size(); ++j)
                     for (size_t k = j + 1; k < on.size(); ++k) {
