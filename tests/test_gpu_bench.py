@@ -1,0 +1,54 @@
+"""bench.py keeps the driver's JSON contract (one line; metric, value, unit,
+n_gpus, steps, warmup, ms_per_step, higher_is_better, scaling, vs_baseline,
+dtype, data, config; roofline, cpu_baseline, e2e, gpu_launches, clocks) for
+the 2D path, the 3D extension and the reference arm — on small configs so the
+test takes seconds."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+BASE_KEYS = {"metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+             "scaling", "vs_baseline", "dtype", "data", "config", "e2e"}
+
+
+def _run(*args):
+    res = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), *args], capture_output=True,
+                         text=True, timeout=900, cwd=ROOT)
+    assert res.returncode == 0, res.stdout[-2000:] + res.stderr[-4000:]
+    lines = [ln for ln in res.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, res.stdout[-2000:]
+    return json.loads(lines[0])
+
+
+@pytest.mark.parametrize("args", [("--config", "C2b"), ("--config", "T1")])
+def test_bench_line_contract(args):
+    d = _run(*args, "--steps", "3", "--warmup", "3", "--no-cpu-baseline")
+    assert BASE_KEYS <= d.keys()
+    assert d["value"] > 0 and d["unit"] == "Gpts/s" and d["n_gpus"] == 1
+    assert d["steps"] == 3 and d["warmup"] == 3 and d["higher_is_better"] is True
+    assert d["scaling"] in ("weak", "strong") and d["data"] == "synthetic"
+    assert "workload" in d["config"]
+    r = d["roofline"]
+    assert {"bound", "achieved", "peak", "unit", "frac", "traffic"} <= r.keys()
+    assert r["bound"] == "hbm" and r["unit"] == "GB/s" and r["achieved"] > 0 and r["peak"] > 0
+    assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-3
+    e = d["e2e"]
+    assert {"value", "unit", "h2d_bytes_per_step", "d2h_bytes_per_step"} <= e.keys()
+    assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
+    assert d["gpu_launches"] > 0
+    assert {"sm_mhz", "sm_max_mhz", "reasons"} <= d["clocks"].keys()
+    assert "cpu_baseline" in d and 0 <= d["discard_pct"] <= 100
+
+
+def test_bench_reference_arm_contract():
+    d = _run("--impl", "reference", "--config", "C1", "--steps", "1", "--warmup", "1")
+    assert BASE_KEYS <= d.keys() and d["impl"] == "reference"
+    assert d["value"] > 0 and d["unit"] == "Gpts/s"
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
