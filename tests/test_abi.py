@@ -472,3 +472,34 @@ def test_filtered_orient_in_step2_vs_fractions(L, oracle_lib):
         else:
             assert poly.degenerate, pts
     assert checked > 500
+
+
+def test_plain_c_client_compiles_links_and_runs(tmp_path):
+    """The boundary is a C ABI: include/cudapre.h compiles as strict C99 and a
+    C program links against libcudapre.so and calls host-only entry points
+    (2D and 3D) — no torch, no C++ in the caller."""
+    import subprocess
+
+    src = tmp_path / "client.c"
+    src.write_text(r"""
+#include <stdio.h>
+#include "cudapre.h"
+int main(void) {
+    int32_t nang = 0; double c[8], s[8];
+    if (cudapre_angles_preset(0, &nang, c, s) != CUDAPRE_OK || nang != 4) return 1;
+    if (cudapre_workspace_bytes(1000) == 0 || cudapre3_workspace_bytes(1000) == 0) return 2;
+    float a[3] = {0, 0, 0}, b[3] = {1, 0, 0}, cc[3] = {0, 1, 0}, d[3] = {0, 0, 1};
+    if (cudapre3_orient(a, b, cc, d) != 1 || cudapre3_orient(a, cc, b, d) != -1) return 3;
+    cudapre_pt pts[4] = {{0, 0}, {1, 0}, {0, 1}, {0.25f, 0.25f}};
+    int64_t ring[4], len = 0;
+    if (cudapre_hull(pts, NULL, 4, ring, &len) != CUDAPRE_OK || len != 3) return 4;
+    printf("ok %s\n", cudapre_version());
+    return 0;
+}
+""")
+    exe = tmp_path / "client"
+    libdir = os.path.dirname(cp.LIB_PATH)
+    subprocess.check_call(["gcc", "-std=c99", "-Wall", "-Werror", "-pedantic", f"-I{ROOT}/include", str(src),
+                           f"-L{libdir}", "-lcudapre", f"-Wl,-rpath,{libdir}", "-o", str(exe)])
+    out = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert out.returncode == 0 and out.stdout.startswith("ok "), (out.returncode, out.stdout, out.stderr)
