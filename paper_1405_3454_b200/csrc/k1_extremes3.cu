@@ -200,7 +200,7 @@ __device__ __forceinline__ void fold_quad(Lane<NANG>& L, const Quad& Q, unsigned
 }
 
 template <int NANG, bool VEC>
-__global__ void __launch_bounds__(kK13Threads, 2) k1_extremes3(const __grid_constant__ K13Params p) {
+__global__ void __launch_bounds__(kK13Threads, NANG >= 8 ? 1 : 2) k1_extremes3(const __grid_constant__ K13Params p) {
     constexpr int R = Lane<NANG>::R;
     constexpr int D = 6 + R;   // distinct keys
     __shared__ double s_key[kK13Threads / 32][D];

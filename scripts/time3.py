@@ -1,5 +1,5 @@
 """Quick CUDA-event timing of the 3D path (K1-3D, host Step 2, K2-3D) on a
-device-generated workload: python scripts/time3.py [family] [n] [reps]."""
+device-generated workload: python scripts/time3.py [family] [n] [reps] [angles]."""
 import sys
 import time
 
@@ -12,6 +12,7 @@ import synth.cuda  # noqa: E402
 fam = sys.argv[1] if len(sys.argv) > 1 else "ball"
 n = int(float(sys.argv[2])) if len(sys.argv) > 2 else 1_000_000_000
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 5
+angles = sys.argv[4] if len(sys.argv) > 4 else "A"
 pts = synth.cuda.generate3(fam, n, seed=23)
 ws = cp.Workspace3(n)
 out_idx = torch.empty(n, dtype=torch.int64, device="cuda")
@@ -20,7 +21,7 @@ ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
 for r in range(reps + 2):
     torch.cuda.synchronize()
     ev[0].record()
-    ext = cp.extremes3(pts, "A", ws=ws)
+    ext = cp.extremes3(pts, angles, ws=ws)
     ev[1].record()
     idx, _, poly = cp.filter3(pts, ext, ws=ws, out_idx=out_idx, out_pts=out_pts)
     ev[2].record()
