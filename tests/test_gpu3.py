@@ -233,3 +233,12 @@ def test_sharded_pipeline(k):
         assert poly.facets.tolist() == want["facets"].tolist()
         got.append(idx.cpu().numpy())
     assert np.array_equal(np.concatenate(got), want["survivors"])
+
+
+def test_degenerate_collinear_keeps_everything():
+    """All points on one line (exactly representable direction): every
+    triple is collinear, there is no facet, nothing is inside."""
+    t = np.random.default_rng(4).integers(-1000, 1001, 50_003).astype(np.float32) / np.float32(8)
+    xyz = np.stack([t, np.float32(2) * t, np.float32(-0.5) * t], 1).astype(np.float32)
+    ext, idx, poly = _check(xyz)
+    assert poly.degenerate and len(idx) == len(xyz)
