@@ -398,7 +398,9 @@ typedef struct {
     int32_t max_candidates;                     /* largest candidate list of a cell */
     int32_t long_cells;                         /* cells whose list exceeds the kernel's 3 slots */
     int32_t n_cells;                            /* direction cells (6 * 32 * 32) */
-    int32_t pad[5];
+    int32_t empty_cells;                        /* cells with no candidate facet (set to every facet
+                                                 * as a fail-safe; 0 by construction) */
+    int32_t pad[4];
 } cudapre3_polyhedron_t;
 
 /* Workspace bytes for a shard of n_local points (3D). */
@@ -442,6 +444,18 @@ cudapre_status cudapre3_filter(const float* d_xyz, int64_t n_local, int64_t inde
                                const cudapre3_extremes_t* h_ext, int64_t* d_surv_idx, float* d_surv_xyz,
                                int64_t capacity, void* d_ws, size_t ws_bytes, void* stream,
                                int64_t* h_count, cudapre3_polyhedron_t* h_poly, double* h_ms_kernel);
+
+/* cudapre3_filter with explicit options: flags = 0 is cudapre3_filter;
+ * CUDAPRE3_FLAG_NO_CELLS forces the every-facet path (no direction cells:
+ * every point goes through the warp-cooperative all-facet test, the path the
+ * library takes by itself when the centre is not certified).  Same result.
+ * INVALID_ARGUMENT for unknown flag bits.                                   */
+#define CUDAPRE3_FLAG_NO_CELLS 1
+cudapre_status cudapre3_filter_ex(const float* d_xyz, int64_t n_local, int64_t index_base,
+                                  const cudapre3_extremes_t* h_ext, int64_t* d_surv_idx, float* d_surv_xyz,
+                                  int64_t capacity, void* d_ws, size_t ws_bytes, void* stream,
+                                  int64_t* h_count, cudapre3_polyhedron_t* h_poly, double* h_ms_kernel,
+                                  int32_t flags);
 
 /* Test hook (host): the direction cells K2-3D would use for h_ext — for
  * every cell the mask of candidate facets (bit j = facet j in

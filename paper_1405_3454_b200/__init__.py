@@ -26,7 +26,7 @@ from dataclasses import dataclass
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.environ.get("CUDAPRE_LIB_OVERRIDE") or os.path.join(_HERE, "libcudapre.so")   # (override: A/B perf experiments only)
+LIB_PATH = os.path.join(_HERE, "libcudapre.so")
 MAX_ANGLES = 8
 MAX_SLOTS = 32
 SECTORS = 1024
@@ -97,7 +97,7 @@ class Polyhedron3T(ctypes.Structure):
                 ("fidx", (ctypes.c_int64 * 3) * MAX_FACETS3), ("fv", (Pt3 * 3) * MAX_FACETS3),
                 ("centre", ctypes.c_float * 3), ("err_max", ctypes.c_float),
                 ("max_candidates", ctypes.c_int32), ("long_cells", ctypes.c_int32), ("n_cells", ctypes.c_int32),
-                ("pad", ctypes.c_int32 * 5)]
+                ("empty_cells", ctypes.c_int32), ("pad", ctypes.c_int32 * 4)]
 
 
 SYMBOLS = ["cudapre_version", "cudapre_last_error", "cudapre_angles_preset",
@@ -109,7 +109,7 @@ SYMBOLS = ["cudapre_version", "cudapre_last_error", "cudapre_angles_preset",
            "cudapre_hull_device",
            # the 3D extension
            "cudapre3_workspace_bytes", "cudapre3_orient", "cudapre3_extremes", "cudapre3_extremes_merge",
-           "cudapre3_polyhedron", "cudapre3_filter", "cudapre3_cells", "cudapre3_planes"]
+           "cudapre3_polyhedron", "cudapre3_filter", "cudapre3_filter_ex", "cudapre3_cells", "cudapre3_planes"]
 WS_GEOM_OFFSET = 4096            # include/cudapre.h CUDAPRE_WS_GEOM_OFFSET
 WS_POLY_OFFSET = 4096 + 16384    # CUDAPRE_WS_POLY_OFFSET
 WS_RESULT_OFFSET = 176           # CUDAPRE_WS_RESULT_OFFSET
@@ -161,6 +161,8 @@ def lib():
     L.cudapre3_cells.argtypes = [P(Extremes3T), vp, i32, vp, P(i32), P(i32)]
     L.cudapre3_planes.argtypes = [P(Extremes3T), vp, i32, P(i32)]
     L.cudapre3_filter.argtypes = [vp, i64, i64, P(Extremes3T), vp, vp, i64, vp, sz, vp, P(i64), P(Polyhedron3T), vp]
+    L.cudapre3_filter_ex.argtypes = [vp, i64, i64, P(Extremes3T), vp, vp, i64, vp, sz, vp, P(i64), P(Polyhedron3T), vp,
+                                     i32]
     for name in SYMBOLS[2:]:
         if name not in ("cudapre_workspace_bytes", "cudapre_hull_device_bytes", "cudapre3_workspace_bytes"):
             getattr(L, name).restype = ctypes.c_int
@@ -796,8 +798,11 @@ def planes3(ext: Extremes3) -> np.ndarray:
     return out[: nf.value].copy()
 
 
+FLAG3_NO_CELLS = 1   # CUDAPRE3_FLAG_NO_CELLS
+
+
 def filter3(pts, ext: Extremes3, index_base: int = 0, return_points: bool = True, ws=None,
-            out_idx=None, out_pts=None, stream=None, timing: list | None = None):
+            out_idx=None, out_pts=None, stream=None, timing: list | None = None, flags: int = 0):
     """3D Steps 2+3: survivors' global indices (ascending, int64 CUDA tensor),
     optionally their xyz, and the polyhedron used.  ``timing``: a list the
     K2-3D launch's device milliseconds are appended to."""
@@ -815,12 +820,12 @@ def filter3(pts, ext: Extremes3, index_base: int = 0, return_points: bool = True
     count = ctypes.c_int64()
     poly = Polyhedron3T()
     ms = ctypes.c_double()
-    _check(lib().cudapre3_filter(
+    _check(lib().cudapre3_filter_ex(
         ctypes.c_void_p(pts.data_ptr()), n, index_base, ctypes.byref(ext.raw),
         ctypes.c_void_p(out_idx.data_ptr()),
         ctypes.c_void_p(out_pts.data_ptr()) if out_pts is not None else None,
         cap, w.ptr, w.nbytes, _stream_ptr(stream), ctypes.byref(count), ctypes.byref(poly),
-        ctypes.byref(ms) if timing is not None else None))
+        ctypes.byref(ms) if timing is not None else None, int(flags)))
     if timing is not None:
         timing.append(ms.value)
     m = count.value

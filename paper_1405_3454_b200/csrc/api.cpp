@@ -174,8 +174,6 @@ void k2_params(K2Params& p, const cudapre_pt* d_pts, int64_t n_local, int64_t in
     p.num_tiles = (unsigned)((n_local + kK2TilePts - 1) / kK2TilePts);
     p.g = ws_geom(d_ws);
     p.edges = 32;
-    const char* e = getenv("CUDAPRE_K2_DEBUG");   // perf experiments only: wrong results
-    p.debug = e ? atoi(e) : 0;
 }
 
 }  // namespace
@@ -274,14 +272,9 @@ cudapre_status cudapre_extremes(const cudapre_pt* d_pts, int64_t n_local, int64_
         int64_t ch = n_local / 16384;
         p.seed_chunks = (unsigned)(ch < 16 ? 16 : (ch > 4096 ? 4096 : ch));
     }
+    // 16-B aligned input: the warp-specialised cp.async.bulk ring; 8-B
+    // aligned: register double-buffered loads
     const int vec16 = (((uintptr_t)d_pts & 15u) == 0);
-    {
-        // K1 input path for 16-B aligned input: the warp-specialised
-        // cp.async.bulk ring (default; C5 2.22 ms vs 2.58 ms) or register
-        // double-buffered 128-bit loads (CUDAPRE_K1_TMA=0).
-        const char* e = getenv("CUDAPRE_K1_TMA");
-        p.use_tma = e ? atoi(e) : 1;
-    }
     cudaEvent_t* ev = nullptr;
     if (h_rep) {
         st = events(&ev);

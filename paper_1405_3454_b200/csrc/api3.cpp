@@ -239,6 +239,15 @@ cudapre_status cudapre3_filter(const float* d_xyz, int64_t n_local, int64_t inde
                                const cudapre3_extremes_t* h_ext, int64_t* d_surv_idx, float* d_surv_xyz,
                                int64_t capacity, void* d_ws, size_t ws_bytes, void* stream, int64_t* h_count,
                                cudapre3_polyhedron_t* h_poly, double* h_ms_kernel) {
+    return cudapre3_filter_ex(d_xyz, n_local, index_base, h_ext, d_surv_idx, d_surv_xyz, capacity, d_ws, ws_bytes,
+                              stream, h_count, h_poly, h_ms_kernel, 0);
+}
+
+cudapre_status cudapre3_filter_ex(const float* d_xyz, int64_t n_local, int64_t index_base,
+                                  const cudapre3_extremes_t* h_ext, int64_t* d_surv_idx, float* d_surv_xyz,
+                                  int64_t capacity, void* d_ws, size_t ws_bytes, void* stream, int64_t* h_count,
+                                  cudapre3_polyhedron_t* h_poly, double* h_ms_kernel, int32_t flags) {
+    if (flags & ~CUDAPRE3_FLAG_NO_CELLS) return fail3(CUDAPRE_ERR_INVALID_ARGUMENT, "unknown flags");
     api_fail(CUDAPRE_OK, "");
     if (!h_ext || !h_count) return fail3(CUDAPRE_ERR_INVALID_ARGUMENT, "h_ext / h_count is NULL");
     if (h_ext->nonfinite) return fail3(CUDAPRE_ERR_NONFINITE_INPUT, "the extremes saw a non-finite coordinate");
@@ -254,7 +263,7 @@ cudapre_status cudapre3_filter(const float* d_xyz, int64_t n_local, int64_t inde
     if (st) return st;
     if (sb < 4096 + sizeof(K3Geom)) return fail3(CUDAPRE_ERR_INVALID_ARGUMENT, "staging buffer too small");
     K3Geom* g = reinterpret_cast<K3Geom*>(static_cast<char*>(stage) + 4096);
-    const int rc = build_polyhedron3(*h_ext, h_poly, g);
+    const int rc = build_polyhedron3(*h_ext, h_poly, g, flags);
     if (rc) return fail3((cudapre_status)rc, "polyhedron build failed");
     cudaStream_t strm = (cudaStream_t)stream;
     *h_count = 0;

@@ -141,7 +141,7 @@ void mark_cells(const double* A, const double* B, const double* C, double tau, i
 
 }  // namespace
 
-int build_polyhedron3(const cudapre3_extremes_t& ext, cudapre3_polyhedron_t* poly, K3Geom* g) {
+int build_polyhedron3(const cudapre3_extremes_t& ext, cudapre3_polyhedron_t* poly, K3Geom* g, int flags) {
     cudapre3_polyhedron_t P;
     std::memset(&P, 0, sizeof(P));
     std::memset(g, 0, sizeof(*g));
@@ -254,7 +254,7 @@ int build_polyhedron3(const cudapre3_extremes_t& ext, cudapre3_polyhedron_t* pol
     bool inside = std::isfinite(o[0]) && std::isfinite(o[1]) && std::isfinite(o[2]);
     for (int f = 0; f < nf && inside; ++f)
         inside = orient3d_sign_f(E[F[f][0]].v, E[F[f][1]].v, E[F[f][2]].v, o) > 0;
-    if (std::getenv("CUDAPRE3_NO_CELLS")) inside = false;   // tests: force the every-facet path
+    if (flags & CUDAPRE3_FLAG_NO_CELLS) inside = false;   // caller: force the every-facet path
     g->ox = o[0], g->oy = o[1], g->oz = o[2];
     g->cells = inside ? 1 : 0;
     P.cells = g->cells;
@@ -293,8 +293,16 @@ int build_polyhedron3(const cudapre3_extremes_t& ext, cudapre3_polyhedron_t* pol
     }
     g->pl[kDummyFacet] = make_float4(0.f, 0.f, 0.f, 1.f);
     g->pe[kDummyFacet] = 0.f;
-    int nent = 0, mx = 0, nlong = 0;
+    int nent = 0, mx = 0, nlong = 0, nempty = 0;
     for (int c = 0; c < kCells; ++c) {
+        // fail-safe: a cell with no candidate facet would discard its points
+        // untested (the dummy slots say "inside"); the exit-facet argument
+        // says it cannot happen, so such a cell tests every facet instead and
+        // is counted (tests assert the count is 0)
+        if (cmask[c] == 0ull) {
+            cmask[c] = g->all;
+            ++nempty;
+        }
         const int k = __builtin_popcountll(cmask[c]);
         nent += k;
         mx = std::max(mx, k);
@@ -318,6 +326,7 @@ int build_polyhedron3(const cudapre3_extremes_t& ext, cudapre3_polyhedron_t* pol
     P.n_entries = nent;
     P.max_candidates = mx;
     P.n_cells = kCells;
+    P.empty_cells = nempty;
     if (poly) *poly = P;
     return 0;
 }

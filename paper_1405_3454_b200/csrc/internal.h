@@ -5,6 +5,7 @@
 #include <cstdint>
 
 #include "../../include/cudapre.h"
+#include "device.h"
 
 namespace cudapre {
 
@@ -84,7 +85,6 @@ constexpr int kK2WarpPts = kK2Sub * 256;            // 2048 points per warp per 
 constexpr int kK2MaxWarps = 10;                    // compute warps per TMA K2 block, at most
 constexpr size_t kK2ScratchPerBlock = (size_t)kK2Bufs * kK2MaxWarps * kK2WarpPts * sizeof(SurvEntry);
 constexpr int kK2BlocksPerSM = 2;
-int device_sm_count();
 inline size_t ws_scratch_blocks(int64_t n) {
     const size_t cap = (size_t)kK2BlocksPerSM * (size_t)device_sm_count();
     const size_t t = ws_tiles(n);
@@ -106,7 +106,7 @@ struct K1Params {
     K1Partial* partials;
     cudapre_extremes_t* d_out;   // nullable extra copy of the result
     unsigned int seed_chunks;    // number of 256-point sample chunks (0 = no seed)
-    int use_tma;                 // 1: stream through the cp.async.bulk ring (16-B aligned input)
+    int pad_;
 };
 
 // Step-3 geometry (built from the polygon on the host or on the device,
@@ -141,7 +141,7 @@ struct K2Params {
     WsHeader* ws;
     unsigned long long* status;   // ntiles tile-status words, kStatusStride apart
     unsigned int num_tiles;
-    int debug;                // perf experiments only (CUDAPRE_K2_DEBUG): 1 = skeleton, 2 = timing build
+    int pad_;
     const K2Geom* g;          // device geometry (workspace)
     SurvEntry* scratch;       // TMA K2 list overflow, kK2ScratchPerBlock per block
     unsigned int scratch_blocks;   // blocks the scratch region covers (caps the TMA K2 grid)
@@ -151,10 +151,7 @@ struct K2Params {
 // All return a cudaError_t as int (0 = success).
 int launch_extremes(const K1Params& p, int vec16, void* stream, int* launches);
 int launch_filter(const K2Params& p, int vec16, void* stream, int* launches);
-int launch_filter_tma(const K2Params& p, void* stream, int* launches);     // vec16: 8 compute warps
-int launch_filter_tma10(const K2Params& p, void* stream, int* launches);   // vec16: 10 compute warps
-int k2_warps();   // CUDAPRE_K2_WARPS (8 or 10)
-int k2_use_tma();   // CUDAPRE_K2_TMA (default 1)
+int launch_filter_tma(const K2Params& p, void* stream, int* launches);     // 16-B aligned input
 
 // ---------------------------------------------------------------- final hull on the GPU (k_hull.cu, f1)
 constexpr int kHullBuckets = 4097;   // b = round(1024 pa), pa in [0, 4]

@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include "../../include/cudapre.h"
+#include "device.h"
 
 namespace cudapre {
 
@@ -131,7 +132,7 @@ int launch_filter3(const K23Params& p, void* stream, int* launches);
 // host Step 2 (host_geom3.cpp): polyhedron + K3Geom from the merged extremes
 // (bbox = exact data bounding box from the angle-0 slots).  Returns 0 or a
 // cudapre_status.
-int build_polyhedron3(const cudapre3_extremes_t& ext, cudapre3_polyhedron_t* poly, K3Geom* g);
+int build_polyhedron3(const cudapre3_extremes_t& ext, cudapre3_polyhedron_t* poly, K3Geom* g, int flags = 0);
 int merge_extremes3(const cudapre3_extremes_t* parts, int count, cudapre3_extremes_t* out);
 
 // api.cpp hooks shared with api3.cpp

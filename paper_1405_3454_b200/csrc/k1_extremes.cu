@@ -256,7 +256,7 @@ __global__ void __launch_bounds__(kSeedThreads) k1_seed(const K1Params p) {
     float L[NS];
 #pragma unroll
     for (int s = 0; s < NS; ++s) L[s] = is_max_slot(s) ? -INFINITY : INFINITY;
-    const unsigned npairs = (p.n + 1u) / 2u;
+    const unsigned npairs = p.n / 2u + (p.n & 1u);   // (n + 1) / 2 without wrapping at 2^32-1
     const unsigned chunk_pairs = kSeedThreads;
     const unsigned span = npairs > chunk_pairs ? npairs - chunk_pairs : 0u;
     for (unsigned c = blockIdx.x; c < p.seed_chunks; c += gridDim.x) {
@@ -346,7 +346,7 @@ __global__ void __launch_bounds__(kK1Threads + (TMA ? 32 : 0), 2) k1_extremes(co
     prescreen_params<NANG>(T, p, pcx, pcy, prho2);
     unsigned qcount = 0;   // this warp's queued points (uniform)
 
-    const unsigned npairs = (p.n + 1u) / 2u;
+    const unsigned npairs = p.n / 2u + (p.n & 1u);   // (n + 1) / 2 without wrapping at 2^32-1
     const unsigned stride = gridDim.x * kK1Threads * kK1Unroll;
     unsigned q0 = blockIdx.x * (kK1Threads * kK1Unroll) + threadIdx.x;
     // full iterations: every pair valid (2q+1 < n  <=>  q < n/2)
@@ -649,19 +649,19 @@ __global__ void __launch_bounds__(kK1Threads + (TMA ? 32 : 0), 2) k1_extremes(co
 
 template <int NANG, bool VEC, bool TMA>
 cudaError_t launch_t(const K1Params& p, cudaStream_t s, int* launches) {
-    static int k1_blocks = 0, seed_blocks = 0;
+    static std::once_flag once[kMaxDevices];
+    static int cap[kMaxDevices];
     const int smem = TMA ? kK1Stages * kK1StagePairs * 16 : 0;
-    if (!k1_blocks) {
+    const int k1_blocks = per_device(once, cap, [&] {
         if (TMA)
             cudaFuncSetAttribute(k1_extremes<NANG, VEC, TMA>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1_extremes<NANG, VEC, TMA>, kK1Threads + (TMA ? 32 : 0), smem);
-        const int sms = device_sm_count();
-        k1_blocks = per_sm * sms;
-        if (k1_blocks > kMaxK1Blocks) k1_blocks = kMaxK1Blocks;
-        if (k1_blocks < 1) k1_blocks = 1;
-        seed_blocks = 2 * sms;
-    }
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1_extremes<NANG, VEC, TMA>,
+                                                      kK1Threads + (TMA ? 32 : 0), smem);
+        int b = per_sm * device_sm_count();
+        return b > kMaxK1Blocks ? kMaxK1Blocks : (b < 1 ? 1 : b);
+    });
+    const int seed_blocks = 2 * device_sm_count();
     const unsigned long long npairs = (p.n + 1ull) / 2ull;
     unsigned blocks = (unsigned)((npairs + kK1Threads * kK1Unroll - 1) / (kK1Threads * kK1Unroll));
     if (blocks > (unsigned)k1_blocks) blocks = (unsigned)k1_blocks;
@@ -680,22 +680,26 @@ template <int NANG>
 cudaError_t launch_n(const K1Params& p, int vec16, cudaStream_t s, int* launches) {
     // 16-B aligned input streams through the TMA ring; 8-B aligned input uses
     // register loads (cp.async.bulk needs 16-B aligned sources).
-    if (vec16) return p.use_tma ? launch_t<NANG, true, true>(p, s, launches)
-                                : launch_t<NANG, true, false>(p, s, launches);
+    if (vec16) return launch_t<NANG, true, true>(p, s, launches);
     return launch_t<NANG, false, false>(p, s, launches);
 }
 
 }  // namespace
 
+int current_device() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+    return dev;
+}
+
 int device_sm_count() {
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (sms <= 0) sms = 148;
-    }
-    return sms;
+    static std::once_flag once[kMaxDevices];
+    static int sms[kMaxDevices];
+    return per_device(once, sms, [] {
+        int v = 0;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, current_device());
+        return v > 0 ? v : 148;
+    });
 }
 
 int launch_extremes(const K1Params& p, int vec16, void* stream, int* launches) {

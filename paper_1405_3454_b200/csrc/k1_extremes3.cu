@@ -72,7 +72,7 @@ __device__ __forceinline__ void load_quad(const float* __restrict__ pts, unsigne
         Q.v[8] = c.x, Q.v[9] = c.y, Q.v[10] = c.z, Q.v[11] = c.w;
     } else {
 #pragma unroll
-        for (int j = 0; j < 12; ++j) Q.v[j] = (unsigned)(j / 3) < valid ? __ldg(pts + 3u * i0 + j) : 0.0f;
+        for (int j = 0; j < 12; ++j) Q.v[j] = (unsigned)(j / 3) < valid ? __ldg(pts + 3ull * i0 + j) : 0.0f;
         if (valid > 0u)   // pad the tail with copies of the quad's first point (no effect on any key)
 #pragma unroll
             for (int j = 3; j < 12; ++j)
@@ -211,7 +211,7 @@ __global__ void __launch_bounds__(kK13Threads, NANG >= 8 ? 1 : 2) k1_extremes3(c
     lane_init<NANG>(L);
     unsigned bad = 0, nexact = 0;
     const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-    const unsigned nq = (p.n + 3u) / 4u;
+    const unsigned nq = p.n / 4u + ((p.n & 3u) != 0u);   // ceil(n / 4) without wrapping near 2^32
     const unsigned gwarps = gridDim.x * (kK13Threads / 32);
     const unsigned gw = blockIdx.x * (kK13Threads / 32) + warp;
     // warp-uniform loop: each warp takes kK13Quads*32 consecutive quads per
@@ -338,7 +338,7 @@ __global__ void __launch_bounds__(kK13Threads, NANG >= 8 ? 1 : 2) k1_extremes3(c
 
 template <int NANG>
 int launch_n(const K13Params& p, void* stream) {
-    const unsigned nq = (p.n + 3u) / 4u;
+    const unsigned nq = p.n / 4u + ((p.n & 3u) != 0u);   // ceil(n / 4) without wrapping near 2^32
     const unsigned per_block = kK13Threads * kK13Quads;
     unsigned blocks = (nq + per_block - 1) / per_block;
     const unsigned cap = (unsigned)device_sm_count() * 2u;

@@ -345,14 +345,15 @@ __global__ void __launch_bounds__(kK2Threads, 2) k2_filter(const __grid_constant
 
 template <bool VEC, int EDGES>
 cudaError_t launch_t(const K2Params& p, cudaStream_t s, int* launches) {
-    static int max_blocks = 0;
+    static std::once_flag once[kMaxDevices];
+    static int cap[kMaxDevices];
     const int smem = (int)sizeof(K2Smem);
-    if (!max_blocks) {
+    const int max_blocks = per_device(once, cap, [&] {
         cudaFuncSetAttribute(k2_filter<VEC, EDGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         int per_sm = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2_filter<VEC, EDGES>, kK2Threads, smem);
-        max_blocks = (per_sm > 0 ? per_sm : 1) * device_sm_count();
-    }
+        return (per_sm > 0 ? per_sm : 1) * device_sm_count();
+    });
     unsigned blocks = p.num_tiles < (unsigned)max_blocks ? p.num_tiles : (unsigned)max_blocks;
     if (blocks < 1) blocks = 1;
     k2_filter<VEC, EDGES><<<blocks, kK2Threads, smem, s>>>(p);
@@ -362,31 +363,13 @@ cudaError_t launch_t(const K2Params& p, cudaStream_t s, int* launches) {
 
 }  // namespace
 
-int k2_use_tma() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("CUDAPRE_K2_TMA");
-        v = e ? atoi(e) : 1;
-    }
-    return v;
-}
-
-int k2_warps() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("CUDAPRE_K2_WARPS");
-        v = (e && atoi(e) == 10) ? 10 : 8;
-    }
-    return v;
-}
-
+// 16-B aligned input: the warp-specialised TMA-ring kernel (handles every ring
+// mode); 8-B aligned input: this register-loading kernel.
 int launch_filter(const K2Params& p, int vec16, void* stream, int* launches) {
-    if (vec16 && k2_use_tma())   // (handles every mode)
-        return k2_warps() == 10 ? launch_filter_tma10(p, stream, launches) : launch_filter_tma(p, stream, launches);
+    if (vec16) return launch_filter_tma(p, stream, launches);
     cudaStream_t s = (cudaStream_t)stream;
-    if (p.edges <= 16)
-        return vec16 ? (int)launch_t<true, 16>(p, s, launches) : (int)launch_t<false, 16>(p, s, launches);
-    return vec16 ? (int)launch_t<true, 32>(p, s, launches) : (int)launch_t<false, 32>(p, s, launches);
+    if (p.edges <= 16) return (int)launch_t<false, 16>(p, s, launches);
+    return (int)launch_t<false, 32>(p, s, launches);
 }
 
 }  // namespace cudapre

@@ -215,7 +215,7 @@ __device__ __forceinline__ unsigned load_quad(const float* __restrict__ pts, uns
         v[6] = b.z, v[7] = b.w, v[8] = c.x, v[9] = c.y, v[10] = c.z, v[11] = c.w;
     } else {
 #pragma unroll
-        for (int j = 0; j < 12; ++j) v[j] = (unsigned)(j / 3) < valid ? __ldg(pts + 3u * i0 + j) : 0.0f;
+        for (int j = 0; j < 12; ++j) v[j] = (unsigned)(j / 3) < valid ? __ldg(pts + 3ull * i0 + j) : 0.0f;
     }
     return valid;
 }
@@ -432,12 +432,13 @@ int launch_filter3(const K23Params& p, void* stream, int* launches) {
     if (blocks > p.num_tiles) blocks = p.num_tiles;
     if (blocks == 0) blocks = 1;
     cudaStream_t s = (cudaStream_t)stream;
-    static bool attr = false;
-    if (!attr) {   // the staging area takes the block past the 48 KB static limit
+    static std::once_flag once[kMaxDevices];
+    static int done[kMaxDevices];
+    per_device(once, done, [] {   // the staging area takes the block past the 48 KB static limit (per device)
         cudaFuncSetAttribute(k2_filter3<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem3));
         cudaFuncSetAttribute(k2_filter3<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem3));
-        attr = true;
-    }
+        return 1;
+    });
     if (p.vec)
         k2_filter3<true><<<blocks, kK23Threads, sizeof(Smem3), s>>>(p);
     else

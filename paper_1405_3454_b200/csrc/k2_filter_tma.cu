@@ -36,8 +36,6 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
-#include <cstdio>
-#include <cstdlib>
 
 #include "k2_common.cuh"
 #include "tma.cuh"
@@ -45,14 +43,10 @@
 namespace cudapre {
 namespace {
 
-// K2_NW: compute warps per block (8 here; k2_filter_tma10.cu builds the same
-// source with 10).  A warp chunk is always 256 points; a sub-tile is NW
-// chunks, a super-tile 8 sub-tiles.
-#ifndef K2_NW
-#define K2_NW 8
-#define K2_ENTRY launch_filter_tma
-#endif
-constexpr int kW = K2_NW;
+// kW compute warps per block.  A warp chunk is always 256 points; a sub-tile
+// is kW chunks, a super-tile 8 sub-tiles.  (10 compute warps measured the
+// same as 8, profiles/r01_experiments.md.)
+constexpr int kW = 8;
 constexpr int kGroups = kK2Sub * kW;                 // groups (sub, warp) per super-tile
 constexpr unsigned kChunkPairs = 128;                // 256 points per warp chunk
 constexpr unsigned kSubPairsT = kW * kChunkPairs;    // pairs per sub-tile (16 KiB at 8 warps)
@@ -63,10 +57,16 @@ constexpr unsigned kBlock = kW * 32 + 64;            // compute warps + producer
 constexpr unsigned kProdWarp = kW, kEmitWarp = kW + 1;
 constexpr int kBufs = kK2Bufs;                       // survivor-list buffers (tiles in flight)
 
+// 4-stage ring, 96-entry lists (~110 KB of shared memory, 2 blocks per SM).
+// Overflowing lists spill to global scratch, so the list size only trades
+// shared memory for traffic (a 3-stage ring with 128-entry lists measured the
+// same, profiles/r01_experiments.md).
+constexpr int kNst = 4;
+constexpr unsigned kL = 96;
+
 using SurvT = SurvEntry;   // meta = (sub << 8) | loc, loc = r*32 + lane = point offset in the warp chunk
 static_assert(kK2Bufs == 3 && kK2WarpPts == kK2Sub * 2 * (int)kChunkPairs && kW <= kK2MaxWarps, "layout");
 
-template <unsigned kL>
 struct TileT {
     SurvT list[kW][kL];                 // per-warp survivors in index order
     unsigned lstart[kW][kK2Sub + 1];    // list position where (warp, sub) starts; [kK2Sub] = total
@@ -75,12 +75,11 @@ struct TileT {
     unsigned tile;                      // super-tile id (kNone: end of work)
 };
 
-template <int kNst, unsigned kL>
 struct SmemT {
     float4 ring[kNst][kSubPairsT];
     unsigned long long full[kNst];
     unsigned long long empty[kNst];
-    TileT<kL> ts[kBufs];
+    TileT ts[kBufs];
     unsigned long long tile_done[kBufs];   // compute warps -> emit warp (count kW)
     unsigned long long buf_free[kBufs];    // emit warp -> compute warps (count 1)
     unsigned long long agg[kBufs];         // (compute warps done << 32) | survivors so far
@@ -108,8 +107,8 @@ __device__ __forceinline__ float rcp_approx(float a) {
 // |g| is within 2 Emax, then the exact predicate over the whole ring.
 // Mode 1 (degenerate ring: keep everything) and mode 2 (coefficients out of
 // float range: exact predicate only) take the uniform early exits.
-template <int EDGES, int kNst, unsigned kL>
-__device__ __forceinline__ bool classify_queued(const SmemT<kNst, kL>& S, int mode, float ox, float oy,
+template <int EDGES>
+__device__ __forceinline__ bool classify_queued(const SmemT& S, int mode, float ox, float oy,
                                                 float e2max, float x, float y) {
     if (mode != 0) return mode == 1 ? true : !exact_inside(S.geo, x, y);
     const float2 d = __fadd2_rn(make_float2(x, y), make_float2(-ox, -oy));
@@ -160,8 +159,7 @@ __device__ __forceinline__ unsigned chunk_point(unsigned sub, unsigned warp, uns
 // prefix ex: list entries [0, kL) from shared memory, the overflow [kL, wc)
 // from the block's global scratch (written by the compute warp before it
 // signalled the tile done; L2-coherent loads)
-template <unsigned kL>
-__device__ __forceinline__ void emit_t(const K2Params& p, const TileT<kL>& ts, const SurvT* ovf, unsigned tile,
+__device__ __forceinline__ void emit_t(const K2Params& p, const TileT& ts, const SurvT* ovf, unsigned tile,
                                        unsigned long long ex, unsigned warp, unsigned lane) {
     const unsigned long long tpt = (unsigned long long)tile * (2u * kTilePairsT);
     float2* out_pts = reinterpret_cast<float2*>(p.out_pts);
@@ -185,23 +183,11 @@ __device__ __forceinline__ void emit_t(const K2Params& p, const TileT<kL>& ts, c
     }
 }
 
-// CFG 0: 4-stage ring, 96-entry lists (default: ~110 KB of shared memory,
-// 2 blocks per SM); CFG 1: 3-stage ring, 128-entry lists.  Overflowing lists
-// spill to global scratch, so the list size only trades smem for traffic.
-template <int CFG> struct K2Cfg;
-#ifndef K2_KL
-#define K2_KL 96
-#endif
-template <> struct K2Cfg<0> { static constexpr int kNst = K2_NW == 10 ? 3 : 4; static constexpr unsigned kL = K2_KL; static constexpr int kMinB = 2; };
-template <> struct K2Cfg<1> { static constexpr int kNst = 3; static constexpr unsigned kL = 128; static constexpr int kMinB = 2; };
 
-// DBG: perf-experiment build with per-warp cycle counters (CUDAPRE_K2_DEBUG=2)
-template <int EDGES, int CFG, bool DBG>
-__global__ void __launch_bounds__(kBlock, K2Cfg<CFG>::kMinB) k2_filter_tma(const __grid_constant__ K2Params p) {
-    constexpr int kNst = K2Cfg<CFG>::kNst;
-    constexpr unsigned kL = K2Cfg<CFG>::kL;
+template <int EDGES>
+__global__ void __launch_bounds__(kBlock, 2) k2_filter_tma(const __grid_constant__ K2Params p) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    SmemT<kNst, kL>& S = *reinterpret_cast<SmemT<kNst, kL>*>(smem_raw);
+    SmemT& S = *reinterpret_cast<SmemT*>(smem_raw);
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const unsigned lt = (1u << lane) - 1u;
     const unsigned epoch = *(volatile unsigned*)&p.ws->epoch;
@@ -279,14 +265,11 @@ __global__ void __launch_bounds__(kBlock, K2Cfg<CFG>::kMinB) k2_filter_tma(const
     // compute warps never wait for any of this.
     if (warp == kEmitWarp) {
         unsigned lb_rounds = 0, lb_spins = 0;
-        unsigned long long dce[4] = {0, 0, 0, 0}, te = 0;   // DBG: wait, scan, resolve, emit
         unsigned pend = kNone, pbuf = 0;
         for (unsigned k = 0;; ++k) {
             const unsigned bi = k % kBufs;
-            TileT<kL>& cur = S.ts[bi];
-            if (DBG) te = clock64();
+            TileT& cur = S.ts[bi];
             mbar_sleep_wait(a_done + 8u * bi, (k / kBufs) & 1u);
-            if (DBG) { const unsigned long long t = clock64(); dce[0] += t - te; te = t; }
             const unsigned tile = cur.tile;
             if (tile != kNone) {
                 // lane l owns groups g = l*kGroupsPerLane + i (g = sub*kW + w, index order)
@@ -320,9 +303,8 @@ __global__ void __launch_bounds__(kBlock, K2Cfg<CFG>::kMinB) k2_filter_tma(const
                 }
                 __syncwarp();
             }
-            if (DBG) { const unsigned long long t = clock64(); dce[1] += t - te; te = t; }
             if (pend != kNone) {
-                TileT<kL>& prv = S.ts[pbuf];
+                TileT& prv = S.ts[pbuf];
                 unsigned long long ex = 0;
                 if (pend != 0) {
                     ex = resolve(p, pend, epoch, lane, lb_rounds, lb_spins);
@@ -331,7 +313,6 @@ __global__ void __launch_bounds__(kBlock, K2Cfg<CFG>::kMinB) k2_filter_tma(const
                         if (pend == p.num_tiles - 1) p.ws->count = ex + prv.total;
                     }
                 }
-                if (DBG) { const unsigned long long t = clock64(); dce[2] += t - te; te = t; }
                 // per-warp passes (measured faster than one flat pass over the tile:
                 // a quicker emit warp reaches the next look-back before the
                 // other blocks' aggregates are out and spins; r01_experiments.md)
@@ -340,17 +321,12 @@ __global__ void __launch_bounds__(kBlock, K2Cfg<CFG>::kMinB) k2_filter_tma(const
                     emit_t(p, prv, sbase + (size_t)(pbuf * kW + w) * kK2WarpPts, pend, ex, w, lane);
                 __syncwarp();
                 if (lane == 0) mbar_arrive_a(a_free + 8u * pbuf);
-                if (DBG) { const unsigned long long t = clock64(); dce[3] += t - te; te = t; }
             }
             if (tile == kNone) break;
             pend = tile;
             pbuf = bi;
         }
         if (lane == 0) {
-            if (DBG) {
-                unsigned long long* d = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(p.ws) + kWsDbgOffset);
-                for (int i = 0; i < 4; ++i) atomicAdd(&d[16 + i], dce[i]);
-            }
             if (lb_rounds) atomicAdd(&p.ws->lb_rounds, lb_rounds);
             if (lb_spins) atomicAdd(&p.ws->lb_spins, lb_spins);
             __threadfence();
@@ -375,16 +351,13 @@ __global__ void __launch_bounds__(kBlock, K2Cfg<CFG>::kMinB) k2_filter_tma(const
     const float gox = S.geo.ox, goy = S.geo.oy, gr2 = S.geo.r2, ge2 = S.geo.e2max;
     const float gbx0 = S.geo.bx0, gbx1 = S.geo.bx1, gby0 = S.geo.by0, gby1 = S.geo.by1;
     unsigned seq = 0;
-    unsigned long long dc[2] = {0, 0}, t0 = 0;   // DBG: pass A, buffer waits
     for (unsigned k = 0;; ++k) {
         const unsigned bi = k % kBufs;
-        TileT<kL>& cur = S.ts[bi];
+        TileT& cur = S.ts[bi];
         mbar_sleep_wait(a_full + 8u * (seq % kNst), (seq / kNst) & 1u);
         const unsigned tile = S.stile[seq % kNst];
         const bool have = tile != kNone;
-        if (DBG) t0 = clock64();
         if (k >= (unsigned)kBufs) mbar_sleep_wait(a_free + 8u * bi, ((k / kBufs) - 1u) & 1u);
-        if (DBG) { const unsigned long long t = clock64(); dc[1] += t - t0; t0 = t; }
         if (have) {
             unsigned wc = 0;
             SurvT* const wscr = sbase + (size_t)(bi * kW + warp) * kK2WarpPts;
@@ -401,19 +374,7 @@ __global__ void __launch_bounds__(kBlock, K2Cfg<CFG>::kMinB) k2_filter_tma(const
                 const float2* chunk2 = reinterpret_cast<const float2*>(chunk);
                 unsigned needy = 0u;   // bit r: point r*32 + lane not decided by the fast test
                 if (np == (unsigned)kSubPairsT) {
-                    if (p.debug == 1 || p.debug == 3) {
-                        // perf experiments only (wrong results): 1 = skeleton, nothing
-                        // survives; 3 = no classification, 1/32 of the points
-                        // (a hash of the global index) survive
-#pragma unroll
-                        for (int r = 0; r < 8; ++r) {
-                            const float x = chunk2[r * 32 + lane].x;
-                            const unsigned h = (tile * (2u * kTilePairsT) + sub * (2u * kSubPairsT) + warp * 256u +
-                                                r * 32u + lane) * 2654435761u;
-                            const bool sel = p.debug == 1 ? x == 12345.0f : (h >> 27) == 0u;
-                            needy |= (sel ? 1u : 0u) << r;
-                        }
-                    } else if (fast == 0) {
+                    if (fast == 0) {
 #pragma unroll
                         for (int r = 0; r < 8; ++r) {
                             const float2 v = chunk2[r * 32 + lane];
@@ -471,7 +432,7 @@ __global__ void __launch_bounds__(kBlock, K2Cfg<CFG>::kMinB) k2_filter_tma(const
                             } else {   // the unpaired last point
                                 q = __ldg(reinterpret_cast<const float2*>(p.pts) + 2u * full_pairs);
                             }
-                            kp = p.debug == 3 ? true : classify_queued<EDGES>(S, mode, gox, goy, ge2, q.x, q.y);
+                            kp = classify_queued<EDGES>(S, mode, gox, goy, ge2, q.x, q.y);
                         }
                         const unsigned kb = __ballot_sync(kFull, kp);
                         if (kp) {
@@ -511,58 +472,36 @@ __global__ void __launch_bounds__(kBlock, K2Cfg<CFG>::kMinB) k2_filter_tma(const
             }
             mbar_arrive_a(a_done + 8u * bi);
         }
-        if (DBG) { const unsigned long long t = clock64(); dc[0] += t - t0; }
         if (!have) break;
-    }
-    if (DBG && lane == 0) {
-        unsigned long long* d = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(p.ws) + kWsDbgOffset);
-        atomicAdd(&d[warp], dc[0]);
-        atomicAdd(&d[8 + warp], dc[1]);
     }
 }
 
-template <int EDGES, int CFG, bool DBG = false>
+template <int EDGES>
 cudaError_t launch_tma_t(const K2Params& p, cudaStream_t s, int* launches) {
-    static int max_blocks = 0;
-    const int smem = (int)sizeof(SmemT<K2Cfg<CFG>::kNst, K2Cfg<CFG>::kL>);
-    if (!max_blocks) {
-        cudaFuncSetAttribute(k2_filter_tma<EDGES, CFG, DBG>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    static std::once_flag once[kMaxDevices];
+    static int cap[kMaxDevices];
+    const int smem = (int)sizeof(SmemT);
+    const int max_blocks = per_device(once, cap, [&] {
+        cudaFuncSetAttribute(k2_filter_tma<EDGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2_filter_tma<EDGES, CFG, DBG>, kBlock, smem);
-        max_blocks = (per_sm > 0 ? per_sm : 1) * device_sm_count();
-        if (getenv("CUDAPRE_K2_VERBOSE"))
-            fprintf(stderr, "k2_filter_tma<%d warps>: %d B shared memory, %d threads, %d blocks/SM\n", K2_NW, smem,
-                    (int)kBlock, per_sm);
-    }
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2_filter_tma<EDGES>, kBlock, smem);
+        return (per_sm > 0 ? per_sm : 1) * device_sm_count();
+    });
     unsigned blocks = p.num_tiles < (unsigned)max_blocks ? p.num_tiles : (unsigned)max_blocks;
     if (blocks > p.scratch_blocks) blocks = p.scratch_blocks;   // one overflow scratch area per block
     if (blocks < 1) return cudaErrorInvalidValue;               // (workspace checked by the caller)
-    k2_filter_tma<EDGES, CFG, DBG><<<blocks, kBlock, smem, s>>>(p);
+    k2_filter_tma<EDGES><<<blocks, kBlock, smem, s>>>(p);
     ++*launches;
     return cudaGetLastError();
 }
 
-int k2_cfg() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("CUDAPRE_K2_CFG");
-        v = e ? atoi(e) : 0;
-        if (v < 0 || v > 1) v = 0;
-    }
-    return v;
-}
-
 }  // namespace
 
-int K2_ENTRY(const K2Params& p_in, void* stream, int* launches) {
+int launch_filter_tma(const K2Params& p_in, void* stream, int* launches) {
     cudaStream_t s = (cudaStream_t)stream;
     K2Params p = p_in;   // this kernel's super-tiles: kTilePairsT pairs
     p.num_tiles = (unsigned)((2ull * kTilePairsT - 1 + p.n) / (2ull * kTilePairsT));
-    if (p.debug == 2)
-        return p.edges <= 16 ? (int)launch_tma_t<16, 0, true>(p, s, launches) : (int)launch_tma_t<32, 0, true>(p, s, launches);
-    if (k2_cfg() == 1)
-        return p.edges <= 16 ? (int)launch_tma_t<16, 1>(p, s, launches) : (int)launch_tma_t<32, 1>(p, s, launches);
-    return p.edges <= 16 ? (int)launch_tma_t<16, 0>(p, s, launches) : (int)launch_tma_t<32, 0>(p, s, launches);
+    return p.edges <= 16 ? (int)launch_tma_t<16>(p, s, launches) : (int)launch_tma_t<32>(p, s, launches);
 }
 
 }  // namespace cudapre

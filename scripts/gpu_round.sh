@@ -7,7 +7,6 @@ run smoke 300 python __graft_entry__.py smoke
 run pytest_gpu 1800 python -m pytest tests -m gpu -x -q ${PYTEST_K:+-k "$PYTEST_K"}
 run bench_c2b 300 python bench.py --config C2b --steps 50 --warmup 5 --no-cpu-baseline
 run bench_c5 600 python bench.py
-CUDAPRE_K2_DEBUG=1 run bench_c5_skel 300 python bench.py --no-e2e --no-cpu-baseline
 if [ -z "$NO_NCU" ]; then
 CMD="python bench.py --steps 3 --warmup 2 --no-e2e --no-cpu-baseline"
 run plain 300 $CMD && run ncu_launches 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $CMD

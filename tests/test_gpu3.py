@@ -19,7 +19,7 @@ pytestmark = pytest.mark.gpu
 THREADS = max(1, min(64, os.cpu_count() or 1))
 
 
-def _run(xyz, angles="A", index_base=0, view_offset=0):
+def _run(xyz, angles="A", index_base=0, view_offset=0, flags=0):
     if view_offset:
         full = torch.from_numpy(np.ascontiguousarray(np.concatenate([np.zeros((view_offset, 3), np.float32),
                                                                        xyz]))).cuda()
@@ -27,8 +27,9 @@ def _run(xyz, angles="A", index_base=0, view_offset=0):
     else:
         pts = torch.from_numpy(np.ascontiguousarray(xyz)).cuda()
     ext = cp.extremes3(pts, angles, index_base=index_base)
-    idx, sp, poly = cp.filter3(pts, ext, index_base=index_base)
+    idx, sp, poly = cp.filter3(pts, ext, index_base=index_base, flags=flags)
     torch.cuda.synchronize()
+    assert poly.raw.empty_cells == 0   # the direction-cell fail-safe never fires
     return ext, idx.cpu().numpy(), sp.cpu().numpy(), poly
 
 
@@ -135,13 +136,12 @@ def test_large_sampled():
     del host
 
 
-def test_every_facet_path(monkeypatch):
+def test_every_facet_path():
     """Without direction cells (the host's fallback when the rounded centre is
     not strictly inside) every point goes through the warp-cooperative pass
     over all facets: the same survivors."""
-    monkeypatch.setenv("CUDAPRE3_NO_CELLS", "1")
     for fam, n in (("ball", 300_007), ("cube", 100_003)):
-        ext, idx, poly = _check(synth.generate3(fam, n, seed=31))
+        ext, idx, poly = _check(synth.generate3(fam, n, seed=31), flags=cp.FLAG3_NO_CELLS)
         assert poly.raw.cells == 0
 
 

@@ -261,29 +261,23 @@ def test_nccl_group_path_under_torchrun():
     assert "nccl ok" in res.stdout
 
 
-@pytest.mark.parametrize("k1_tma,k2_tma", [("0", "0"), ("0", "1"), ("1", "0")])
-def test_register_kernel_fallbacks_match(k1_tma, k2_tma):
-    """CUDAPRE_K1_TMA=0 / CUDAPRE_K2_TMA=0 route 16-B aligned input through
-    the register-loading K1 / K2 kernels instead of the warp-specialised
-    cp.async.bulk ones; they must give the same bytes: extreme indices and
-    survivors (separate process: the switches are read once per process)."""
-    import subprocess
-    import sys
-
-    code = ("import numpy as np, torch, oracle, synth, paper_1405_3454_b200 as cp\n"
-            "for fam, n in (('disk', 1000003), ('square', 400001), ('circle', 300007)):\n"
-            "    xy = synth.generate(fam, n, seed=3)\n"
-            "    d = torch.from_numpy(xy).cuda()\n"
-            "    ext = cp.extremes(d, 'A')\n"
-            "    assert np.array_equal(ext.idx, oracle.extremes(xy, 'A', threads=8)), fam\n"
-            "    idx, sp, rep = cp.cuda_pre(d)\n"
-            "    want = oracle.cudapre(xy, 'A', threads=8)\n"
-            "    assert np.array_equal(idx.cpu().numpy(), want['survivors']), fam\n"
-            "print('reg ok')\n")
-    env = dict(os.environ, CUDAPRE_K1_TMA=k1_tma, CUDAPRE_K2_TMA=k2_tma)
-    res = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600,
-                         env=env, cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-    assert res.returncode == 0 and "reg ok" in res.stdout, res.stderr[-3000:]
+@pytest.mark.parametrize("family,n", [("disk", 1_000_003), ("square", 400_001), ("circle", 300_007),
+                                      ("gauss", 65_537)])
+def test_register_kernels_on_8_byte_aligned_input(family, n):
+    """8-byte (not 16-byte) aligned input takes the register-loading K1 / K2
+    kernels instead of the warp-specialised cp.async.bulk ones (TMA bulk
+    copies need 16-byte aligned sources): same extreme indices, survivors and
+    coordinates as the oracle."""
+    xy = synth.generate(family, n, seed=3)
+    full = torch.from_numpy(np.concatenate([np.zeros((1, 2), np.float32), xy])).cuda()
+    view = full[1:]
+    assert view.data_ptr() % 16 == 8
+    ext = cp.extremes(view, "A")
+    idx, sp, rep = cp.filter(view, ext)
+    want = oracle.cudapre(xy, "A", threads=THREADS)
+    assert np.array_equal(ext.idx, want["ext_idx"])
+    assert np.array_equal(idx.cpu().numpy(), want["survivors"])
+    assert np.array_equal(sp.cpu().numpy(), xy[want["survivors"]])
 
 
 def test_workspace_reuse_across_sizes_and_densities():
