@@ -121,6 +121,66 @@ def oracle_rate(pts_host: np.ndarray, threads: int, angles: str):
     return len(pts_host) / dt, dt
 
 
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+
+    return platform.processor() or "unknown"
+
+
+def oracle_phases(pts_host: np.ndarray, threads: int, angles: str) -> dict:
+    """The oracle's Steps timed one by one on the same bytes:
+    extremes (Step 1), polygon (Step 2), filter (Step 3), hull of the
+    survivors (P:47), in seconds."""
+    import oracle
+
+    t0 = time.perf_counter()
+    ext = oracle.extremes(pts_host, angles, threads=threads)
+    t1 = time.perf_counter()
+    ring = oracle.polygon(pts_host, ext)
+    t2 = time.perf_counter()
+    keep = oracle.filter_mask(pts_host, pts_host[ring], threads=threads) if len(ring) >= 3 else None
+    t3 = time.perf_counter()
+    surv = np.flatnonzero(keep) if keep is not None else np.arange(len(pts_host))
+    oracle.hull(pts_host, surv)
+    t4 = time.perf_counter()
+    return {"extremes": round(t1 - t0, 4), "polygon": round(t2 - t1, 6), "filter": round(t3 - t2, 4),
+            "hull": round(t4 - t3, 4), "survivors": int(len(surv))}
+
+
+def cpu_baseline(pts_dev, n_local: int, threads: int, angles: str, config: str, target_s: float = 12.0) -> dict:
+    """the oracle as it stands on the host cores -- all cores
+    (--threads nproc) and one core pinned to CPU 0 (taskset -c 0), on leading
+    samples of the same workload sized for ~target_s seconds each; per-phase
+    times; the CPU model."""
+    n_s, _ = sized_sample(pts_dev, target_s, threads, angles, min(n_local, 200_000_000))
+    host = pts_dev[:n_s].cpu().numpy()
+    rate, dt = oracle_rate(host, threads, angles)
+    phases = oracle_phases(host, threads, angles)
+    # single thread, pinned to CPU 0
+    old = os.sched_getaffinity(0) if hasattr(os, "sched_getaffinity") else None
+    try:
+        if old is not None:
+            os.sched_setaffinity(0, {min(old)})
+        n1 = max(100_000, min(n_s, int(rate / max(threads, 1) * target_s / 2)))
+        h1 = host[:n1]
+        rate1, dt1 = oracle_rate(h1, 1, angles)
+        phases1 = oracle_phases(h1, 1, angles)
+    finally:
+        if old is not None:
+            os.sched_setaffinity(0, old)
+    return {"value": rate / 1e9, "unit": "Gpts/s", "cores": threads, "kind": "oracle",
+            "sample": f"first {n_s} points of {config} (oracle Steps 1-3, {dt:.1f} s, {threads} threads)",
+            "per_phase_s": phases, "cpu_model": cpu_model(), "host_cpus": os.cpu_count(),
+            "single_thread": {"value": rate1 / 1e9, "unit": "Gpts/s", "cores": 1, "pinned": f"cpu {min(old) if old else 0}",
+                              "sample": f"first {n1} points ({dt1:.1f} s)", "per_phase_s": phases1}}
+
+
 def sized_sample(pts_dev, target_s: float, threads: int, angles: str, cap: int):
     """Pick a sample size that takes about target_s seconds of oracle work."""
     pilot = min(cap, 2_000_000)
@@ -610,11 +670,7 @@ def main():
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
         import oracle
 
-        n_s, _ = sized_sample(pts, 15.0, threads, args.angles, min(n_local, 200_000_000))
-        host = pts[:n_s].cpu().numpy()
-        rate, dt = oracle_rate(host, threads, args.angles)
-        cpu = {"value": rate / 1e9, "unit": "Gpts/s", "cores": threads, "kind": "oracle",
-               "sample": f"first {n_s} points of {args.config} (oracle Steps 1-3, {dt:.1f} s)"}
+        cpu = cpu_baseline(pts, n_local, threads, args.angles, args.config)
 
     if rank == 0:
         line = {

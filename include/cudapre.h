@@ -63,7 +63,8 @@ typedef enum {
     CUDAPRE_ERR_NONFINITE_INPUT = 3,  /* a NaN / Inf coordinate was seen (precondition S:32, A16) */
     CUDAPRE_ERR_CUDA = 4,             /* a CUDA runtime call failed (message has the CUDA error) */
     CUDAPRE_ERR_CAPACITY = 5,         /* survivor buffer too small; *h_count holds the needed size */
-    CUDAPRE_ERR_WORKSPACE = 6         /* workspace smaller than cudapre_workspace_bytes(n) */
+    CUDAPRE_ERR_WORKSPACE = 6,        /* workspace smaller than cudapre_workspace_bytes(n) */
+    CUDAPRE_ERR_NCCL = 7              /* NCCL could not be loaded or a NCCL call failed */
 } cudapre_status;
 
 typedef struct { float x, y; } cudapre_pt; /* == float2 */
@@ -322,6 +323,35 @@ cudapre_status cudapre_graph_create(const cudapre_pt* d_pts, int64_t n_local, in
 cudapre_status cudapre_graph_launch(cudapre_graph_t* g, void* stream);
 cudapre_status cudapre_graph_destroy(cudapre_graph_t* g);
 
+/* ---------------------------------------------------------------- speculative pre-filter
+ * DESIGN.md §6.6.  Step 1 (cudapre_extremes, 16-byte aligned input, <= 4
+ * angles, n_local >= CUDAPRE_SPEC_MIN_N) also sets aside, in the workspace,
+ * the points that are not certainly inside a region D built from a small
+ * sample before the pass ("candidates").  The next Step 3 on the same
+ * workspace and the same input (d_pts, n_local, index_base) checks, after
+ * Step 2, that D lies strictly inside the Step-2 polygon (rigorous / exact
+ * predicates); if so it classifies the candidates only — every other point is
+ * strictly inside the polygon — otherwise it reads every point.  The
+ * survivors are identical either way.  Precondition: the points are
+ * not modified between the two calls.  The candidates are used by at most one
+ * Step 3.
+ * cudapre_spec_info reads the state of the last Step 1 / Step 3 on a
+ * workspace (blocks on `stream`).                                          */
+#define CUDAPRE_SPEC_MIN_N 4194304
+typedef struct {
+    int32_t enabled;           /* Step 1 built D and wrote candidate records */
+    int32_t used;              /* the last Step 3 verified D and classified the candidates only */
+    int32_t seed_vertices;     /* vertices of the sample's polygon D was built from */
+    int32_t region_box;        /* 1: D is the box below, 0: the disk */
+    int64_t candidates;        /* points set aside by Step 1 */
+    int64_t records;           /* 256-point records (8 per 2048-point chunk) */
+    int64_t overflow_records;  /* records with more than 28 candidates (re-read by Step 3) */
+    float centre[2];           /* D's centre */
+    float r2min;               /* the disk |p - centre|^2 < r2min */
+    float box[4];              /* the box x0, x1, y0, y1 (closed) */
+} cudapre_spec_info_t;
+cudapre_status cudapre_spec_info(const void* d_ws, size_t ws_bytes, void* stream, cudapre_spec_info_t* h_out);
+
 /* ---------------------------------------------------------------- final hull on the GPU
  * SURVEY §8 f1 (the paper runs Qhull on the survivors).
  * The canonical ring of the survivors (identical to cudapre_hull on them)
@@ -341,10 +371,84 @@ cudapre_status cudapre_graph_destroy(cudapre_graph_t* g);
  * (degenerate polygon) the chain runs on every survivor.  Synchronises the
  * stream.  CAPACITY if the ring exceeds ring_capacity.                   */
 size_t cudapre_hull_device_bytes(int64_t m);
+/* cudapre_hull_device that also returns the ring's coordinates
+ * (h_ring_pts: host cudapre_pt[ring_capacity], nullable).                  */
+cudapre_status cudapre_hull_device_ex(const cudapre_pt* d_pts, const int64_t* d_ids, int64_t m,
+                                      const cudapre_polygon_t* h_poly, void* d_scratch, size_t scratch_bytes,
+                                      void* stream, int64_t* h_ring, cudapre_pt* h_ring_pts,
+                                      int64_t ring_capacity, int64_t* h_ring_len, int64_t* h_remaining);
 cudapre_status cudapre_hull_device(const cudapre_pt* d_pts, const int64_t* d_ids, int64_t m,
                                    const cudapre_polygon_t* h_poly, void* d_scratch, size_t scratch_bytes,
                                    void* stream, int64_t* h_ring, int64_t ring_capacity,
                                    int64_t* h_ring_len, int64_t* h_remaining);
+
+/* ---------------------------------------------------------------- multi-GPU (e)
+ * One process per GPU.  The points are sharded into contiguous global index
+ * ranges, rank r holding [base_r, base_r + n_r) with base_r increasing in r
+ * (pass base_r as index_base everywhere).  The communicator wraps NCCL, which
+ * is loaded at run time (libnccl.so.2; CUDAPRE_ERR_NCCL if it is missing); it
+ * is bound to the CUDA device current at cudapre_comm_create.
+ *
+ * cudapre_comm_unique_id   rank 0 makes the 128-byte NCCL id (h_id) and the
+ *                          caller distributes it (e.g. a torch broadcast)
+ * cudapre_comm_create      collective over the `world` ranks; *out owned by
+ *                          the caller, freed with cudapre_comm_destroy      */
+typedef struct cudapre_comm cudapre_comm_t;
+cudapre_status cudapre_comm_unique_id(void* h_id);
+cudapre_status cudapre_comm_create(const void* h_id, int32_t rank, int32_t world, cudapre_comm_t** out);
+cudapre_status cudapre_comm_destroy(cudapre_comm_t* comm);
+cudapre_status cudapre_comm_rank(const cudapre_comm_t* comm, int32_t* rank, int32_t* world);
+
+/* Cross-rank combine input: all-gather of every rank's Step-1 result block
+ * (the one cudapre_extremes left at CUDAPRE_WS_RESULT_OFFSET of d_ws) into
+ * d_parts (device, world entries, rank order), enqueued on `stream` (no host
+ * synchronisation; capturable).  Merge with cudapre_polygon_device(d_parts,
+ * world, ...) on the device or cudapre_extremes_merge on the host.        */
+cudapre_status cudapre_comm_allgather_extremes(cudapre_comm_t* comm, const void* d_ws,
+                                               cudapre_extremes_t* d_parts, void* stream);
+
+/* Step 1 of a sharded set with the paper's host Step 2 in mind: K1 on the
+ * local shard (may be empty), the all-gather, and the host merge: h_out =
+ * the single-GPU result of the whole set on every rank (then call
+ * cudapre_filter with it).  Blocks.  EMPTY_INPUT if every shard is empty.   */
+cudapre_status cudapre_extremes_comm(const cudapre_pt* d_pts, int64_t n_local, int64_t index_base,
+                                     int32_t nang, const double* c, const double* s, void* d_ws,
+                                     size_t ws_bytes, cudapre_comm_t* comm, cudapre_extremes_t* d_parts,
+                                     void* stream, cudapre_extremes_t* h_out);
+
+/* Steps 1-3 of a sharded set on the stream, no host synchronisation: K1 on
+ * the local shard (n_local > 0), the all-gather into d_parts, the merge and
+ * Step 2 on the device (every rank builds the same polygon), Step 3 on the
+ * local shard.  Survivors (ascending global indices of this shard) in
+ * d_surv_idx / d_surv_pts, their number in *d_count (device int64).        */
+cudapre_status cudapre_pipeline_comm(const cudapre_pt* d_pts, int64_t n_local, int64_t index_base,
+                                     int32_t nang, const double* c, const double* s, int64_t* d_surv_idx,
+                                     cudapre_pt* d_surv_pts, int64_t capacity, void* d_ws, size_t ws_bytes,
+                                     cudapre_comm_t* comm, cudapre_extremes_t* d_parts, void* stream,
+                                     int64_t* d_count);
+
+/* Survivor collection: every rank passes its `count` survivors (d_idx and,
+ * nullable, d_pts); the root receives all of them in rank order = ascending
+ * global index order (the single-GPU survivor array) in d_out_idx /
+ * d_out_pts (root only; capacity out_capacity, ignored on other ranks).
+ * *h_total = the number of survivors, on every rank.  An all-gather of
+ * (count, capacity) (16 bytes per rank), then one grouped ncclSend /
+ * ncclRecv; blocks.  CAPACITY on every rank alike if the total exceeds the
+ * root's out_capacity (nothing is sent; *h_total says how much is needed). */
+cudapre_status cudapre_gather_survivors(cudapre_comm_t* comm, const int64_t* d_idx, const cudapre_pt* d_pts,
+                                        int64_t count, int32_t root, int64_t* d_out_idx, cudapre_pt* d_out_pts,
+                                        int64_t out_capacity, void* stream, int64_t* h_total);
+
+/* Final hull of the sharded set: each rank's GPU hull of its own
+ * survivors (cudapre_hull_device with its polygon), the rings' vertices
+ * gathered on the root, the root's monotone chain over them: hull(U S_r) =
+ * hull(U hull(S_r)).  The root gets the canonical ring of the whole set (as
+ * cudapre_hull on all survivors) in h_ring; other ranks get *h_ring_len = 0.
+ * Blocks.                                                                   */
+cudapre_status cudapre_hull_comm(cudapre_comm_t* comm, const cudapre_pt* d_pts, const int64_t* d_ids, int64_t m,
+                                 const cudapre_polygon_t* h_poly, void* d_scratch, size_t scratch_bytes,
+                                 int32_t root, void* stream, int64_t* h_ring, int64_t ring_capacity,
+                                 int64_t* h_ring_len);
 
 /* ====================================================================
  * The 3D extension (DESIGN.md §3 B1-B6, §6.5).

@@ -31,9 +31,9 @@ MAX_ANGLES = 8
 MAX_SLOTS = 32
 SECTORS = 1024
 
-OK, ERR_EMPTY, ERR_ARG, ERR_NONFINITE, ERR_CUDA, ERR_CAPACITY, ERR_WORKSPACE = range(7)
+OK, ERR_EMPTY, ERR_ARG, ERR_NONFINITE, ERR_CUDA, ERR_CAPACITY, ERR_WORKSPACE, ERR_NCCL = range(8)
 _STATUS = {1: "EMPTY_INPUT", 2: "INVALID_ARGUMENT", 3: "NONFINITE_INPUT", 4: "CUDA",
-           5: "CAPACITY", 6: "WORKSPACE"}
+           5: "CAPACITY", 6: "WORKSPACE", 7: "NCCL"}
 PRESETS = {"A": 0, "B": 1, "AT": 2, "C": 3, "D": 4}   # {0,30,45,60} {0,30,45,45} {0} {0,22.5,45,67.5} {0,15,..,75}
 
 
@@ -74,6 +74,13 @@ class ReportT(ctypes.Structure):
                 ("lookback_spins", ctypes.c_int64)]
 
 
+class SpecInfoT(ctypes.Structure):
+    _fields_ = [("enabled", ctypes.c_int32), ("used", ctypes.c_int32), ("seed_vertices", ctypes.c_int32),
+                ("region_box", ctypes.c_int32), ("candidates", ctypes.c_int64), ("records", ctypes.c_int64),
+                ("overflow_records", ctypes.c_int64), ("centre", ctypes.c_float * 2), ("r2min", ctypes.c_float),
+                ("box", ctypes.c_float * 4)]
+
+
 EXTREMES_BYTES = ctypes.sizeof(ExtremesT)
 
 MAX_SLOTS3 = 6 * 8     # CUDAPRE3_MAX_SLOTS
@@ -106,7 +113,11 @@ SYMBOLS = ["cudapre_version", "cudapre_last_error", "cudapre_angles_preset",
            "cudapre_run_host", "cudapre_geometry", "cudapre_filter_device", "cudapre_pipeline_device",
            "cudapre_graph_create", "cudapre_graph_launch", "cudapre_graph_destroy",
            "cudapre_polygon_device", "cudapre_filter_geom", "cudapre_hull_device_bytes",
-           "cudapre_hull_device",
+           "cudapre_hull_device", "cudapre_hull_device_ex", "cudapre_spec_info",
+           # multi-GPU (in-library NCCL communicator)
+           "cudapre_comm_unique_id", "cudapre_comm_create", "cudapre_comm_destroy", "cudapre_comm_rank",
+           "cudapre_comm_allgather_extremes", "cudapre_extremes_comm", "cudapre_pipeline_comm",
+           "cudapre_gather_survivors", "cudapre_hull_comm",
            # the 3D extension
            "cudapre3_workspace_bytes", "cudapre3_orient", "cudapre3_extremes", "cudapre3_extremes_merge",
            "cudapre3_polyhedron", "cudapre3_filter", "cudapre3_filter_ex", "cudapre3_cells", "cudapre3_planes"]
@@ -152,6 +163,17 @@ def lib():
     L.cudapre_hull_device_bytes.argtypes = [i64]
     L.cudapre_hull_device_bytes.restype = sz
     L.cudapre_hull_device.argtypes = [vp, vp, i64, P(PolygonT), vp, sz, vp, vp, i64, P(i64), P(i64)]
+    L.cudapre_spec_info.argtypes = [vp, sz, vp, P(SpecInfoT)]
+    L.cudapre_hull_device_ex.argtypes = [vp, vp, i64, P(PolygonT), vp, sz, vp, vp, vp, i64, P(i64), P(i64)]
+    L.cudapre_comm_unique_id.argtypes = [vp]
+    L.cudapre_comm_create.argtypes = [vp, i32, i32, P(vp)]
+    L.cudapre_comm_destroy.argtypes = [vp]
+    L.cudapre_comm_rank.argtypes = [vp, P(i32), P(i32)]
+    L.cudapre_comm_allgather_extremes.argtypes = [vp, vp, vp, vp]
+    L.cudapre_extremes_comm.argtypes = [vp, i64, i64, i32, vp, vp, vp, sz, vp, vp, vp, P(ExtremesT)]
+    L.cudapre_pipeline_comm.argtypes = [vp, i64, i64, i32, vp, vp, vp, vp, i64, vp, sz, vp, vp, vp, vp]
+    L.cudapre_gather_survivors.argtypes = [vp, vp, vp, i64, i32, vp, vp, i64, vp, P(i64)]
+    L.cudapre_hull_comm.argtypes = [vp, vp, vp, i64, P(PolygonT), vp, sz, i32, vp, vp, i64, P(i64)]
     L.cudapre3_workspace_bytes.argtypes = [i64]
     L.cudapre3_workspace_bytes.restype = sz
     L.cudapre3_orient.argtypes = [vp, vp, vp, vp]
@@ -571,6 +593,23 @@ class Graph:
             pass
 
 
+def spec_info(ws=None, device=None, stream=None) -> dict:
+    """State of the speculative pre-filter of the last Step 1
+    / Step 3 on a workspace (default: this device's cached one)."""
+    torch = _torch()
+    if ws is None:
+        dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        ws = _ws_cache.get(dev.index if dev.index is not None else torch.cuda.current_device())
+        if ws is None:
+            raise ValueError("no workspace on this device yet")
+    out = SpecInfoT()
+    _check(lib().cudapre_spec_info(ws.ptr, ws.nbytes, _stream_ptr(stream), ctypes.byref(out)))
+    return {"enabled": bool(out.enabled), "used": bool(out.used), "seed_vertices": out.seed_vertices,
+            "candidates": out.candidates, "records": out.records, "overflow_records": out.overflow_records,
+            "centre": (out.centre[0], out.centre[1]), "r2min": out.r2min,
+            "region": "box" if out.region_box else "disk", "box": tuple(out.box)}
+
+
 def hull_device(pts, ids, m: int, poly, stream=None, return_remaining: bool = False):
     """Final hull of the survivors pts[:m] (device float2) with
     global ids ids[:m] (device int64), filtered with polygon `poly` (the
@@ -588,6 +627,145 @@ def hull_device(pts, ids, m: int, poly, stream=None, return_remaining: bool = Fa
         ring.ctypes.data_as(ctypes.c_void_p), len(ring), ctypes.byref(n_ring), ctypes.byref(rem)))
     out = ring[: n_ring.value].copy()
     return (out, rem.value) if return_remaining else out
+
+
+# ------------------------------------------------------------------ multi-GPU (in-library NCCL)
+class Comm:
+    """In-library NCCL communicator (cudapre_comm_*), one per process/GPU,
+    bound to the current CUDA device.  ``Comm.from_group(group)`` makes the
+    NCCL id on rank 0 and distributes it with torch.distributed (any backend:
+    plumbing only)."""
+
+    def __init__(self, rank: int, world: int, unique_id: bytes):
+        if len(unique_id) != 128:
+            raise ValueError("the NCCL unique id is 128 bytes")
+        h = ctypes.c_void_p()
+        buf = ctypes.create_string_buffer(unique_id, 128)
+        _check(lib().cudapre_comm_create(buf, int(rank), int(world), ctypes.byref(h)))
+        self._h, self.rank, self.world = h, int(rank), int(world)
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = ctypes.create_string_buffer(128)
+        _check(lib().cudapre_comm_unique_id(buf))
+        return buf.raw
+
+    @classmethod
+    def from_group(cls, group=None):
+        import torch.distributed as dist
+
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        obj = [cls.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group is not None else 0,
+                                   group=group)
+        return cls(rank, world, obj[0])
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if self._h:
+            lib().cudapre_comm_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def extremes_comm(pts, comm: Comm, angles_="A", index_base: int = 0, ws=None, stream=None) -> Extremes:
+    """Step 1 of a sharded set (cudapre_extremes_comm): K1 on the local shard,
+    NCCL all-gather of the ranks' results, host merge: the single-GPU answer."""
+    torch = _torch()
+    pts = _points(pts)
+    n = pts.shape[0]
+    nang, c, s = _angle_arrays(angles_)
+    w = _workspace(max(n, 1), pts.device, ws)
+    parts = torch.empty(comm.world * EXTREMES_BYTES, dtype=torch.uint8, device=pts.device)
+    out = ExtremesT()
+    _check(lib().cudapre_extremes_comm(
+        ctypes.c_void_p(pts.data_ptr()) if n else None, n, index_base, nang,
+        c.ctypes.data_as(ctypes.c_void_p), s.ctypes.data_as(ctypes.c_void_p), w.ptr, w.nbytes,
+        comm.handle, ctypes.c_void_p(parts.data_ptr()), _stream_ptr(stream), ctypes.byref(out)))
+    return Extremes(out)
+
+
+def pipeline_comm(pts, comm: Comm, angles_="A", index_base: int = 0, return_points: bool = True, ws=None,
+                  out_idx=None, out_pts=None, parts=None, stream=None):
+    """Steps 1-3 of a sharded set on the stream (cudapre_pipeline_comm): K1,
+    NCCL all-gather, merge + Step 2 on the device, Step 3 on the local shard;
+    returns (out_idx, out_pts, count) as filter_device."""
+    torch = _torch()
+    pts = _points(pts)
+    n = pts.shape[0]
+    nang, c, s = _angle_arrays(angles_)
+    w = _workspace(n, pts.device, ws)
+    out_idx, out_pts, cap = _outputs(pts, out_idx, out_pts, return_points)
+    if parts is None:
+        parts = torch.empty(comm.world * EXTREMES_BYTES, dtype=torch.uint8, device=pts.device)
+    count = torch.zeros(1, dtype=torch.int64, device=pts.device)
+    _check(lib().cudapre_pipeline_comm(
+        ctypes.c_void_p(pts.data_ptr()), n, index_base, nang,
+        c.ctypes.data_as(ctypes.c_void_p), s.ctypes.data_as(ctypes.c_void_p),
+        ctypes.c_void_p(out_idx.data_ptr()),
+        ctypes.c_void_p(out_pts.data_ptr()) if out_pts is not None else None, cap,
+        w.ptr, w.nbytes, comm.handle, ctypes.c_void_p(parts.data_ptr()), _stream_ptr(stream),
+        ctypes.c_void_p(count.data_ptr())))
+    return out_idx, out_pts, count
+
+
+def gather_survivors(comm: Comm, idx, pts, count: int, root: int = 0, out_idx=None, out_pts=None, stream=None):
+    """Collect every rank's survivors on ``root`` in rank order (= ascending
+    global index: the single-GPU array).  Returns (idx, pts, total) on the
+    root, (None, None, total) elsewhere.  Collective: every rank calls it."""
+    torch = _torch()
+    h_total = ctypes.c_int64()
+    is_root = comm.rank == root
+    cap = out_idx.shape[0] if (is_root and out_idx is not None) else 0
+    for attempt in range(2):
+        st = lib().cudapre_gather_survivors(
+            comm.handle, ctypes.c_void_p(idx.data_ptr()),
+            ctypes.c_void_p(pts.data_ptr()) if pts is not None else None, int(count), int(root),
+            ctypes.c_void_p(out_idx.data_ptr()) if (is_root and out_idx is not None) else None,
+            ctypes.c_void_p(out_pts.data_ptr()) if (is_root and out_pts is not None) else None,
+            cap, _stream_ptr(stream), ctypes.byref(h_total))
+        if st == ERR_CAPACITY and attempt == 0:   # (every rank sees it) size the root's buffers, retry
+            if is_root:
+                cap = h_total.value
+                out_idx = torch.empty(max(cap, 1), dtype=torch.int64, device=idx.device)
+                out_pts = (torch.empty((max(cap, 1), 2), dtype=torch.float32, device=idx.device)
+                           if pts is not None else None)
+            continue
+        _check(st)
+        break
+    m = h_total.value
+    if not is_root:
+        return None, None, m
+    if m == 0:
+        return idx[:0], (pts[:0] if pts is not None else None), 0
+    return out_idx[:m], (out_pts[:m] if out_pts is not None else None), m
+
+
+def hull_comm(comm: Comm, pts, ids, m: int, poly, root: int = 0, stream=None) -> np.ndarray:
+    """Final hull of a sharded set (cudapre_hull_comm): per-rank GPU hulls of
+    the local survivors, their vertices gathered on the root, one chain
+    there.  The canonical ring (global ids) on the root, empty elsewhere."""
+    torch = _torch()
+    m = int(m)
+    nbytes = int(lib().cudapre_hull_device_bytes(m))
+    scratch = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=pts.device)
+    cap = max(m, 1) * comm.world + 64
+    ring = np.empty(cap, np.int64)
+    k = ctypes.c_int64()
+    raw = poly.raw if isinstance(poly, Polygon) else poly
+    _check(lib().cudapre_hull_comm(
+        comm.handle, ctypes.c_void_p(pts.data_ptr()), ctypes.c_void_p(ids.data_ptr()), m, ctypes.byref(raw),
+        ctypes.c_void_p(scratch.data_ptr()), nbytes, int(root), _stream_ptr(stream),
+        ring.ctypes.data_as(ctypes.c_void_p), cap, ctypes.byref(k)))
+    return ring[: k.value].copy()
 
 
 def cuda_pre(pts, angles_="A", group=None, index_base: int = 0, return_points=True, ws=None):

@@ -1,6 +1,17 @@
-"""Run under torchrun: each rank filters its contiguous shard through the
-public API with group=WORLD (NCCL all-gather of the per-rank Step-1 structs),
-then rank 0 gathers the survivors and checks them against the oracle."""
+"""Run under torchrun (one process per GPU): the multi-GPU paths of the public
+API against the oracle on the whole set.
+
+1. torch.distributed group path: cp.cuda_pre(..., group) (NCCL all-gather of
+   the per-rank Step-1 structs + host merge), survivors concatenated in rank
+   order;
+2. the device-resident path: K1 -> NCCL all-gather of the workspace Step-1
+   blocks -> merge + Step 2 on the device -> K2;
+3. the in-library NCCL communicator (cudapre_comm_*): cudapre_extremes_comm
+   (host merge), cudapre_pipeline_comm (Steps 1-3 on the stream), the survivor
+   gather to rank 0 (cudapre_gather_survivors) and the sharded final hull
+   (cudapre_hull_comm);
+4. the 3D extension over NCCL.
+Prints "nccl ok" on rank 0 when every check passed."""
 import os
 import sys
 
@@ -12,23 +23,30 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspa
 import oracle  # noqa: E402
 import paper_1405_3454_b200 as cp  # noqa: E402
 import synth  # noqa: E402
+import synth.cuda as scuda  # noqa: E402
 
 N = int(os.environ.get("NCCL_TEST_N", "3000017"))
+N_SPEC = int(os.environ.get("NCCL_TEST_N_SPEC", "24000017"))   # large enough for the pre-filter on every rank
+
+
+def shard(n, rank, world):
+    n_local = n // world + (1 if rank < n % world else 0)
+    base = rank * (n // world) + min(rank, n % world)
+    return n_local, base
 
 
 def main():
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
     dist.init_process_group("nccl", device_id=torch.device("cuda", torch.cuda.current_device()))
-    n_local = N // world + (1 if rank < N % world else 0)
-    base = rank * (N // world) + min(rank, N % world)
+    n_local, base = shard(N, rank, world)
     xy = synth.generate("disk", n_local, seed=6, base=base)
     pts = torch.from_numpy(xy).cuda()
+    # 1. torch.distributed group path
     idx, sp, rep = cp.cuda_pre(pts, "A", group=dist.group.WORLD, index_base=base)
     counts = [None] * world
     dist.all_gather_object(counts, idx.cpu().numpy())
-    # device-resident path: K1 -> NCCL all-gather of the workspace's Step-1
-    # blocks -> merge + Step 2 on the device -> K2, no host round trip
+    # 2. device-resident path over torch's NCCL
     ws = cp.Workspace(n_local)
     gathered = torch.empty(world * cp.EXTREMES_BYTES, dtype=torch.uint8, device="cuda")
     cp.extremes_device(pts, "A", index_base=base, ws=ws)
@@ -39,11 +57,37 @@ def main():
     cp.filter_geom(pts, index_base=base, ws=ws, out_idx=d_idx, count=d_count)
     torch.cuda.synchronize()
     assert np.array_equal(d_idx[: int(d_count.item())].cpu().numpy(), idx.cpu().numpy()), "device path"
-    # the 3D extension: K1-3D writes its Step-1 block to a device
-    # buffer, NCCL all-gathers the blocks, the host merges them (cp.exchange3)
+    # 3. the in-library communicator
+    comm = cp.Comm.from_group(dist.group.WORLD)
+    assert (comm.rank, comm.world) == (rank, world)
+    ext_c = cp.extremes_comm(pts, comm, "A", index_base=base)
+    assert ext_c.idx.tolist() == rep["extremes"].idx.tolist(), "extremes_comm"
+    o_idx, o_pts, o_cnt = cp.pipeline_comm(pts, comm, "A", index_base=base)
+    torch.cuda.synchronize()
+    m = int(o_cnt.item())
+    assert np.array_equal(o_idx[:m].cpu().numpy(), idx.cpu().numpy()), "pipeline_comm"
+    assert np.array_equal(o_pts[:m].cpu().numpy(), xy[o_idx[:m].cpu().numpy() - base]), "pipeline_comm points"
+    g_idx, g_pts, g_tot = cp.gather_survivors(comm, o_idx, o_pts, m, root=0)
+    poly = cp.polygon(ext_c)
+    ring_c = cp.hull_comm(comm, o_pts, o_idx, m, poly, root=0)
+    # an empty shard on the last rank (world > 1): extremes_comm still gives the global answer
+    if world > 1:
+        e_local, e_base = (n_local, base) if rank < world - 1 else (0, N)
+        e_pts = pts if rank < world - 1 else torch.empty((0, 2), dtype=torch.float32, device="cuda")
+        ext_e = cp.extremes_comm(e_pts, comm, "A", index_base=e_base)
+        assert ext_e.n == N - shard(N, world - 1, world)[0], "empty-shard extremes_comm"
+    # the speculative pre-filter on every shard (n_local >= CUDAPRE_SPEC_MIN_N): per-rank
+    # regions verified against the global polygon
+    ns_local, ns_base = shard(N_SPEC, rank, world)
+    sp_pts = scuda.generate("disk", ns_local, seed=8, base=ns_base)
+    s_idx, s_pts, s_cnt = cp.pipeline_comm(sp_pts, comm, "A", index_base=ns_base)
+    torch.cuda.synchronize()
+    s_m = int(s_cnt.item())
+    s_all, _, s_tot = cp.gather_survivors(comm, s_idx, None, s_m, root=0)
+    s_used = cp.spec_info()["used"]
+    # 4. the 3D extension
     n3 = N // 3
-    n3_local = n3 // world + (1 if rank < n3 % world else 0)
-    base3 = rank * (n3 // world) + min(rank, n3 % world)
+    n3_local, base3 = shard(n3, rank, world)
     xyz = synth.generate3("ball", n3_local, seed=7, base=base3)
     p3 = torch.from_numpy(xyz).cuda()
     dev3 = torch.empty(cp.ctypes.sizeof(cp.Extremes3T), dtype=torch.uint8, device="cuda")
@@ -58,12 +102,21 @@ def main():
         want = oracle.cudapre(full, "A", threads=os.cpu_count())
         assert rep["extremes"].idx.tolist() == want["ext_idx"].tolist(), "Step 1"
         assert np.array_equal(got, want["survivors"]), "Step 3"
+        assert g_tot == len(want["survivors"]), "gather total"
+        assert np.array_equal(g_idx.cpu().numpy(), want["survivors"]), "gathered survivors"
+        assert np.array_equal(g_pts.cpu().numpy(), full[want["survivors"]]), "gathered points"
+        assert ring_c.tolist() == oracle.hull(full).tolist(), "hull_comm"
+        full_s = synth.generate("disk", N_SPEC, seed=8)
+        want_s = oracle.cudapre(full_s, "A", threads=os.cpu_count())
+        assert np.array_equal(s_all.cpu().numpy(), want_s["survivors"]), "pre-filter path, sharded"
         full3 = synth.generate3("ball", n3, seed=7)
         want3 = oracle.cudapre3(full3, "A", threads=os.cpu_count())
         assert ext3.idx.tolist() == want3["ext_idx"].tolist(), "3D Step 1"
         assert poly3.facets.tolist() == want3["facets"].tolist(), "3D Step 2"
         assert np.array_equal(np.concatenate(parts3), want3["survivors"]), "3D Step 3"
-        print(f"nccl ok world={world} survivors={len(got)} 3d={len(want3['survivors'])}")
+        print(f"nccl ok world={world} survivors={len(got)} gathered={g_tot} hull={len(ring_c)} "
+              f"spec_used={s_used} 3d={len(want3['survivors'])}")
+    comm.close()
     dist.barrier()
     dist.destroy_process_group()
 

@@ -193,28 +193,38 @@ def test_config_full_size(name):
     print(f"{name}: n={n} survivors={len(idx)} ({100 * len(idx) / n:.4f}%)")
 
 
-def test_config_c5_2b_sampled():
-    """C5 at its full 2e9 points on one GPU (the bench workload): Step 1 vs the
-    oracle over all 2e9 points (chunked D2H of generator-verified bytes);
-    Step 3 element by element on sampled contiguous index windows."""
+def test_config_c5_full():
+    """C5 at its full 2e9 points on one GPU, the bench workload and launch
+    configuration (device generator, 16-byte aligned, the pre-filter on):
+    every point through the oracle, chunk by chunk (generator-verified bytes
+    D2H): Step 1 merged over the chunks with the lexicographic rule,
+    the oracle's ring, Step 3's keep mask -> the complete survivor index array
+    compared element by element with cudapre_filter (host Step 2) and with the
+    device pipeline; the final hull of the survivors by the oracle compared
+    with cudapre_hull and cudapre_hull_device (P:47)."""
     cfg = dict(synth.CONFIGS["C5"])
     n = cfg.pop("n")
     pts = scuda.generate(cfg["family"], n, seed=cfg["seed"])
-    ext = cp.extremes(pts, "A")
+    ws = cp.Workspace(n)
     cap = n // 16
-    idx, _, rep = cp.filter(pts, ext, out_idx=torch.empty(cap, dtype=torch.int64, device="cuda"),
-                            return_points=False)
-    torch.cuda.synchronize()
+    ext = cp.extremes(pts, "A", ws=ws)
+    idx, sp, rep = cp.filter(pts, ext, ws=ws, out_idx=torch.empty(cap, dtype=torch.int64, device="cuda"),
+                             out_pts=torch.empty((cap, 2), dtype=torch.float32, device="cuda"))
+    used = cp.spec_info(ws)["used"]
     surv = idx.cpu().numpy()
-    assert np.all(np.diff(surv) > 0)
-    # Step 1: oracle over every chunk, merged by the lexicographic rule (S:192)
-    c, s = oracle.coeffs("A")
+    # the device-resident pipeline (Step 2 on the device) into separate buffers
+    d_idx, _, d_cnt = cp.pipeline(pts, "A", ws=ws, out_idx=torch.empty(cap, dtype=torch.int64, device="cuda"),
+                                  return_points=False)
+    torch.cuda.synchronize()
+    assert int(d_cnt.item()) == len(surv)
+    assert bool(torch.equal(d_idx[: len(surv)], idx)), "device pipeline survivors"
+    del d_idx
+    # Step 1: the oracle over every chunk, merged by the lexicographic rule
     best_k = [None] * 16
     best_i = [None] * 16
     chunk = 100_000_000
     for lo in range(0, n, chunk):
-        hi = min(n, lo + chunk)
-        host = pts[lo:hi].cpu().numpy()
+        host = pts[lo:min(n, lo + chunk)].cpu().numpy()
         if lo == 0:
             want = synth.generate("disk", 4096, seed=cfg["seed"])
             assert np.array_equal(host[:4096].view(np.uint32), want.view(np.uint32))
@@ -225,30 +235,58 @@ def test_config_c5_2b_sampled():
             if best_k[sl] is None or (k > best_k[sl] if mx else k < best_k[sl]):
                 best_k[sl], best_i[sl] = k, i
     assert ext.idx.tolist() == best_i
-    # Step 2 (oracle polygon from the oracle's picks) and Step 3 on windows
-    ring_ids = oracle.hull(np.concatenate([pts[i:i + 1].cpu().numpy() for i in best_i]))
-    ring_xy = np.concatenate([pts[best_i[j]:best_i[j] + 1].cpu().numpy() for j in ring_ids])
+    # Step 2 (the oracle's chain on its own picks) and Step 3 on every point
+    picks = np.concatenate([pts[i:i + 1].cpu().numpy() for i in best_i])
+    ring_xy = picks[oracle.hull(picks)]
     assert rep["polygon"].v.tolist() == ring_xy.tolist()
-    rng = np.random.default_rng(0)
-    for lo in [0, n - 1_000_000, *rng.integers(0, n - 1_000_000, 6).tolist()]:
-        hi = lo + 1_000_000
-        host = pts[lo:hi].cpu().numpy()
-        keep = np.flatnonzero(oracle.filter_mask(host, ring_xy, threads=THREADS)) + lo
-        a, b = np.searchsorted(surv, [lo, hi])
-        assert np.array_equal(surv[a:b], keep), lo
+    got_at = 0
+    for lo in range(0, n, chunk):
+        hi = min(n, lo + chunk)
+        keep = np.flatnonzero(oracle.filter_mask(pts[lo:hi].cpu().numpy(), ring_xy, threads=THREADS)) + lo
+        assert np.array_equal(surv[got_at:got_at + len(keep)], keep), lo
+        got_at += len(keep)
+    assert got_at == len(surv)
     frac = len(surv) / n
     assert 0.0330 < frac < 0.0345, frac            # closed form 3.384 % (reading A1)
+    # the final hull of the survivors: the oracle's chain vs the library's two
+    sxy = sp.cpu().numpy()
+    want_ring = surv[oracle.hull(sxy)]
+    assert surv[cp.hull(sxy)].tolist() == want_ring.tolist()
+    assert cp.hull_device(sp, idx, len(surv), rep["polygon"]).tolist() == want_ring.tolist()
+    print(f"C5: {len(surv)} survivors, hull {len(want_ring)} vertices, pre-filter used: {used}")
 
 
-def test_nccl_group_path_under_torchrun():
-    """The multi-rank path of the public API (NCCL all-gather of the per-rank
-    Step-1 structs + host merge) on the GPUs this box has (torchrun, one
-    process per GPU), against the oracle on the whole set."""
+@pytest.mark.parametrize("name", ["C4", "C4e0", "C2b"])
+def test_config_hull_device_full_size(name):
+    """The GPU final hull at full config size, including the
+    near-circle sets where its second filter prunes least."""
+    cfg = dict(synth.CONFIGS[name])
+    n = cfg.pop("n")
+    fam = cfg.pop("family")
+    seed = cfg.pop("seed")
+    xy = synth.generate(fam, n, seed=seed, **cfg)
+    pts = torch.from_numpy(xy).cuda()
+    ext = cp.extremes(pts, "A")
+    idx, sp, rep = cp.filter(pts, ext)
+    torch.cuda.synchronize()
+    surv = idx.cpu().numpy()
+    want = oracle.hull(xy)
+    assert cp.hull_device(sp, idx, len(surv), rep["polygon"]).tolist() == want.tolist()
+
+
+@pytest.mark.parametrize("nproc", [1, 2, 4, 8])
+def test_nccl_paths_under_torchrun(nproc):
+    """The multi-rank paths (torch group path, device-resident path, the
+    in-library NCCL communicator: extremes, Steps 1-3, survivor gather,
+    sharded hull, the pre-filter per shard; 3D) under torchrun, one process
+    per GPU, against the oracle on the whole set (tests/scripts/nccl_cudapre.py)."""
     import socket
     import subprocess
     import sys
 
-    ngpu = torch.cuda.device_count()
+    if torch.cuda.device_count() < nproc:
+        pytest.skip(f"needs {nproc} GPUs (one process per GPU)")
+    ngpu = nproc
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
         port = s.getsockname()[1]
