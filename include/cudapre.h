@@ -323,35 +323,6 @@ cudapre_status cudapre_graph_create(const cudapre_pt* d_pts, int64_t n_local, in
 cudapre_status cudapre_graph_launch(cudapre_graph_t* g, void* stream);
 cudapre_status cudapre_graph_destroy(cudapre_graph_t* g);
 
-/* ---------------------------------------------------------------- speculative pre-filter
- * DESIGN.md §6.6.  Step 1 (cudapre_extremes, 16-byte aligned input, <= 4
- * angles, n_local >= CUDAPRE_SPEC_MIN_N) also sets aside, in the workspace,
- * the points that are not certainly inside a region D built from a small
- * sample before the pass ("candidates").  The next Step 3 on the same
- * workspace and the same input (d_pts, n_local, index_base) checks, after
- * Step 2, that D lies strictly inside the Step-2 polygon (rigorous / exact
- * predicates); if so it classifies the candidates only — every other point is
- * strictly inside the polygon — otherwise it reads every point.  The
- * survivors are identical either way.  Precondition: the points are
- * not modified between the two calls.  The candidates are used by at most one
- * Step 3.
- * cudapre_spec_info reads the state of the last Step 1 / Step 3 on a
- * workspace (blocks on `stream`).                                          */
-#define CUDAPRE_SPEC_MIN_N 4194304
-typedef struct {
-    int32_t enabled;           /* Step 1 built D and wrote candidate records */
-    int32_t used;              /* the last Step 3 verified D and classified the candidates only */
-    int32_t seed_vertices;     /* vertices of the sample's polygon D was built from */
-    int32_t region_box;        /* 1: D is the box below, 0: the disk */
-    int64_t candidates;        /* points set aside by Step 1 */
-    int64_t records;           /* 256-point records (8 per 2048-point chunk) */
-    int64_t overflow_records;  /* records with more than 28 candidates (re-read by Step 3) */
-    float centre[2];           /* D's centre */
-    float r2min;               /* the disk |p - centre|^2 < r2min */
-    float box[4];              /* the box x0, x1, y0, y1 (closed) */
-} cudapre_spec_info_t;
-cudapre_status cudapre_spec_info(const void* d_ws, size_t ws_bytes, void* stream, cudapre_spec_info_t* h_out);
-
 /* ---------------------------------------------------------------- final hull on the GPU
  * SURVEY §8 f1 (the paper runs Qhull on the survivors).
  * The canonical ring of the survivors (identical to cudapre_hull on them)

@@ -74,13 +74,6 @@ class ReportT(ctypes.Structure):
                 ("lookback_spins", ctypes.c_int64)]
 
 
-class SpecInfoT(ctypes.Structure):
-    _fields_ = [("enabled", ctypes.c_int32), ("used", ctypes.c_int32), ("seed_vertices", ctypes.c_int32),
-                ("region_box", ctypes.c_int32), ("candidates", ctypes.c_int64), ("records", ctypes.c_int64),
-                ("overflow_records", ctypes.c_int64), ("centre", ctypes.c_float * 2), ("r2min", ctypes.c_float),
-                ("box", ctypes.c_float * 4)]
-
-
 EXTREMES_BYTES = ctypes.sizeof(ExtremesT)
 
 MAX_SLOTS3 = 6 * 8     # CUDAPRE3_MAX_SLOTS
@@ -113,7 +106,7 @@ SYMBOLS = ["cudapre_version", "cudapre_last_error", "cudapre_angles_preset",
            "cudapre_run_host", "cudapre_geometry", "cudapre_filter_device", "cudapre_pipeline_device",
            "cudapre_graph_create", "cudapre_graph_launch", "cudapre_graph_destroy",
            "cudapre_polygon_device", "cudapre_filter_geom", "cudapre_hull_device_bytes",
-           "cudapre_hull_device", "cudapre_hull_device_ex", "cudapre_spec_info",
+           "cudapre_hull_device", "cudapre_hull_device_ex",
            # multi-GPU (in-library NCCL communicator)
            "cudapre_comm_unique_id", "cudapre_comm_create", "cudapre_comm_destroy", "cudapre_comm_rank",
            "cudapre_comm_allgather_extremes", "cudapre_extremes_comm", "cudapre_pipeline_comm",
@@ -163,7 +156,6 @@ def lib():
     L.cudapre_hull_device_bytes.argtypes = [i64]
     L.cudapre_hull_device_bytes.restype = sz
     L.cudapre_hull_device.argtypes = [vp, vp, i64, P(PolygonT), vp, sz, vp, vp, i64, P(i64), P(i64)]
-    L.cudapre_spec_info.argtypes = [vp, sz, vp, P(SpecInfoT)]
     L.cudapre_hull_device_ex.argtypes = [vp, vp, i64, P(PolygonT), vp, sz, vp, vp, vp, i64, P(i64), P(i64)]
     L.cudapre_comm_unique_id.argtypes = [vp]
     L.cudapre_comm_create.argtypes = [vp, i32, i32, P(vp)]
@@ -591,23 +583,6 @@ class Graph:
             self.close()
         except Exception:
             pass
-
-
-def spec_info(ws=None, device=None, stream=None) -> dict:
-    """State of the speculative pre-filter of the last Step 1
-    / Step 3 on a workspace (default: this device's cached one)."""
-    torch = _torch()
-    if ws is None:
-        dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
-        ws = _ws_cache.get(dev.index if dev.index is not None else torch.cuda.current_device())
-        if ws is None:
-            raise ValueError("no workspace on this device yet")
-    out = SpecInfoT()
-    _check(lib().cudapre_spec_info(ws.ptr, ws.nbytes, _stream_ptr(stream), ctypes.byref(out)))
-    return {"enabled": bool(out.enabled), "used": bool(out.used), "seed_vertices": out.seed_vertices,
-            "candidates": out.candidates, "records": out.records, "overflow_records": out.overflow_records,
-            "centre": (out.centre[0], out.centre[1]), "r2min": out.r2min,
-            "region": "box" if out.region_box else "disk", "box": tuple(out.box)}
 
 
 def hull_device(pts, ids, m: int, poly, stream=None, return_remaining: bool = False):

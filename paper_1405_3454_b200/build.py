@@ -16,14 +16,14 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libcudapre.so")
 BUILD = os.path.join(HERE, "_build")
-SOURCES = ["api.cpp", "host_geom.cpp", "k1_extremes.cu", "k2_filter.cu", "k2_filter_tma.cu", "k2_spec.cu",
+SOURCES = ["api.cpp", "host_geom.cpp", "k1_extremes.cu", "k2_filter.cu", "k2_filter_tma.cu",
            "k_polygon.cu", "k_hull.cu",
            # the 3D extension
            "api3.cpp", "host_geom3.cpp", "comm.cpp", "k1_extremes3.cu", "k2_filter3.cu"]
 # per-file extra flags: the device polygon builder must not contract multiply-adds (it has to agree
 # bit for bit with the host builder, compiled with -ffp-contract=off)
 EXTRA = {"k_polygon.cu": ["-fmad=false"]}
-HEADERS = ["internal.h", "device.h", "spec.cuh", "exact.cuh", "geom.cuh", "k2_common.cuh", "tma.cuh", "internal3.h", "exact3.cuh",
+HEADERS = ["internal.h", "device.h", "exact.cuh", "geom.cuh", "k2_common.cuh", "tma.cuh", "internal3.h", "exact3.cuh",
            os.path.join("..", "..", "include", "cudapre.h")]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-ffp-contract=off,-O2",

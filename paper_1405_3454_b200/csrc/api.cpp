@@ -115,37 +115,19 @@ unsigned long long* ws_status(void* d_ws) {
     return reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(d_ws) + kWsFixedBytes +
                                                  kWsPartialBytes);
 }
-SpecPage* ws_spec(void* d_ws) { return reinterpret_cast<SpecPage*>(reinterpret_cast<char*>(d_ws) + kWsSpecOff); }
-// The overflow scratch and, before it, the candidate records sit at the END
-// of the caller's workspace: the tile-status words start at a fixed offset and
-// are epoch-tagged across calls, so a workspace reused for a smaller n must
-// never write scratch or record data where a larger n's status words live
-// (status(n) grows from the front, records and scratch from the back;
-// ws_bytes >= ws_bytes_for(n) keeps them apart).
-size_t ws_scratch_off(size_t ws_bytes, int64_t n, unsigned* blocks) {
-    const size_t used = kWsFixedBytes + kWsPartialBytes + ws_status_bytes(n) + ws_records_bytes(n) + 256;
+// The overflow scratch sits at the END of the caller's workspace: the
+// tile-status words start at a fixed offset and are epoch-tagged across calls,
+// so a workspace reused for a smaller n must never write scratch data where a
+// larger n's status words live (status(n) grows from the front, scratch from
+// the back; ws_bytes >= ws_bytes_for(n) keeps them apart).
+SurvEntry* ws_scratch(void* d_ws, size_t ws_bytes, int64_t n, unsigned* blocks) {
+    const size_t used = kWsFixedBytes + kWsPartialBytes + ws_status_bytes(n);
     size_t nb = ws_bytes > used + 16 ? (ws_bytes - used - 16) / kK2ScratchPerBlock : 0;
     const size_t want = (size_t)kK2BlocksPerSM * (size_t)device_sm_count();
     if (nb > want) nb = want;
     *blocks = (unsigned)nb;
-    return (ws_bytes - nb * kK2ScratchPerBlock) & ~(size_t)15;
-}
-SurvEntry* ws_scratch(void* d_ws, size_t ws_bytes, int64_t n, unsigned* blocks) {
-    return reinterpret_cast<SurvEntry*>(reinterpret_cast<char*>(d_ws) + ws_scratch_off(ws_bytes, n, blocks));
-}
-// records (kRecBytes each, 8 per chunk) followed by their count bytes
-unsigned char* ws_records(void* d_ws, size_t ws_bytes, int64_t n, unsigned char** counts) {
-    unsigned nb = 0;
-    const size_t end = ws_scratch_off(ws_bytes, n, &nb);
-    const size_t off = (end - ws_records_bytes(n)) & ~(size_t)255;
-    unsigned char* r = reinterpret_cast<unsigned char*>(d_ws) + off;
-    if (counts) *counts = r + 8 * ws_rec_chunks(n) * kRecBytes;
-    return r;
-}
-// The speculative pre-filter applies to 16-B aligned input (K1's TMA ring),
-// <= 4 angles and n_local >= kSpecMinN.
-bool spec_possible(const void* d_pts, int64_t n, int nang) {
-    return (((uintptr_t)d_pts & 15u) == 0) && n >= kSpecMinN && nang <= 4 && ws_rec_chunks(n) > 0;
+    const size_t off = (ws_bytes - nb * kK2ScratchPerBlock) & ~(size_t)15;
+    return reinterpret_cast<SurvEntry*>(reinterpret_cast<char*>(d_ws) + off);
 }
 
 cudapre_status check_points(const cudapre_pt* d_pts, int64_t n) {
@@ -192,27 +174,6 @@ void k2_params(K2Params& p, const cudapre_pt* d_pts, int64_t n_local, int64_t in
     p.num_tiles = (unsigned)((n_local + kK2TilePts - 1) / kK2TilePts);
     p.g = ws_geom(d_ws);
     p.edges = 32;
-    p.sp = nullptr;
-    if (spec_possible(d_pts, n_local, 4)) {   // (the verification checks what K1 actually did)
-        unsigned char* counts = nullptr;
-        p.records = ws_records(d_ws, ws_bytes, n_local, &counts);
-        p.rcount = counts;
-        p.sp = ws_spec(d_ws);
-    }
-}
-
-// Step 3 launches: with the pre-filter possible, the verification first
-// (decides on the device), then both Step-3 kernels (the one not selected
-// exits at once).
-cudaError_t launch_step3(const K2Params& p, int vec16, void* stream, int* launches) {
-    if (p.sp) {
-        cudaError_t e = (cudaError_t)launch_spec_verify(p.g, const_cast<SpecPage*>(p.sp), p.pts, p.n, p.base,
-                                                        stream, launches);
-        if (e != cudaSuccess) return e;
-    }
-    cudaError_t e = (cudaError_t)launch_filter(p, vec16, stream, launches);
-    if (e != cudaSuccess || !p.sp) return e;
-    return (cudaError_t)launch_filter_spec(p, stream, launches);
 }
 
 }  // namespace
@@ -307,9 +268,6 @@ cudapre_status cudapre_extremes(const cudapre_pt* d_pts, int64_t n_local, int64_
     p.ws = ws_header(d_ws);
     p.partials = ws_partials(d_ws);
     p.d_out = d_out;
-    p.sp = ws_spec(d_ws);
-    p.spec = spec_possible(d_pts, n_local, nang) ? 1 : 0;
-    if (p.spec) p.records = ws_records(d_ws, ws_bytes, n_local, &p.rcount);
     if (n_local >= 65536) {
         int64_t ch = n_local / 16384;
         p.seed_chunks = (unsigned)(ch < 16 ? 16 : (ch > 4096 ? 4096 : ch));
@@ -422,7 +380,7 @@ cudapre_status cudapre_filter(const cudapre_pt* d_pts, int64_t n_local, int64_t 
         CUDA_TRY(cudaEventRecord(ev[2], strm));
     }
     int launches = 0;
-    CUDA_TRY(launch_step3(p, vec16, stream, &launches));
+    CUDA_TRY(launch_filter(p, vec16, stream, &launches));
     if (h_rep) CUDA_TRY(cudaEventRecord(ev[3], strm));
     CUDA_TRY(cudaMemcpyAsync(stage, &p.ws->count, 16, cudaMemcpyDeviceToHost, strm));   // count + stats
     CUDA_TRY(cudaStreamSynchronize(strm));
@@ -537,7 +495,7 @@ cudapre_status cudapre_filter_geom(const cudapre_pt* d_pts, int64_t n_local, int
     k2_params(p, d_pts, n_local, index_base, d_surv_idx, d_surv_pts, capacity, d_ws, ws_bytes);
     const int vec16 = (((uintptr_t)d_pts & 15u) == 0);
     int launches = 0;
-    CUDA_TRY(launch_step3(p, vec16, stream, &launches));
+    CUDA_TRY(launch_filter(p, vec16, stream, &launches));
     if (d_count)
         CUDA_TRY(cudaMemcpyAsync(d_count, &p.ws->count, sizeof(int64_t), cudaMemcpyDeviceToDevice, strm));
     return CUDAPRE_OK;
@@ -622,33 +580,6 @@ cudapre_status cudapre_graph_launch(cudapre_graph_t* g, void* stream) {
     g_err.clear();
     if (!g || !g->exec) return fail(CUDAPRE_ERR_INVALID_ARGUMENT, "graph is NULL");
     CUDA_TRY(cudaGraphLaunch(g->exec, (cudaStream_t)stream));
-    return CUDAPRE_OK;
-}
-
-// ------------------------------------------------------------------ speculative pre-filter state
-static_assert(CUDAPRE_SPEC_MIN_N == kSpecMinN, "include/cudapre.h CUDAPRE_SPEC_MIN_N");
-
-cudapre_status cudapre_spec_info(const void* d_ws, size_t ws_bytes, void* stream, cudapre_spec_info_t* h_out) {
-    g_err.clear();
-    if (!d_ws || !h_out || ws_bytes < kWsFixedBytes)
-        return fail(CUDAPRE_ERR_INVALID_ARGUMENT, "need a workspace and an output");
-    SpecPage sp;
-    cudaStream_t strm = (cudaStream_t)stream;
-    CUDA_TRY(cudaMemcpyAsync(&sp, reinterpret_cast<const char*>(d_ws) + kWsSpecOff, sizeof(SpecPage),
-                             cudaMemcpyDeviceToHost, strm));
-    CUDA_TRY(cudaStreamSynchronize(strm));
-    std::memset(h_out, 0, sizeof(*h_out));
-    h_out->enabled = sp.enabled;
-    h_out->used = sp.on;
-    h_out->seed_vertices = (int32_t)sp.nv_seed;
-    h_out->candidates = (int64_t)sp.candidates;
-    h_out->records = (int64_t)(8 * sp.rec_chunks);
-    h_out->overflow_records = sp.overflow;
-    h_out->centre[0] = sp.cx;
-    h_out->centre[1] = sp.cy;
-    h_out->r2min = sp.r2min;
-    h_out->region_box = sp.use_box;
-    for (int j = 0; j < 4; ++j) h_out->box[j] = sp.box[j];
     return CUDAPRE_OK;
 }
 

@@ -26,9 +26,8 @@ constexpr int kMaxK1Blocks = 148 * 16;
 
 // ---------------------------------------------------------------- workspace
 // Device workspace layout (caller-owned, zero-filled once):
-//   [WsHeader, padded to 4 KiB][geometry page 32 KiB][spec page 8 KiB][K1Partial x kMaxK1Blocks x 32]
-//   [tile status x ntiles] ... [candidate records + counts][TMA K2 list-overflow scratch]
-// (the last two at the END of the buffer, see ws_records / ws_scratch)
+//   [WsHeader, padded to 4 KiB][geometry page 32 KiB][K1Partial x kMaxK1Blocks x 32][tile status x ntiles]
+//   ... [TMA K2 list-overflow scratch, at the END of the buffer]
 // Every kernel leaves the counters it uses back at their reset values, so the
 // workspace stays valid from call to call.
 struct alignas(16) WsHeader {
@@ -44,13 +43,12 @@ struct alignas(16) WsHeader {
     unsigned int lb_spins;       // K2 look-back rounds that waited
     unsigned int seed[CUDAPRE_MAX_SLOTS];   // seed thresholds, order-preserving encoding, 0 = none
     cudapre_extremes_t result;   // K1 final result
-    // seed picks for the pre-filter region: per slot the sample
-    // point with the best float key, (order-preserving key << 32) | local index, 0 = none
-    unsigned long long seed_pick[CUDAPRE_MAX_SLOTS];
-    unsigned int seed_ticket;    // seed blocks finished (the last one builds the region)
-    unsigned int pad1[3];
 };
 static_assert(sizeof(WsHeader) <= 2048, "header too large");
+// perf experiments only (CUDAPRE_K2_DEBUG=2): per-warp cycle counters of the
+// TMA K2 at this offset of the workspace header page (see scripts/k2_timing.py)
+constexpr size_t kWsDbgOffset = 2048;
+constexpr int kWsDbgWords = 48;
 
 struct K1Partial {
     double key;
@@ -63,46 +61,7 @@ constexpr size_t kWsHeaderBytes = 4096;
 // polygon (cudapre_polygon_t) at +kWsPolyOff
 constexpr size_t kWsGeomBytes = 32768;
 constexpr size_t kWsPolyOff = 16384;
-// ---------------------------------------------------------------- speculative pre-filter
-// K1 sets aside, per (2048-point chunk c, warp w) "record", the points of its
-// 256 that are not certainly inside the region D (spec.cuh): up to kRecSlots
-// entries; more => the record's count byte says kRecOverflow and Step 3
-// re-reads those 256 points.  Record (c, w) covers the points 2048 c + 512 u +
-// 64 w + [0, 64), u = 0..3 (K1's TMA-ring ownership); an entry's meta byte is
-// (u << 6) | offset.
-constexpr int kRecSlots = 56;            // candidate entries per record
-constexpr int kRecMetaBytes = 64;        // [0, 64): meta bytes
-constexpr int kRecBytes = 512;           // [64, 512): float2 entries
-constexpr int kRecChunkPts = 2048;       // points per chunk (= K1's TMA stage of 1024 pairs)
-constexpr unsigned kRecOverflow = 0xffu;
-constexpr long long kSpecMinN = 1ll << 22;   // K1 writes records for n_local >= this (16-B aligned, <= 4 angles)
-static_assert(kRecMetaBytes + 8 * kRecSlots <= kRecBytes && kRecSlots <= kRecMetaBytes, "record layout");
-struct SpecPage {
-    int enabled;                  // seed: the region below is usable (K1 writes records)
-    int on;                       // Step-2 verification: 1 = Step 3 classifies the records only
-    unsigned int overflow;        // K1: records whose candidates overflowed kRecSlots
-    unsigned int nv_seed;         // seed ring size (diagnostic)
-    float cx, cy, r2min;          // D = the disk d2 < r2min around (cx, cy) ...
-    int use_box;                  // ... or (use_box) the closed box [box0, box1] x [box2, box3]
-    float box[4];
-    // token: what the records describe; K1's finalize writes it (tok_n = 0: none),
-    // the verification consumes it (so records are used at most once)
-    const float* tok_pts;
-    unsigned long long tok_n;
-    long long tok_base;
-    unsigned long long rec_chunks;   // chunks that have records (K1's full TMA chunks)
-    unsigned long long candidates;   // K1: entries written (diagnostic)
-};
-constexpr size_t kWsSpecBytes = 8192;
-static_assert(sizeof(SpecPage) <= kWsSpecBytes, "spec page");
-inline size_t ws_rec_chunks(int64_t n) { return (size_t)(n / kRecChunkPts); }
-inline size_t ws_records_bytes(int64_t n) {   // records + one count byte per record (rounded)
-    const size_t nr = 8 * ws_rec_chunks(n);
-    return nr * kRecBytes + ((nr + 255) & ~(size_t)255);
-}
-
-constexpr size_t kWsSpecOff = kWsHeaderBytes + kWsGeomBytes;
-constexpr size_t kWsFixedBytes = kWsHeaderBytes + kWsGeomBytes + kWsSpecBytes;   // header + geometry + spec
+constexpr size_t kWsFixedBytes = kWsHeaderBytes + kWsGeomBytes;   // header + geometry page
 constexpr size_t kWsPartialBytes = sizeof(K1Partial) * kMaxK1Blocks * CUDAPRE_MAX_SLOTS;
 
 // One tile-status word per super-tile, each on its own 128-byte line: packed
@@ -131,9 +90,8 @@ inline size_t ws_scratch_blocks(int64_t n) {
     const size_t t = ws_tiles(n);
     return t < cap ? t : cap;
 }
-inline size_t ws_bytes_for(int64_t n) {   // (+16 +256: alignment slack of the regions at the end)
-    return kWsFixedBytes + kWsPartialBytes + ws_status_bytes(n) + ws_records_bytes(n) +
-           kK2ScratchPerBlock * ws_scratch_blocks(n) + 16 + 256;
+inline size_t ws_bytes_for(int64_t n) {   // (+16: alignment slack of the scratch at the end)
+    return kWsFixedBytes + kWsPartialBytes + ws_status_bytes(n) + kK2ScratchPerBlock * ws_scratch_blocks(n) + 16;
 }
 
 // ---------------------------------------------------------------- kernel params
@@ -148,10 +106,7 @@ struct K1Params {
     K1Partial* partials;
     cudapre_extremes_t* d_out;   // nullable extra copy of the result
     unsigned int seed_chunks;    // number of 256-point sample chunks (0 = no seed)
-    int spec;                    // 1: build the pre-filter region and write candidate records
-    SpecPage* sp;                // workspace spec page
-    unsigned char* records;      // kRecBytes per record, record = chunk * 8 + warp
-    unsigned char* rcount;       // one count byte per record (kRecOverflow = overflow)
+    int pad_;
 };
 
 // Step-3 geometry (built from the polygon on the host or on the device,
@@ -190,12 +145,6 @@ struct K2Params {
     const K2Geom* g;          // device geometry (workspace)
     SurvEntry* scratch;       // TMA K2 list overflow, kK2ScratchPerBlock per block
     unsigned int scratch_blocks;   // blocks the scratch region covers (caps the TMA K2 grid)
-    // speculative pre-filter: null sp = not possible for this call
-    // (the streaming K2 always runs); otherwise sp->on (set by the verification)
-    // selects the record kernel and the streaming K2 exits at once
-    const SpecPage* sp;
-    const unsigned char* records;
-    const unsigned char* rcount;
 };
 
 // ---------------------------------------------------------------- launchers (.cu)
@@ -203,12 +152,6 @@ struct K2Params {
 int launch_extremes(const K1Params& p, int vec16, void* stream, int* launches);
 int launch_filter(const K2Params& p, int vec16, void* stream, int* launches);
 int launch_filter_tma(const K2Params& p, void* stream, int* launches);     // 16-B aligned input
-// speculative pre-filter (k2_spec.cu): the verification of the region against
-// the Step-2 ring (one block; sets sp->on, consumes the token) and Step 3 over
-// the candidate records (exits at once unless sp->on)
-int launch_spec_verify(const K2Geom* g, SpecPage* sp, const float* pts, unsigned long long n, long long base,
-                       void* stream, int* launches);
-int launch_filter_spec(const K2Params& p, void* stream, int* launches);
 
 // ---------------------------------------------------------------- final hull on the GPU (k_hull.cu, f1)
 constexpr int kHullBuckets = 4097;   // b = round(1024 pa), pa in [0, 4]

@@ -45,7 +45,6 @@
 #include <cstdint>
 
 #include "internal.h"
-#include "spec.cuh"
 #include "tma.cuh"
 
 namespace cudapre {
@@ -222,15 +221,11 @@ __device__ __forceinline__ void refresh_thresholds(float (&T)[4 * NANG], const W
 // relative terms).  The kernel tests d2 = RN(RN(dx^2)+RN(dy^2)) < rho2 with
 // (dx, dy) = RN(p - c); d2 >= |p-c|^2 (1 - 4u) and rho2 <= rho^2 (1 - 2^-16).
 // rho2 = -1 disables the pre-screen (no seed yet, or no positive slack).
-// fixc: keep the caller's centre (the pre-filter region's, DESIGN.md §6.6:
-// the argument holds for any centre) instead of the thresholds' midpoint.
 template <int NANG>
 __device__ __forceinline__ void prescreen_params(const float (&T)[4 * NANG], const K1Params& p,
-                                                 float& cx, float& cy, float& rho2, bool fixc = false) {
-    if (!fixc) {
-        cx = __fmul_rn(__fadd_rn(T[0], T[1]), 0.5f);
-        cy = __fmul_rn(__fadd_rn(T[2], T[3]), 0.5f);
-    }
+                                                 float& cx, float& cy, float& rho2) {
+    cx = __fmul_rn(__fadd_rn(T[0], T[1]), 0.5f);
+    cy = __fmul_rn(__fadd_rn(T[2], T[3]), 0.5f);
     rho2 = -1.0f;
     if (!isfinite(cx) || !isfinite(cy)) return;
     double smin = INFINITY;
@@ -255,26 +250,12 @@ __device__ __forceinline__ void prescreen_params(const float (&T)[4 * NANG], con
 // Float-only bounds over sample chunks spread evenly over the input:
 //   max slot: a float <= the exact key of some sampled point  (RD(Xf - m))
 //   min slot: a float >= the exact key of some sampled point  (RU(Xf + m))
-// SPEC: also the sample point with the best float key per slot (the "seed
-// picks"); the last block to finish builds the pre-filter region from them
-// (build_region).
-template <int NANG>
-__device__ void build_region(const K1Params& p);
-
-template <int NANG, bool VEC, bool SPEC>
+template <int NANG, bool VEC>
 __global__ void __launch_bounds__(kSeedThreads) k1_seed(const K1Params p) {
     constexpr int NS = 4 * NANG;
     float L[NS];
-    float BK[SPEC ? NS : 1];      // best float key per slot (SPEC)
-    unsigned BI[SPEC ? NS : 1];   // its local index
 #pragma unroll
-    for (int s = 0; s < NS; ++s) {
-        L[s] = is_max_slot(s) ? -INFINITY : INFINITY;
-        if (SPEC) {
-            BK[s] = L[s];
-            BI[s] = kNoIdx;
-        }
-    }
+    for (int s = 0; s < NS; ++s) L[s] = is_max_slot(s) ? -INFINITY : INFINITY;
     const unsigned npairs = p.n / 2u + (p.n & 1u);   // (n + 1) / 2 without wrapping at 2^32-1
     const unsigned chunk_pairs = kSeedThreads;
     const unsigned span = npairs > chunk_pairs ? npairs - chunk_pairs : 0u;
@@ -291,17 +272,10 @@ __global__ void __launch_bounds__(kSeedThreads) k1_seed(const K1Params p) {
         for (int h = 0; h < 2; ++h) {
             if (!ok[h]) continue;
             const float x = px[h], y = py[h];
-            const unsigned i = 2u * q + (unsigned)h;
             L[0] = fminf(L[0], x);
             L[1] = fmaxf(L[1], x);
             L[2] = fminf(L[2], y);
             L[3] = fmaxf(L[3], y);
-            if (SPEC) {
-                const float kv[4] = {x, x, y, y};
-#pragma unroll
-                for (int r = 0; r < 4; ++r)
-                    if ((r & 1) ? kv[r] > BK[r] : kv[r] < BK[r]) BK[r] = kv[r], BI[r] = i;
-            }
             const float m = __fmaf_rn(__fadd_rn(fabsf(x), fabsf(y)), 0x1p-20f, 0x1p-120f);
 #pragma unroll
             for (int k = 1; k < NANG; ++k) {
@@ -311,19 +285,10 @@ __global__ void __launch_bounds__(kSeedThreads) k1_seed(const K1Params p) {
                 L[4 * k + 1] = fmaxf(L[4 * k + 1], __fsub_rd(X, m));
                 L[4 * k + 2] = fminf(L[4 * k + 2], __fadd_ru(Y, m));
                 L[4 * k + 3] = fmaxf(L[4 * k + 3], __fsub_rd(Y, m));
-                if (SPEC) {
-                    const float kv[4] = {X, X, Y, Y};
-#pragma unroll
-                    for (int r = 0; r < 4; ++r) {
-                        const int s = 4 * k + r;
-                        if ((r & 1) ? kv[r] > BK[s] : kv[r] < BK[s]) BK[s] = kv[r], BI[s] = i;
-                    }
-                }
             }
         }
     }
     __shared__ float red[kSeedThreads / 32][NS];
-    __shared__ unsigned long long redp[kSeedThreads / 32][SPEC ? NS : 1];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
     for (int s = 0; s < NS; ++s) {
@@ -334,19 +299,6 @@ __global__ void __launch_bounds__(kSeedThreads) k1_seed(const K1Params p) {
             v = is_max_slot(s) ? fmaxf(v, w) : fminf(v, w);
         }
         if (lane == 0) red[warp][s] = v;
-        if (SPEC) {   // (order-preserving key << 32) | index; 0 = none
-            unsigned long long e = 0;
-            if (BI[s] != kNoIdx) {
-                const unsigned ek = is_max_slot(s) ? enc_f(BK[s]) : ~enc_f(BK[s]);
-                e = ((unsigned long long)ek << 32) | BI[s];
-            }
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                const unsigned long long w = __shfl_xor_sync(kFull, e, o);
-                e = w > e ? w : e;
-            }
-            if (lane == 0) redp[warp][s] = e;
-        }
     }
     __syncthreads();
     if (threadIdx.x < NS) {
@@ -359,127 +311,7 @@ __global__ void __launch_bounds__(kSeedThreads) k1_seed(const K1Params p) {
         } else {
             if (v < INFINITY) atomicMax(&p.ws->seed[s], ~enc_f(v));
         }
-        if (SPEC) {
-            unsigned long long e = redp[0][s];
-            for (int w = 1; w < kSeedThreads / 32; ++w) e = redp[w][s] > e ? redp[w][s] : e;
-            if (e) atomicMax(&p.ws->seed_pick[s], e);
-        }
     }
-    if (SPEC) {   // last block out builds the pre-filter region
-        __shared__ bool s_last;
-        __threadfence();
-        __syncthreads();
-        if (threadIdx.x == 0) s_last = atomicAdd(&p.ws->seed_ticket, 1u) == gridDim.x - 1;
-        __syncthreads();
-        if (s_last) {
-            __threadfence();
-            build_region<NANG>(p);
-        }
-    }
-}
-
-// The pre-filter region D (spec.cuh) from the seed picks:
-// their convex hull (plain binary64 monotone chain: D only has to be a good
-// guess, the Step-2 verification makes it safe), centre = vertex mean,
-// shrunk towards it by ~ the sample's angular resolution (spec::shrink), then
-// the largest disk around the centre and the largest centred axis-aligned box
-// inside the shrunk ring; D is the one covering more area.  Thread 0 of the
-// last seed block.
-template <int NANG>
-__device__ void build_region(const K1Params& p) {
-    constexpr int NS = 4 * NANG;
-    if (threadIdx.x != 0) return;
-    SpecPage* sp = p.sp;
-    double px[NS], py[NS];
-    int m = 0;
-    bool ok = true;
-    for (int s = 0; s < NS; ++s) {
-        const unsigned long long e = __ldcg(&p.ws->seed_pick[s]);
-        p.ws->seed_pick[s] = 0ull;   // (reset for the next call)
-        if (!e) {
-            ok = false;
-            continue;
-        }
-        const float2 q = __ldg(reinterpret_cast<const float2*>(p.pts) + (unsigned)(e & 0xffffffffu));
-        if (!isfinite(q.x) || !isfinite(q.y)) ok = false;
-        // insertion sort by (x, y), dropping duplicates
-        bool dup = false;
-        for (int t = 0; t < m; ++t) dup |= (px[t] == (double)q.x && py[t] == (double)q.y);
-        if (dup) continue;
-        int j = m;
-        while (j > 0 && (px[j - 1] > q.x || (px[j - 1] == q.x && py[j - 1] > q.y))) {
-            px[j] = px[j - 1];
-            py[j] = py[j - 1];
-            --j;
-        }
-        px[j] = q.x;
-        py[j] = q.y;
-        ++m;
-    }
-    // monotone chain (CCW), strict turns
-    double hx[2 * NS + 1], hy[2 * NS + 1];
-    int k = 0;
-    for (int i = 0; i < m && ok; ++i) {
-        while (k >= 2 && (hx[k - 1] - hx[k - 2]) * (py[i] - hy[k - 2]) - (hy[k - 1] - hy[k - 2]) * (px[i] - hx[k - 2]) <= 0.0)
-            --k;
-        hx[k] = px[i], hy[k] = py[i], ++k;
-    }
-    for (int i = m - 2, t = k + 1; i >= 0 && ok; --i) {
-        while (k >= t && (hx[k - 1] - hx[k - 2]) * (py[i] - hy[k - 2]) - (hy[k - 1] - hy[k - 2]) * (px[i] - hx[k - 2]) <= 0.0)
-            --k;
-        hx[k] = px[i], hy[k] = py[i], ++k;
-    }
-    const int nv = ok && m >= 3 ? k - 1 : 0;
-    sp->nv_seed = (unsigned)nv;
-    p.ws->seed_ticket = 0u;
-    float r2 = -1.0f, box[4] = {1.f, -1.f, 1.f, -1.f};
-    float fx = 0.f, fy = 0.f;
-    bool use_box = false;
-    if (nv >= 3) {
-        // centre: the midpoint of the ring's bounding box (the angle-0 picks) --
-        // also the K1 pre-screen centre, which wants it close to the data's
-        double lx = INFINITY, ly = INFINITY, ux = -INFINITY, uy = -INFINITY;
-        for (int j = 0; j < nv; ++j)
-            lx = fmin(lx, hx[j]), ux = fmax(ux, hx[j]), ly = fmin(ly, hy[j]), uy = fmax(uy, hy[j]);
-        fx = (float)(0.5 * (lx + ux)), fy = (float)(0.5 * (ly + uy));
-        lx = ly = INFINITY, ux = uy = -INFINITY;
-        const double eps = spec::shrink(fmin((double)p.seed_chunks * (2.0 * kSeedThreads), (double)p.n));
-        for (int j = 0; j < nv; ++j) {   // shrink towards the (float) centre
-            hx[j] = fx + (1.0 - eps) * (hx[j] - fx);
-            hy[j] = fy + (1.0 - eps) * (hy[j] - fy);
-            lx = fmin(lx, hx[j]), ux = fmax(ux, hx[j]), ly = fmin(ly, hy[j]), uy = fmax(uy, hy[j]);
-        }
-        if (isfinite(fx) && isfinite(fy) && spec::ring_contains(hx, hy, nv, fx, fy)) {
-            r2 = spec::ring_r2(hx, hy, nv, fx, fy);
-            // largest t in [0, 1]: the ring's bounding box scaled by t towards the
-            // centre, [fx - t (fx - lx), fx + t (ux - fx)] x [fy - t (fy - ly), fy + t (uy - fy)], inside
-            double lo = 0.0, hi = 1.0;
-            for (int it = 0; it < 24; ++it) {
-                const double t = 0.5 * (lo + hi);
-                const double x0 = fx - t * (fx - lx), x1 = fx + t * (ux - fx);
-                const double y0 = fy - t * (fy - ly), y1 = fy + t * (uy - fy);
-                const bool in = spec::ring_contains(hx, hy, nv, x0, y0) && spec::ring_contains(hx, hy, nv, x1, y0) &&
-                                spec::ring_contains(hx, hy, nv, x1, y1) && spec::ring_contains(hx, hy, nv, x0, y1);
-                (in ? lo : hi) = t;
-            }
-            if (lo > 0.0) {
-                box[0] = (float)(fx - lo * (fx - lx)), box[1] = (float)(fx + lo * (ux - fx));
-                box[2] = (float)(fy - lo * (fy - ly)), box[3] = (float)(fy + lo * (uy - fy));
-                const double barea = (double)(box[1] - box[0]) * (double)(box[3] - box[2]);
-                use_box = box[0] < box[1] && box[2] < box[3] && barea > 3.14159 * fmax((double)r2, 0.0);
-            }
-        }
-    }
-    const bool on = use_box || r2 > 0.0f;
-    sp->cx = fx;
-    sp->cy = fy;
-    sp->r2min = r2;
-    sp->use_box = use_box ? 1 : 0;
-    for (int j = 0; j < 4; ++j) sp->box[j] = box[j];
-    sp->overflow = 0u;
-    sp->candidates = 0ull;
-    sp->on = 0;
-    sp->enabled = on ? 1 : 0;
 }
 
 // ---------------------------------------------------------------- main kernel
@@ -491,8 +323,6 @@ __global__ void __launch_bounds__(kK1Threads + (TMA ? 32 : 0), 2) k1_extremes(co
     __shared__ WarpState<NANG> sst[kWarps];
     __shared__ float sqx[kWarps][kK1Queue], sqy[kWarps][kK1Queue];
     __shared__ unsigned sqi[kWarps][kK1Queue];
-    // spec: per warp, two record images being built / stored by a bulk copy
-    __shared__ __align__(16) unsigned char srec[TMA ? kWarps : 1][1][TMA ? kRecBytes : 16];
     __shared__ bool s_last;
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     WarpState<NANG>& st = sst[warp < (unsigned)kWarps ? warp : 0u];   // (TMA producer warp: unused)
@@ -512,25 +342,9 @@ __global__ void __launch_bounds__(kK1Threads + (TMA ? 32 : 0), 2) k1_extremes(co
         st.idx[lane] = kNoIdx;
     }
     __syncwarp();
-    // Spec mode (TMA ring only): the pre-filter region D
-    // (the disk d2 < r2min around its centre, or its box, whichever the seed
-    // found larger) shares its centre with the pre-screen, so one d2 serves
-    // both tests.  Each lane writes its points outside D straight into the
-    // chunk's record at the slots a warp scan of their counts gives.
-    const bool spec = TMA && p.spec && p.sp->enabled;
-    float scx = 0.f, scy = 0.f, sr2min = -1.f, sbx0 = 1.f, sbx1 = -1.f, sby0 = 1.f, sby1 = -1.f;
-    int sbox = 0;
-    if (spec) {
-        scx = p.sp->cx;
-        scy = p.sp->cy;
-        sr2min = p.sp->r2min;
-        sbox = p.sp->use_box;
-        sbx0 = p.sp->box[0], sbx1 = p.sp->box[1], sby0 = p.sp->box[2], sby1 = p.sp->box[3];
-    }
-    float pcx = scx, pcy = scy, prho2;
-    prescreen_params<NANG>(T, p, pcx, pcy, prho2, spec);
+    float pcx, pcy, prho2;
+    prescreen_params<NANG>(T, p, pcx, pcy, prho2);
     unsigned qcount = 0;   // this warp's queued points (uniform)
-    unsigned ncand = 0;    // spec: candidates written (diagnostic)
 
     const unsigned npairs = p.n / 2u + (p.n & 1u);   // (n + 1) / 2 without wrapping at 2^32-1
     const unsigned stride = gridDim.x * kK1Threads * kK1Unroll;
@@ -580,7 +394,7 @@ __global__ void __launch_bounds__(kK1Threads + (TMA ? 32 : 0), 2) k1_extremes(co
                 }
                 if (lane == 0) atomicAdd(&p.ws->k1_exact, hits);
                 refresh_thresholds<NANG>(T, st);
-                prescreen_params<NANG>(T, p, pcx, pcy, prho2, spec);
+                prescreen_params<NANG>(T, p, pcx, pcy, prho2);
             }
         }
         const unsigned rem = qcount - nb;   // < 32: move to the front
@@ -601,65 +415,15 @@ __global__ void __launch_bounds__(kK1Threads + (TMA ? 32 : 0), 2) k1_extremes(co
         qcount = rem;
     };
     // Pre-screen 4 pairs against the warp's disk; queue the rest.
-    auto process = [&](const float4 (&v)[kK1Unroll], unsigned qb, const float2* stage2) {
+    auto process = [&](const float4 (&v)[kK1Unroll], unsigned qb) {
         unsigned needy = 0u;   // bit b = 2u + h
-        unsigned keep = 0u;    // spec: bit b = outside the pre-filter region (NaN: outside)
         const float2 nc = make_float2(-pcx, -pcy);
 #pragma unroll
         for (int u = 0; u < kK1Unroll; ++u) {
-            const float2 e0 = __fadd2_rn(make_float2(v[u].x, v[u].y), nc);
-            const float2 e1 = __fadd2_rn(make_float2(v[u].z, v[u].w), nc);
-            const float2 d0 = __fmul2_rn(e0, e0), d1 = __fmul2_rn(e1, e1);
-            const float q0 = __fadd_rn(d0.x, d0.y), q1 = __fadd_rn(d1.x, d1.y);
-            needy |= ((q0 < prho2) ? 0u : 1u) << (2 * u);
-            needy |= ((q1 < prho2) ? 0u : 2u) << (2 * u);
-            if (spec) {
-                const bool in0 = sbox ? (v[u].x >= sbx0) & (v[u].x <= sbx1) & (v[u].y >= sby0) & (v[u].y <= sby1)
-                                      : q0 < sr2min;
-                const bool in1 = sbox ? (v[u].z >= sbx0) & (v[u].z <= sbx1) & (v[u].w >= sby0) & (v[u].w <= sby1)
-                                      : q1 < sr2min;
-                keep |= (in0 ? 0u : 1u) << (2 * u);
-                keep |= (in1 ? 0u : 2u) << (2 * u);
-            }
-        }
-        if (spec) {
-            // the chunk's record (this warp's 256 points): slots by a warp scan of
-            // the lanes' counts; each lane copies its points from the ring stage
-            // into the warp's record image in shared memory (a loop over its
-            // points outside D only), one bulk copy stores the image
-            const unsigned nk = __popc(keep);
-            unsigned kinc = nk;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const unsigned t = __shfl_up_sync(kFull, kinc, o);
-                if (lane >= (unsigned)o) kinc += t;
-            }
-            const unsigned ktotal = __shfl_sync(kFull, kinc, 31);
-            const unsigned chunk = qb >> 10;
-            unsigned char* img = srec[warp][0];
-            if (ktotal) {
-                unsigned slot = kinc - nk;
-                for (unsigned kb = keep; kb; kb &= kb - 1, ++slot) {
-                    const unsigned b = __ffs(kb) - 1;
-                    if (slot < (unsigned)kRecSlots) {
-                        img[slot] = (unsigned char)(((b >> 1) << 6) | (lane << 1) | (b & 1));   // (u << 6) | offset
-                        reinterpret_cast<float2*>(img + kRecMetaBytes)[slot] =
-                            stage2[2u * ((b >> 1) * kK1Threads + threadIdx.x) + (b & 1)];
-                    }
-                }
-                __syncwarp();
-                // the image's used bytes, 16 per lane, coalesced
-                const unsigned m = ktotal > (unsigned)kRecSlots ? 0u : ktotal;
-                const unsigned nq = (kRecMetaBytes + 8u * m + 15u) / 16u;
-                uint4* dst = reinterpret_cast<uint4*>(p.records + ((size_t)chunk * kWarps + warp) * kRecBytes);
-                for (unsigned q = lane; q < nq; q += 32) dst[q] = reinterpret_cast<const uint4*>(img)[q];
-                __syncwarp();
-            }
-            if (lane == 0) {
-                p.rcount[(size_t)chunk * kWarps + warp] = (unsigned char)(ktotal > (unsigned)kRecSlots ? kRecOverflow : ktotal);
-                if (ktotal > (unsigned)kRecSlots) atomicAdd(&p.sp->overflow, 1u);
-            }
-            ncand += ktotal;
+            const float2 d0 = __fmul2_rn(__fadd2_rn(make_float2(v[u].x, v[u].y), nc), __fadd2_rn(make_float2(v[u].x, v[u].y), nc));
+            const float2 d1 = __fmul2_rn(__fadd2_rn(make_float2(v[u].z, v[u].w), nc), __fadd2_rn(make_float2(v[u].z, v[u].w), nc));
+            needy |= ((__fadd_rn(d0.x, d0.y) < prho2) ? 0u : 1u) << (2 * u);
+            needy |= ((__fadd_rn(d1.x, d1.y) < prho2) ? 0u : 2u) << (2 * u);
         }
         const unsigned nq = __popc(needy);
         unsigned incl = nq;
@@ -728,19 +492,11 @@ __global__ void __launch_bounds__(kK1Threads + (TMA ? 32 : 0), 2) k1_extremes(co
 #pragma unroll
                 for (int u = 0; u < kK1Unroll; ++u) v[u] = ring[sidx * kK1StagePairs + u * kK1Threads + threadIdx.x];
                 __syncwarp();
-                // data now in registers (spec: the record copies read the stage: release after)
-                if (!spec && lane == 0) mbar_arrive_a(a_empty + 8u * sidx);
-                const unsigned chunk = blockIdx.x + i * gridDim.x;
-                process(v, chunk * kK1StagePairs + threadIdx.x,
-                        reinterpret_cast<const float2*>(&ring[sidx * kK1StagePairs]));
-                if (spec) {
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive_a(a_empty + 8u * sidx);
-                }
+                if (lane == 0) mbar_arrive_a(a_empty + 8u * sidx);   // data now in registers
+                process(v, (blockIdx.x + i * gridDim.x) * kK1StagePairs + threadIdx.x);
             }
         }
         q0 = nchunks * kK1StagePairs + blockIdx.x * (kK1Threads * kK1Unroll) + threadIdx.x;
-        if (spec && lane == 0 && ncand) atomicAdd(&p.sp->candidates, (unsigned long long)ncand);
     } else if (full(q0)) {
         // registers: the next iteration's 4 x 128-bit loads are issued before
         // this one is screened
@@ -751,7 +507,7 @@ __global__ void __launch_bounds__(kK1Threads + (TMA ? 32 : 0), 2) k1_extremes(co
             const bool more = full(qn);
             float4 vn[kK1Unroll];
             if (more) load_full(vn, qn);
-            process(v, q0, nullptr);
+            process(v, q0);
             q0 = qn;
             if (!more) break;
 #pragma unroll
@@ -872,14 +628,6 @@ __global__ void __launch_bounds__(kK1Threads + (TMA ? 32 : 0), 2) k1_extremes(co
                 outs[o]->key[threadIdx.x] = 0.0;
                 outs[o]->pt[threadIdx.x] = cudapre_pt{0.f, 0.f};
             }
-            if (threadIdx.x == 0 && o == 0 && p.sp) {   // what the records describe (token; none if tok_n = 0)
-                SpecPage* sp = p.sp;
-                const bool on = TMA && p.spec && sp->enabled;
-                sp->tok_pts = p.pts;
-                sp->tok_base = p.base;
-                sp->rec_chunks = (p.n / 2u) / (unsigned)kK1StagePairs;
-                sp->tok_n = on ? (unsigned long long)p.n : 0ull;
-            }
             if (threadIdx.x == 0) {
                 outs[o]->nang = p.nang;
                 outs[o]->nonfinite = nf ? 1 : 0;
@@ -920,16 +668,7 @@ cudaError_t launch_t(const K1Params& p, cudaStream_t s, int* launches) {
     if (blocks < 1) blocks = 1;
     if (p.seed_chunks) {
         const unsigned sb = p.seed_chunks < (unsigned)seed_blocks ? p.seed_chunks : (unsigned)seed_blocks;
-        // spec (16-B aligned TMA path, <= 4 angles): the seed also builds the
-        // pre-filter region
-        bool spec_seed = false;
-        if constexpr (TMA && NANG <= 4) {
-            if (p.spec) {
-                k1_seed<NANG, VEC, true><<<sb, kSeedThreads, 0, s>>>(p);
-                spec_seed = true;
-            }
-        }
-        if (!spec_seed) k1_seed<NANG, VEC, false><<<sb, kSeedThreads, 0, s>>>(p);
+        k1_seed<NANG, VEC><<<sb, kSeedThreads, 0, s>>>(p);
         ++*launches;
     }
     k1_extremes<NANG, VEC, TMA><<<blocks, kK1Threads + (TMA ? 32 : 0), smem, s>>>(p);

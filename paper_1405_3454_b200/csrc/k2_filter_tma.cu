@@ -186,7 +186,6 @@ __device__ __forceinline__ void emit_t(const K2Params& p, const TileT& ts, const
 
 template <int EDGES>
 __global__ void __launch_bounds__(kBlock, 2) k2_filter_tma(const __grid_constant__ K2Params p) {
-    if (p.sp && p.sp->on) return;   // Step 3 runs over K1's candidate records (k2_spec.cu; uniform)
     extern __shared__ __align__(128) unsigned char smem_raw[];
     SmemT& S = *reinterpret_cast<SmemT*>(smem_raw);
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;

@@ -23,10 +23,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspa
 import oracle  # noqa: E402
 import paper_1405_3454_b200 as cp  # noqa: E402
 import synth  # noqa: E402
-import synth.cuda as scuda  # noqa: E402
 
 N = int(os.environ.get("NCCL_TEST_N", "3000017"))
-N_SPEC = int(os.environ.get("NCCL_TEST_N_SPEC", "24000017"))   # large enough for the pre-filter on every rank
 
 
 def shard(n, rank, world):
@@ -76,15 +74,6 @@ def main():
         e_pts = pts if rank < world - 1 else torch.empty((0, 2), dtype=torch.float32, device="cuda")
         ext_e = cp.extremes_comm(e_pts, comm, "A", index_base=e_base)
         assert ext_e.n == N - shard(N, world - 1, world)[0], "empty-shard extremes_comm"
-    # the speculative pre-filter on every shard (n_local >= CUDAPRE_SPEC_MIN_N): per-rank
-    # regions verified against the global polygon
-    ns_local, ns_base = shard(N_SPEC, rank, world)
-    sp_pts = scuda.generate("disk", ns_local, seed=8, base=ns_base)
-    s_idx, s_pts, s_cnt = cp.pipeline_comm(sp_pts, comm, "A", index_base=ns_base)
-    torch.cuda.synchronize()
-    s_m = int(s_cnt.item())
-    s_all, _, s_tot = cp.gather_survivors(comm, s_idx, None, s_m, root=0)
-    s_used = cp.spec_info()["used"]
     # 4. the 3D extension
     n3 = N // 3
     n3_local, base3 = shard(n3, rank, world)
@@ -106,16 +95,13 @@ def main():
         assert np.array_equal(g_idx.cpu().numpy(), want["survivors"]), "gathered survivors"
         assert np.array_equal(g_pts.cpu().numpy(), full[want["survivors"]]), "gathered points"
         assert ring_c.tolist() == oracle.hull(full).tolist(), "hull_comm"
-        full_s = synth.generate("disk", N_SPEC, seed=8)
-        want_s = oracle.cudapre(full_s, "A", threads=os.cpu_count())
-        assert np.array_equal(s_all.cpu().numpy(), want_s["survivors"]), "pre-filter path, sharded"
         full3 = synth.generate3("ball", n3, seed=7)
         want3 = oracle.cudapre3(full3, "A", threads=os.cpu_count())
         assert ext3.idx.tolist() == want3["ext_idx"].tolist(), "3D Step 1"
         assert poly3.facets.tolist() == want3["facets"].tolist(), "3D Step 2"
         assert np.array_equal(np.concatenate(parts3), want3["survivors"]), "3D Step 3"
         print(f"nccl ok world={world} survivors={len(got)} gathered={g_tot} hull={len(ring_c)} "
-              f"spec_used={s_used} 3d={len(want3['survivors'])}")
+              f"3d={len(want3['survivors'])}")
     comm.close()
     dist.barrier()
     dist.destroy_process_group()

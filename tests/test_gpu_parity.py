@@ -195,7 +195,7 @@ def test_config_full_size(name):
 
 def test_config_c5_full():
     """C5 at its full 2e9 points on one GPU, the bench workload and launch
-    configuration (device generator, 16-byte aligned, the pre-filter on):
+    configuration (device generator, 16-byte aligned):
     every point through the oracle, chunk by chunk (generator-verified bytes
     D2H): Step 1 merged over the chunks with the lexicographic rule,
     the oracle's ring, Step 3's keep mask -> the complete survivor index array
@@ -210,7 +210,6 @@ def test_config_c5_full():
     ext = cp.extremes(pts, "A", ws=ws)
     idx, sp, rep = cp.filter(pts, ext, ws=ws, out_idx=torch.empty(cap, dtype=torch.int64, device="cuda"),
                              out_pts=torch.empty((cap, 2), dtype=torch.float32, device="cuda"))
-    used = cp.spec_info(ws)["used"]
     surv = idx.cpu().numpy()
     # the device-resident pipeline (Step 2 on the device) into separate buffers
     d_idx, _, d_cnt = cp.pipeline(pts, "A", ws=ws, out_idx=torch.empty(cap, dtype=torch.int64, device="cuda"),
@@ -253,7 +252,7 @@ def test_config_c5_full():
     want_ring = surv[oracle.hull(sxy)]
     assert surv[cp.hull(sxy)].tolist() == want_ring.tolist()
     assert cp.hull_device(sp, idx, len(surv), rep["polygon"]).tolist() == want_ring.tolist()
-    print(f"C5: {len(surv)} survivors, hull {len(want_ring)} vertices, pre-filter used: {used}")
+    print(f"C5: {len(surv)} survivors, hull {len(want_ring)} vertices")
 
 
 @pytest.mark.parametrize("name", ["C4", "C4e0", "C2b"])
@@ -278,7 +277,7 @@ def test_config_hull_device_full_size(name):
 def test_nccl_paths_under_torchrun(nproc):
     """The multi-rank paths (torch group path, device-resident path, the
     in-library NCCL communicator: extremes, Steps 1-3, survivor gather,
-    sharded hull, the pre-filter per shard; 3D) under torchrun, one process
+    sharded hull; 3D) under torchrun, one process
     per GPU, against the oracle on the whole set (tests/scripts/nccl_cudapre.py)."""
     import socket
     import subprocess
