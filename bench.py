@@ -48,10 +48,6 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-points", action="store_true",
                     help="write only the survivors' indices (perf experiment; not the benchmark workload)")
-    ap.add_argument("--no-host-step2-check", action="store_true",
-                    help="skip the extra host-Step-2 timing loop reported as host_step2_value")
-    ap.add_argument("--host-step2", action="store_true",
-                    help="run Step 2 (and, N > 1, the merge) on the host between the kernels, as the paper")
     return ap.parse_args()
 
 
@@ -468,7 +464,7 @@ def main():
     from paper_1405_3454_b200 import build as pbuild
 
     torch.cuda.set_device(local)
-    group = None
+    group = comm = None
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         group = dist.group.WORLD
@@ -477,6 +473,7 @@ def main():
         scuda.build()
     if group is not None:
         dist.barrier()   # no rank loads a library rank 0 may be rebuilding
+        comm = cp.Comm.from_group(group)   # the library's own NCCL communicator
     n_local = n_total // world + (1 if rank < n_total % world else 0)
     base = rank * (n_total // world) + min(rank, n_total % world)
     pts = scuda.generate(family, n_local, seed=seed, base=base, **cfg)
@@ -484,35 +481,30 @@ def main():
     cap = n_local if n_local <= 250_000_000 else n_local // 8   # dense configs (C4) keep ~all points
     out_idx = torch.empty(cap, dtype=torch.int64, device="cuda")
     out_pts = None if args.no_points else torch.empty((cap, 2), dtype=torch.float32, device="cuda")
+    count = torch.zeros(1, dtype=torch.int64, device="cuda")
+    parts = torch.empty(world * cp.EXTREMES_BYTES, dtype=torch.uint8, device="cuda")
     torch.cuda.synchronize()
 
-    exact_pts = [0]
+    def max_over_ranks(v: float) -> float:
+        if group is None:
+            return v
+        t = torch.tensor([v], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
 
-    def step(rep1):   # host Step 2 (and, N > 1, the cross-rank combine)
-        ext = cp.extremes(pts, args.angles, index_base=base, group=group, ws=ws, report=rep1)
-        exact_pts[0] = ext.raw.exact_points
-        idx, sp, rep2 = cp.filter(pts, ext, index_base=base, ws=ws, out_idx=out_idx, out_pts=out_pts,
-                                  return_points=out_pts is not None)
-        return idx.shape[0], rep2
-
-    # Steps 1-3 stay on the device (Step 2 by the device builder, SURVEY §8
-    # f3; N > 1: NCCL all-gather of the ranks' Step-1 blocks straight from the
-    # workspace, merged by the builder), the host only enqueues; CUDA events
-    # between the calls time seed+K1, (all-gather +) Step 2 and K2 separately
-    # on the stream they run on.
-    device_path = not args.host_step2
-    count = torch.zeros(1, dtype=torch.int64, device="cuda")
-    gathered = torch.empty(world * cp.EXTREMES_BYTES, dtype=torch.uint8, device="cuda")
-
+    # (A) Steps 1-3 on the device (Step 2 by the device builder, SURVEY §8 f3;
+    # N > 1: the library's NCCL all-gather of the ranks' Step-1 blocks, merged
+    # by the builder): the host only enqueues; CUDA events between the calls
+    # time seed+K1, (all-gather +) Step 2 and K2 on their stream.
     def dstep(ev):
         if ev:
             ev[0].record()
         cp.extremes_device(pts, args.angles, index_base=base, ws=ws)
         if ev:
             ev[1].record()
-        if group is not None:
-            dist.all_gather_into_tensor(gathered, cp.result_view(ws), group=group)
-            cp.polygon_device(ws, parts=gathered, nparts=world)
+        if comm is not None:
+            cp.allgather_extremes(comm, ws, parts)
+            cp.polygon_device(ws, parts=parts, nparts=world)
         else:
             cp.polygon_device(ws)
         if ev:
@@ -521,72 +513,59 @@ def main():
         if ev:
             ev[3].record()
 
-    rep1 = cp.ReportT()
-    for _ in range(args.warmup):
-        dstep(None) if device_path else step(rep1)
-    k1_ms, k2_ms, poly_ms, launches = [], [], [], 0
-    lb_rounds = [0, 0]
-    surv = 0
-    clocks = ClockSampler(torch.cuda.current_device())
-    if group is not None:
-        dist.barrier()
-    torch.cuda.synchronize()
-    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
-    with clocks:
-        start.record()
-        for i in range(args.steps):
-            if device_path:
-                dstep(evs[i])
-            else:
-                surv, rep2 = step(rep1)
-                k1_ms.append(rep1.ms_extremes_kernels)
-                k2_ms.append(rep2["ms_filter_kernel"])
-                poly_ms.append(rep2["ms_polygon_host"])
-                lb_rounds[:] = [rep2["lookback_rounds"], rep2["lookback_spins"]]
-                launches += rep1.launches + rep2["launches"]
-        end.record()
-        torch.cuda.synchronize()
-    ms = start.elapsed_time(end)
-    if device_path:
-        k1_ms = [e[0].elapsed_time(e[1]) for e in evs]
-        poly_ms = [e[1].elapsed_time(e[2]) for e in evs]
-        k2_ms = [e[2].elapsed_time(e[3]) for e in evs]
-        surv = int(count.item())
-        # seed (n >= 65536) + K1 + polygon builder + K2 per step
-        launches = args.steps * ((2 if n_local >= 65536 else 1) + 2)
-        # per-step diagnostics (not timed): one host-path step with reports
-        _, rep2 = step(rep1)
-        lb_rounds[:] = [rep2["lookback_rounds"], rep2["lookback_spins"]]
-        assert rep2["survivors"] == surv, (rep2["survivors"], surv)
-    # the same K steps with the paper's host Step 2 between the kernels (D2H of
-    # the picks, host polygon, H2D of the geometry; N > 1: host merge), for
-    # comparison with the device-resident default (identical outputs)
-    host_ms = None
-    if device_path and not args.no_host_step2_check:
+    # (B) the paper's host Step 2 between the kernels: N = 1 one library
+    # call per step (K1 writes the picks to mapped host memory, the host builds
+    # the polygon, one H2D of the geometry, K2; one host wait); N > 1 the
+    # all-gather + host merge (cudapre_extremes_comm), then cudapre_filter.
+    hpoly = []
+
+    def hstep():
+        if comm is None:
+            hpoly.clear()
+            cp.pipeline_host(pts, args.angles, index_base=base, ws=ws, out_idx=out_idx, out_pts=out_pts,
+                             polygon_out=hpoly)
+        else:
+            ext = cp.extremes_comm(pts, comm, args.angles, index_base=base, ws=ws)
+            cp.filter(pts, ext, index_base=base, ws=ws, out_idx=out_idx, out_pts=out_pts,
+                      return_points=out_pts is not None)
+
+    def timed(fn, steps, evs=None):
         if group is not None:
             dist.barrier()
         torch.cuda.synchronize()
-        h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        h0.record()
-        for _ in range(args.steps):
-            step(rep1)
-        h1.record()
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record()
+        for i in range(steps):
+            fn(evs[i]) if evs is not None else fn()
+        t1.record()
         torch.cuda.synchronize()
-        host_ms = h0.elapsed_time(h1)
-        if group is not None:
-            t = torch.tensor([host_ms], device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            host_ms = float(t.item())
+        return max_over_ranks(t0.elapsed_time(t1))
+
+    for _ in range(args.warmup):
+        dstep(None)
+        hstep()
+    clocks = ClockSampler(torch.cuda.current_device())
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    with clocks:
+        ms = timed(dstep, args.steps, evs)
+        surv = int(count.item())
+        host_ms = timed(hstep, args.steps)
+    k1_ms = [e[0].elapsed_time(e[1]) for e in evs]
+    poly_ms = [e[1].elapsed_time(e[2]) for e in evs]
+    k2_ms = [e[2].elapsed_time(e[3]) for e in evs]
+    launches = args.steps * ((2 if n_local >= 65536 else 1) + 2)   # seed + K1 + Step-2 builder + K2
+    # per-step diagnostics (not timed): one reported host-path step
+    rep1 = cp.ReportT()
+    ext = cp.extremes(pts, args.angles, index_base=base, group=group, ws=ws, report=rep1)
+    _, _, rep2 = cp.filter(pts, ext, index_base=base, ws=ws, out_idx=out_idx, out_pts=out_pts,
+                           return_points=out_pts is not None)
+    assert rep2["survivors"] == surv, (rep2["survivors"], surv)
+    exact_pts = ext.raw.exact_points
+    surv_total = surv
     if group is not None:
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-        s = torch.tensor([surv], device="cuda", dtype=torch.int64)
-        dist.all_reduce(s)
-        surv_total = int(s.item())
-    else:
-        surv_total = surv
+        st = torch.tensor([surv], device="cuda", dtype=torch.int64)
+        dist.all_reduce(st)
+        surv_total = int(st.item())
     value = n_total * args.steps / (ms / 1e3) / 1e9
 
     # ------------------------------------------------------------ roofline of the dominant kernel
@@ -595,7 +574,7 @@ def main():
     k1 = statistics.mean(k1_ms)
     k2 = statistics.mean(k2_ms)
     k1_bytes = K1_BYTES_PER_PT * n_local
-    k2_bytes = K2_BYTES_PER_PT * n_local + K2_BYTES_PER_SURVIVOR * surv
+    k2_bytes = K2_BYTES_PER_PT * n_local + (K2_BYTES_PER_SURVIVOR if out_pts is not None else 8) * surv
     kernels = {"k1_extremes(+seed)": (k1, k1_bytes), "k2_filter": (k2, k2_bytes)}
     dom = max(kernels, key=lambda k: kernels[k][0])
     d_ms, d_bytes = kernels[dom]
@@ -608,12 +587,89 @@ def main():
             traffic = ent["dram_bytes_per_launch"]
     except (OSError, ValueError):
         pass
+    pipe_bytes = (k1_bytes + k2_bytes) * world
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic, "kernel": dom,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, measured)" if pk else "fallback",
                 "per_kernel_ms": {k: round(v[0], 4) for k, v in kernels.items()},
                 "per_kernel_GBps": {k: round(v[1] / (v[0] / 1e3) / 1e9, 1) for k, v in kernels.items()},
-                "pipeline_GBps": round((k1_bytes + k2_bytes) * args.steps / (ms / 1e3) / 1e9, 1)}
+                "pipeline_GBps": round(pipe_bytes * args.steps / (ms / 1e3) / 1e9 / world, 1),
+                "pipeline_frac_of_8TBps": round(pipe_bytes * args.steps / (ms / 1e3) / 1e12 / world / 8.0, 4)}
+    host_step2 = {
+        "value": round(n_total * args.steps / (host_ms / 1e3) / 1e9, 3), "unit": "Gpts/s",
+        "ms_per_step": round(host_ms / args.steps, 4),
+        "pipeline_frac_of_8TBps": round(pipe_bytes * args.steps / (host_ms / 1e3) / 1e12 / world / 8.0, 4),
+        "host_polygon_ms": round(hpoly[0][1], 4) if hpoly else round(rep2["ms_polygon_host"], 4),
+        "path": ("cudapre_pipeline_host: K1 -> picks in mapped host memory -> host chain + geometry -> "
+                 "one H2D -> K2 (one host wait per step)" if comm is None else
+                 "cudapre_extremes_comm (NCCL all-gather + host merge) -> cudapre_filter"),
+    }
+
+    # ------------------------------------------------------------ N > 1: collecting the survivors
+    multi = None
+    if comm is not None:
+        g_steps = max(1, min(args.steps, 5))
+        root_idx = torch.empty(max(1, int(surv_total * 1.01) + 1024) if rank == 0 else 1, dtype=torch.int64,
+                               device="cuda")
+        root_pts = torch.empty((root_idx.shape[0], 2), dtype=torch.float32, device="cuda") if rank == 0 else None
+
+        def gather_step():
+            _, _, c = cp.pipeline_comm(pts, comm, args.angles, index_base=base, ws=ws, out_idx=out_idx,
+                                       out_pts=out_pts, parts=parts)
+            cp.gather_survivors(comm, out_idx, out_pts, int(c.item()), root=0, out_idx=root_idx, out_pts=root_pts)
+
+        poly_raw = cp.PolygonT()
+
+        def hull_step():
+            _, _, c = cp.pipeline_comm(pts, comm, args.angles, index_base=base, ws=ws, out_idx=out_idx,
+                                       out_pts=out_pts, parts=parts)
+            m = int(c.item())
+            ctypes_memmove(poly_raw, ws.tensor[cp.WS_POLY_OFFSET:cp.WS_POLY_OFFSET + ctypes_sizeof(cp.PolygonT)])
+            return cp.hull_comm(comm, out_pts, out_idx, m, poly_raw, root=0)
+
+        gather_step()
+        ring = hull_step()
+        g_ms = timed(gather_step, g_steps)
+        h_ms = timed(hull_step, g_steps)
+        multi = {"filter_value": round(value, 3),
+                 "filter_gather_value": round(n_total * g_steps / (g_ms / 1e3) / 1e9, 3),
+                 "filter_gather_ms_per_step": round(g_ms / g_steps, 4),
+                 "gathered_bytes_per_step": 16 * surv_total,
+                 "filter_hull_value": round(n_total * g_steps / (h_ms / 1e3) / 1e9, 3),
+                 "filter_hull_ms_per_step": round(h_ms / g_steps, 4), "hull_vertices": int(len(ring)) if rank == 0 else None,
+                 "comm": "in-library NCCL (cudapre_comm_*): Step-1 all-gather; counts all-gather + grouped "
+                         "send/recv of the survivors to rank 0; per-rank GPU hulls + vertex gather"}
+        del root_idx, root_pts
+
+    # ------------------------------------------------------------ the paper's end to end: hull with / without CudaPre
+    hull_e2e = None
+    if comm is None and n_local <= 50_000_000 and not args.no_e2e:
+        t0 = time.perf_counter()
+        ring_all = cp.hull(pts.cpu().numpy())   # without CudaPre: D2H of every point + the host chain
+        t_without = time.perf_counter() - t0
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        idx_h, sp_h, rep_h = cp.filter(pts, cp.extremes(pts, args.angles, ws=ws), ws=ws, out_idx=out_idx,
+                                       out_pts=out_pts if out_pts is not None else torch.empty((cap, 2), device="cuda"))
+        ring_dev = cp.hull_device(sp_h, idx_h, idx_h.shape[0], rep_h["polygon"])   # with CudaPre, GPU final hull
+        t_with = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        idx_h, sp_h, rep_h = cp.filter(pts, cp.extremes(pts, args.angles, ws=ws), ws=ws, out_idx=out_idx,
+                                       out_pts=out_pts if out_pts is not None else torch.empty((cap, 2), device="cuda"))
+        m_h = idx_h.shape[0]
+        sidx = idx_h.cpu().numpy()
+        ring_host = sidx[cp.hull(sp_h.cpu().numpy())] if m_h else sidx
+        t_with_host = time.perf_counter() - t0
+        assert ring_dev.tolist() == ring_all.tolist() == ring_host.tolist(), "hull with / without CudaPre"
+        hull_e2e = {"without_cudapre_ms": round(1e3 * t_without, 3),
+                    "with_cudapre_gpu_hull_ms": round(1e3 * t_with, 3),
+                    "with_cudapre_host_hull_ms": round(1e3 * t_with_host, 3),
+                    "speedup_gpu_hull": round(t_without / t_with, 2),
+                    "speedup_host_hull": round(t_without / t_with_host, 2),
+                    "hull_vertices": int(len(ring_all)), "survivors": int(m_h),
+                    "note": ("wall clock: without = D2H of every point + cudapre_hull (host monotone chain); "
+                             "with = Steps 1-3 + the survivors' hull (cudapre_hull_device, or D2H + cudapre_hull); "
+                             "paper Tables 1-2 report 4-6x (GT640 + Qhull): context only")}
 
     # ------------------------------------------------------------ e2e: host buffers through the API
     e2e = None
@@ -641,24 +697,14 @@ def main():
         else:
             def e2e_step():
                 pts.copy_(h_pts, non_blocking=True)
-                ext = cp.extremes(pts, args.angles, index_base=base, group=group, ws=ws)
+                ext = cp.extremes_comm(pts, comm, args.angles, index_base=base, ws=ws)
                 idx, _, _ = cp.filter(pts, ext, index_base=base, ws=ws, out_idx=out_idx,
                                       return_points=False)
                 h_surv[: idx.shape[0]].copy_(idx)
                 return idx.shape[0]
             e2e_step()
-            dist.barrier()
-            torch.cuda.synchronize()
-            t0 = torch.cuda.Event(enable_timing=True)
-            t1 = torch.cuda.Event(enable_timing=True)
-            t0.record()
-            for _ in range(e_steps):
-                m = e2e_step()
-            t1.record()
-            torch.cuda.synchronize()
-            t = torch.tensor([t0.elapsed_time(t1)], device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e_ms = float(t.item())
+            e_ms = timed(e2e_step, e_steps)
+            m = surv
             d2h = 8 * m + world * cp.EXTREMES_BYTES + 8
         e2e = {"value": n_total * e_steps / (e_ms / 1e3) / 1e9, "unit": "Gpts/s",
                "h2d_bytes_per_step": 8 * n_local, "d2h_bytes_per_step": d2h, "steps": e_steps,
@@ -668,8 +714,6 @@ def main():
     # ------------------------------------------------------------ CPU baseline (oracle), rank 0, N=1
     cpu = None
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
-        import oracle
-
         cpu = cpu_baseline(pts, n_local, threads, args.angles, args.config)
 
     if rank == 0:
@@ -678,28 +722,40 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32+f64",
             "data": "synthetic",
-            "config": {"workload": f"{args.config}: {n_total} pts uniform {family} (seed {seed}), "
+            "config": {"workload": f"{args.config}: {n_total} pts {family} (seed {seed}), "
                                    f"contiguous shards of {n_local}", "n_total": n_total,
                        "angles": args.angles,
                        "l2": (f"inputs larger than L2 ({8 * n_local / 1e9:.2f} GB vs 126 MB), no flush"
                               if 8 * n_local > 126e6 else
                               f"inputs ({8 * n_local / 1e6:.0f} MB) fit in L2: warm-L2 numbers, not a roofline claim"),
-                       "parallelism": f"dp{world} (point shards; 912 B NCCL all-gather per step)",
-                       "step2": ("device (byte-identical to the host build, SURVEY f3; host_step2_value: the paper's host Step 2)"
-                                 if device_path else "host")},
+                       "parallelism": f"dp{world} (point shards; {cp.EXTREMES_BYTES} B NCCL all-gather per step)",
+                       "step2": "device (byte-identical to the host build, SURVEY f3); host_step2: the paper's host Step 2"},
             "discard_pct": round(100 * (1 - surv_total / n_total), 4),
             "remaining_pct": round(100 * surv_total / n_total, 4),
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roofline, "host_step2": host_step2, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": clocks.result(),
-            "k1_exact_path_points_per_step": int(exact_pts[0]),
-            ("host_step2_ms" if not device_path else "step2_device_ms"): round(statistics.median(poly_ms), 4),
-            "host_step2_value": (round(n_total * args.steps / (host_ms / 1e3) / 1e9, 3) if host_ms else None),
-            "k2_lookback_rounds_per_step": int(lb_rounds[0]), "k2_lookback_spins_per_step": int(lb_rounds[1]),
+            "k1_exact_path_points_per_step": int(exact_pts),
+            "step2_device_ms": round(statistics.median(poly_ms), 4),
+            "k2_lookback_rounds_per_step": int(rep2["lookback_rounds"]),
+            "k2_lookback_spins_per_step": int(rep2["lookback_spins"]),
         }
+        if multi is not None:
+            line["multi_gpu"] = multi
+        if hull_e2e is not None:
+            line["hull_e2e"] = hull_e2e
         print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.close()
     if group is not None:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def ctypes_memmove(dst_struct, src_u8_tensor):
+    import ctypes
+
+    buf = src_u8_tensor.cpu().numpy().tobytes()
+    ctypes.memmove(ctypes.addressof(dst_struct), buf, len(buf))
 
 
 if __name__ == "__main__":

@@ -310,6 +310,21 @@ cudapre_status cudapre_pipeline_device(const cudapre_pt* d_pts, int64_t n_local,
                                        int64_t* d_surv_idx, cudapre_pt* d_surv_pts, int64_t capacity,
                                        void* d_ws, size_t ws_bytes, void* stream, int64_t* d_count);
 
+/* Steps 1-3 with the paper's host Step 2 between the kernels, one
+ * call, one host wait per step: K1's last block writes the Step-1 result into
+ * a mapped pinned host block, the host waits for it, builds the polygon and
+ * the Step-3 geometry, enqueues one H2D copy of the geometry and K2, and
+ * returns; the survivor count stays on the device (*d_count, nullable).
+ *   h_poly         nullable host copy of the polygon
+ *   h_ms_polygon   nullable: host time of Step 2 (ms)
+ * Other arguments as cudapre_pipeline_device.  EMPTY_INPUT / NONFINITE_INPUT
+ * as cudapre_extremes (nothing enqueued after Step 1 then).               */
+cudapre_status cudapre_pipeline_host(const cudapre_pt* d_pts, int64_t n_local, int64_t index_base,
+                                     int32_t nang, const double* c, const double* s,
+                                     int64_t* d_surv_idx, cudapre_pt* d_surv_pts, int64_t capacity,
+                                     void* d_ws, size_t ws_bytes, void* stream, int64_t* d_count,
+                                     cudapre_polygon_t* h_poly, double* h_ms_polygon);
+
 /* One CUDA graph of cudapre_pipeline_device on fixed buffers: create runs
  * the pipeline once on `stream` (synchronised), then captures it; launch
  * replays it (one graph launch per step); destroy frees it.  The buffers

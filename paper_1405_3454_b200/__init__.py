@@ -104,7 +104,7 @@ SYMBOLS = ["cudapre_version", "cudapre_last_error", "cudapre_angles_preset",
            "cudapre_workspace_bytes", "cudapre_workspace_init", "cudapre_extremes",
            "cudapre_extremes_merge", "cudapre_polygon", "cudapre_filter", "cudapre_hull",
            "cudapre_run_host", "cudapre_geometry", "cudapre_filter_device", "cudapre_pipeline_device",
-           "cudapre_graph_create", "cudapre_graph_launch", "cudapre_graph_destroy",
+           "cudapre_graph_create", "cudapre_graph_launch", "cudapre_graph_destroy", "cudapre_pipeline_host",
            "cudapre_polygon_device", "cudapre_filter_geom", "cudapre_hull_device_bytes",
            "cudapre_hull_device", "cudapre_hull_device_ex",
            # multi-GPU (in-library NCCL communicator)
@@ -148,6 +148,8 @@ def lib():
     L.cudapre_geometry.argtypes = [P(ExtremesT), vp, sz, P(sz)]
     L.cudapre_filter_device.argtypes = [vp, i64, i64, vp, vp, vp, i64, vp, sz, vp, vp, vp]
     L.cudapre_pipeline_device.argtypes = [vp, i64, i64, i32, vp, vp, vp, vp, i64, vp, sz, vp, vp]
+    L.cudapre_pipeline_host.argtypes = [vp, i64, i64, i32, vp, vp, vp, vp, i64, vp, sz, vp, vp, P(PolygonT),
+                                         P(ctypes.c_double)]
     L.cudapre_graph_create.argtypes = [vp, i64, i64, i32, vp, vp, vp, vp, i64, vp, sz, vp, vp, P(vp)]
     L.cudapre_graph_launch.argtypes = [vp, vp]
     L.cudapre_graph_destroy.argtypes = [vp]
@@ -546,6 +548,33 @@ def pipeline(pts, angles_="A", index_base: int = 0, return_points: bool = True, 
     return out_idx, out_pts, count
 
 
+def pipeline_host(pts, angles_="A", index_base: int = 0, return_points: bool = True, ws=None, out_idx=None,
+                  out_pts=None, stream=None, polygon_out: list | None = None):
+    """Steps 1-3 with the paper's host Step 2 between the kernels in one
+    library call (cudapre_pipeline_host): one host wait per step, for the
+    Step-1 picks; returns (out_idx, out_pts, count) as pipeline().
+    ``polygon_out``: a list the Polygon and the host Step-2 ms are appended to."""
+    torch = _torch()
+    pts = _points(pts)
+    n = pts.shape[0]
+    nang, c, s = _angle_arrays(angles_)
+    w = _workspace(n, pts.device, ws)
+    out_idx, out_pts, cap = _outputs(pts, out_idx, out_pts, return_points)
+    count = torch.zeros(1, dtype=torch.int64, device=pts.device)
+    poly = PolygonT()
+    ms = ctypes.c_double()
+    _check(lib().cudapre_pipeline_host(
+        ctypes.c_void_p(pts.data_ptr()), n, index_base, nang,
+        c.ctypes.data_as(ctypes.c_void_p), s.ctypes.data_as(ctypes.c_void_p),
+        ctypes.c_void_p(out_idx.data_ptr()),
+        ctypes.c_void_p(out_pts.data_ptr()) if out_pts is not None else None, cap,
+        w.ptr, w.nbytes, _stream_ptr(stream), ctypes.c_void_p(count.data_ptr()), ctypes.byref(poly),
+        ctypes.byref(ms)))
+    if polygon_out is not None:
+        polygon_out.append((Polygon(poly), ms.value))
+    return out_idx, out_pts, count
+
+
 class Graph:
     """Steps 1-3 captured once in a CUDA graph on fixed buffers; launch()
     replays the whole step with one graph launch.  count is a device int64
@@ -649,6 +678,14 @@ class Comm:
             self.close()
         except Exception:
             pass
+
+
+def allgather_extremes(comm: Comm, ws, parts, stream=None):
+    """NCCL all-gather of every rank's Step-1 result block (the one
+    extremes_device left in ``ws``) into ``parts`` (device uint8,
+    world * EXTREMES_BYTES), on the stream; merge with polygon_device."""
+    _check(lib().cudapre_comm_allgather_extremes(comm.handle, ws.ptr, ctypes.c_void_p(parts.data_ptr()),
+                                                 _stream_ptr(stream)))
 
 
 def extremes_comm(pts, comm: Comm, angles_="A", index_base: int = 0, ws=None, stream=None) -> Extremes:

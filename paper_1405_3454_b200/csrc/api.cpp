@@ -56,6 +56,27 @@ cudapre_status staging(void** out) {
     return CUDAPRE_OK;
 }
 
+// Per-thread mapped pinned block the Step-1 result is written to by K1's
+// last block directly (cudapre_pipeline_host: no copy call between the kernels).
+struct Mapped {
+    void* h = nullptr;
+    void* d = nullptr;
+    ~Mapped() {
+        if (h) cudaFreeHost(h);
+    }
+};
+thread_local Mapped g_mapped;
+
+cudapre_status mapped_block(void** h, void** d) {
+    if (!g_mapped.h) {
+        CUDA_TRY(cudaHostAlloc(&g_mapped.h, 4096, cudaHostAllocMapped | cudaHostAllocPortable));
+        CUDA_TRY(cudaHostGetDevicePointer(&g_mapped.d, g_mapped.h, 0));
+    }
+    *h = g_mapped.h;
+    *d = g_mapped.d;
+    return CUDAPRE_OK;
+}
+
 // Per-thread timing events (created on first use).
 struct Events {
     cudaEvent_t e[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -527,6 +548,48 @@ cudapre_status cudapre_pipeline_device(const cudapre_pt* d_pts, int64_t n_local,
     if (st) return st;
     return cudapre_filter_device(d_pts, n_local, index_base, nullptr, d_surv_idx, d_surv_pts, capacity, d_ws,
                                  ws_bytes, stream, d_count, nullptr);
+}
+
+cudapre_status cudapre_pipeline_host(const cudapre_pt* d_pts, int64_t n_local, int64_t index_base, int32_t nang,
+                                     const double* c, const double* s, int64_t* d_surv_idx, cudapre_pt* d_surv_pts,
+                                     int64_t capacity, void* d_ws, size_t ws_bytes, void* stream, int64_t* d_count,
+                                     cudapre_polygon_t* h_poly, double* h_ms_polygon) {
+    g_err.clear();
+    if (capacity < 0 || (n_local > 0 && !d_surv_idx)) return fail(CUDAPRE_ERR_INVALID_ARGUMENT, "bad survivor buffers");
+    void *hm = nullptr, *dm = nullptr;
+    cudapre_status st = mapped_block(&hm, &dm);
+    if (st) return st;
+    cudaStream_t strm = (cudaStream_t)stream;
+    // Step 1; K1's last block writes the result straight into the mapped block
+    st = cudapre_extremes(d_pts, n_local, index_base, nang, c, s, d_ws, ws_bytes, stream,
+                          reinterpret_cast<cudapre_extremes_t*>(dm), nullptr, nullptr);
+    if (st) return st;
+    CUDA_TRY(cudaStreamSynchronize(strm));   // (the one host wait of the step: the picks)
+    cudapre_extremes_t ext;
+    std::memcpy(&ext, hm, sizeof(ext));
+    if (ext.nonfinite) return fail(CUDAPRE_ERR_NONFINITE_INPUT, "non-finite coordinate in the input");
+    // Step 2 on the host, straight into pinned staging
+    void* stage = nullptr;
+    st = staging(&stage);
+    if (st) return st;
+    K2Geom* hg = reinterpret_cast<K2Geom*>(reinterpret_cast<char*>(stage) + kStageGeomOff);
+    cudapre_polygon_t poly;
+    const auto t0 = std::chrono::steady_clock::now();
+    build_polygon(ext, &poly, hg);
+    const auto t1 = std::chrono::steady_clock::now();
+    if (h_poly) *h_poly = poly;
+    if (h_ms_polygon) *h_ms_polygon = std::chrono::duration<double, std::milli>(t1 - t0).count();
+    // Step 3, enqueued: one H2D of the geometry, K2, the count stays on the device
+    K2Params p;
+    std::memset(&p, 0, sizeof(p));
+    k2_params(p, d_pts, n_local, index_base, d_surv_idx, d_surv_pts, capacity, d_ws, ws_bytes);
+    p.edges = poly.nv <= 16 ? 16 : 32;
+    CUDA_TRY(cudaMemcpyAsync(ws_geom(d_ws), hg, sizeof(K2Geom), cudaMemcpyHostToDevice, strm));
+    int launches = 0;
+    CUDA_TRY(launch_filter(p, (((uintptr_t)d_pts & 15u) == 0), stream, &launches));
+    if (d_count)
+        CUDA_TRY(cudaMemcpyAsync(d_count, &p.ws->count, sizeof(int64_t), cudaMemcpyDeviceToDevice, strm));
+    return CUDAPRE_OK;
 }
 
 struct cudapre_graph {

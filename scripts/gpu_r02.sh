@@ -15,7 +15,7 @@ for s in ${STEPS:-smoke pytest bench_c5}; do
     bench_c5_quick) run bench_c5 600 python bench.py --no-e2e --no-cpu-baseline ;;
     bench_cfgs) for c in C2a C2b C3 C4 C4e0; do run bench_$c 600 python bench.py --config $c --no-cpu-baseline; done ;;
     ncu_c5)
-      CMD="python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline --no-host-step2-check"
+      CMD="python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline"
       run ncu_launches 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c5.csv $CMD
       run ncu_full 1200 ncu --set full --clock-control none --import-source on -k "regex:${NCU_REGEX:-k1_extremes|k2_filter}" -s ${NCU_SKIP:-6} -c ${NCU_COUNT:-3} -o gpurun_out/prof_c5 $CMD ;;
     custom) run custom ${CUSTOM_T:-600} bash -c "$CUSTOM" ;;

@@ -44,6 +44,21 @@ def test_bench_line_contract(args):
     assert d["gpu_launches"] > 0
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= d["clocks"].keys()
     assert "cpu_baseline" in d and 0 <= d["discard_pct"] <= 100
+    if args[1] == "C2b":   # the paper's host Step 2 and end-to-end hull with / without CudaPre
+        h = d["host_step2"]
+        assert h["value"] > 0 and h["ms_per_step"] > 0 and 0 < h["pipeline_frac_of_8TBps"]
+        he = d["hull_e2e"]
+        assert he["without_cudapre_ms"] > 0 and he["with_cudapre_gpu_hull_ms"] > 0 and he["hull_vertices"] >= 3
+
+
+def test_bench_cpu_baseline_fields():
+    """cpu_baseline: all cores and one pinned core, per-phase
+    times, the CPU model."""
+    d = _run("--config", "C1", "--steps", "3", "--warmup", "3", "--no-e2e")
+    c = d["cpu_baseline"]
+    assert c["kind"] == "oracle" and c["value"] > 0 and c["cores"] >= 1 and c["cpu_model"]
+    assert c["single_thread"]["cores"] == 1 and c["single_thread"]["value"] > 0
+    assert {"extremes", "polygon", "filter", "hull"} <= c["per_phase_s"].keys()
 
 
 def test_bench_reference_arm_contract():
