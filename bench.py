@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--angles", default="A")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--align8", action="store_true",
+                    help="feed an 8-byte (not 16-byte) aligned view: the register-loading K1 / K2 kernels")
     ap.add_argument("--no-points", action="store_true",
                     help="write only the survivors' indices (perf experiment; not the benchmark workload)")
     return ap.parse_args()
@@ -477,6 +479,11 @@ def main():
     n_local = n_total // world + (1 if rank < n_total % world else 0)
     base = rank * (n_total // world) + min(rank, n_total % world)
     pts = scuda.generate(family, n_local, seed=seed, base=base, **cfg)
+    if args.align8:   # the same points at an 8-byte aligned address
+        buf = torch.empty((n_local + 1, 2), dtype=torch.float32, device="cuda")
+        buf[1:] = pts
+        pts = buf[1:]
+        assert pts.data_ptr() % 16 == 8
     ws = cp.Workspace(n_local)
     cap = n_local if n_local <= 250_000_000 else n_local // 8   # dense configs (C4) keep ~all points
     out_idx = torch.empty(cap, dtype=torch.int64, device="cuda")

@@ -164,21 +164,33 @@ __device__ __forceinline__ void emit_t(const K2Params& p, const TileT& ts, const
     const unsigned long long tpt = (unsigned long long)tile * (2u * kTilePairsT);
     float2* out_pts = reinterpret_cast<float2*>(p.out_pts);
     const unsigned wc = ts.lstart[warp][kK2Sub];
-    for (unsigned r = lane; r < wc; r += 32) {
-        SurvT e;
-        if (r < kL) {
-            e = ts.list[warp][r];
-        } else {
-            const SurvT* q = ovf + (r - kL);
-            e.x = __ldcg(&q->x);
-            e.y = __ldcg(&q->y);
-            e.meta = __ldcg(&q->meta);
+    constexpr int kU = 4;
+    for (unsigned r0 = 0; r0 < wc; r0 += 32 * kU) {
+        SurvT e[kU];
+#pragma unroll
+        for (int k = 0; k < kU; ++k) {
+            const unsigned r = r0 + 32u * k + lane;
+            if (r < wc) {
+                if (r < kL) {
+                    e[k] = ts.list[warp][r];
+                } else {
+                    const SurvT* q = ovf + (r - kL);
+                    e[k].x = __ldcg(&q->x);
+                    e[k].y = __ldcg(&q->y);
+                    e[k].meta = __ldcg(&q->meta);
+                }
+            }
         }
-        const unsigned sub = e.meta >> 8, loc = e.meta & 0xffu;
-        const unsigned long long pos = ex + ts.off[sub * kW + warp] + (r - ts.lstart[warp][sub]);
-        if (pos < p.capacity) {
-            p.out_idx[pos] = p.base + (long long)(tpt + chunk_point(sub, warp, loc));
-            if (out_pts) out_pts[pos] = make_float2(e.x, e.y);
+#pragma unroll
+        for (int k = 0; k < kU; ++k) {
+            const unsigned r = r0 + 32u * k + lane;
+            if (r >= wc) break;
+            const unsigned sub = e[k].meta >> 8, loc = e[k].meta & 0xffu;
+            const unsigned long long pos = ex + ts.off[sub * kW + warp] + (r - ts.lstart[warp][sub]);
+            if (pos < p.capacity) {
+                p.out_idx[pos] = p.base + (long long)(tpt + chunk_point(sub, warp, loc));
+                if (out_pts) out_pts[pos] = make_float2(e[k].x, e[k].y);
+            }
         }
     }
 }
