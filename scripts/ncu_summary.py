@@ -83,6 +83,8 @@ def main():
             lines += [f"- {k}: {v:.2f}" for v, k in sorted(st, reverse=True)[:6]]
         lines.append("")
         for short, key in KEY.items():
+            if short + "3" in name:   # the 3D kernels (k1_extremes3, k2_filter3): their own keys
+                key = short + "3"
             if short in name:
                 rb = to_bytes(d["dram__bytes_read.sum"], units[hdr.index("dram__bytes_read.sum")])
                 wb = to_bytes(d["dram__bytes_write.sum"], units[hdr.index("dram__bytes_write.sum")])
