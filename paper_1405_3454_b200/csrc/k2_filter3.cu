@@ -135,10 +135,10 @@ __device__ __forceinline__ float rcp_approx(float a) {
 }
 
 // Fast test of one point: 0 = discard, 1 = keep, 2 = slow (a long candidate
-// list, an undecided plane test, or no cell); `mask` then holds the
-// candidate facets for the warp-cooperative pass.
-__device__ __forceinline__ int classify_fast(const Smem3& g, const K3Geom* __restrict__ G, float x, float y,
-                                             float z, unsigned long long& mask) {
+// list, an undecided plane test, or no cell); `cw` then holds the cell's list
+// word (kNoCell: every facet) for the warp-cooperative pass (cell_mask).
+constexpr unsigned kNoCell = 0xffffffffu;
+__device__ __forceinline__ int classify_fast(const Smem3& g, float x, float y, float z, unsigned& cw) {
     const float dx = __fsub_rn(x, g.ox), dy = __fsub_rn(y, g.oy), dz = __fsub_rn(z, g.oz);
     const float ax = fabsf(dx), ay = fabsf(dy), az = fabsf(dz);
     const bool xm = ax >= ay && ax >= az;
@@ -154,13 +154,9 @@ __device__ __forceinline__ int classify_fast(const Smem3& g, const K3Geom* __res
     const int cell = (face * kCellG + (int)fu) * kCellG + (int)fv;
     const bool ok = am >= 0x1p-100f;   // false for NaN and for directions too short for the reciprocal
     const unsigned w = g.clist[ok ? cell : 0];
-    if (!ok || (w >> 24) > (unsigned)kCellSlots) {   // long list (or no cell)
-        const unsigned li = w & 0xffffffu;
-        mask = (ok && li != kNoLong) ? __ldg(&G->lmask[li]) : g.all;
-        return 2;
-    }
+    cw = ok ? w : kNoCell;
+    if (!ok || (w >> 24) > (unsigned)kCellSlots) return 2;   // long list (or no cell)
     bool out = false, unsure = false;
-    unsigned long long cand = 0;
 #pragma unroll
     for (int k = 0; k < kCellSlots; ++k) {   // branch-free: unused slots test the dummy plane
         const unsigned t = (w >> (8 * k)) & 0xffu;
@@ -169,10 +165,24 @@ __device__ __forceinline__ int classify_fast(const Smem3& g, const K3Geom* __res
         const float val = __fmaf_rn(P.x, x, __fmaf_rn(P.y, y, __fmaf_rn(P.z, z, P.w)));
         out |= val < -E;
         unsure |= !(val > E);
-        cand |= (t < (unsigned)kMax3Facets) ? (1ull << t) : 0ull;
     }
-    mask = cand;
     return out ? 1 : (unsure ? 2 : 0);
+}
+
+// the candidate facets of a cell list word (for the slow pass)
+__device__ __forceinline__ unsigned long long cell_mask(const Smem3& g, const K3Geom* __restrict__ G, unsigned w) {
+    if (w == kNoCell) return g.all;
+    if ((w >> 24) > (unsigned)kCellSlots) {
+        const unsigned li = w & 0xffffffu;
+        return li != kNoLong ? __ldg(&G->lmask[li]) : g.all;
+    }
+    unsigned long long m = 0;
+#pragma unroll
+    for (int k = 0; k < kCellSlots; ++k) {
+        const unsigned t = (w >> (8 * k)) & 0xffu;
+        if (t < (unsigned)kMax3Facets) m |= 1ull << t;
+    }
+    return m;
 }
 
 // The slow decision for one point, by the whole warp (x, y, z, mask uniform):
@@ -302,9 +312,8 @@ __global__ void __launch_bounds__(kK23Threads, kK23BlocksPerSM) k2_filter3(const
                     unsigned b = 0;
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
-                        unsigned long long mask = 0;
-                        const int st =
-                            (unsigned)e < n ? classify_fast(g, G, q[3 * e], q[3 * e + 1], q[3 * e + 2], mask) : 0;
+                        unsigned cw = 0;
+                        const int st = (unsigned)e < n ? classify_fast(g, q[3 * e], q[3 * e + 1], q[3 * e + 2], cw) : 0;
                         b |= (st == 1 ? 1u : 0u) << e;
                         // slow points of this element, one at a time by the whole warp
                         for (unsigned slow = __ballot_sync(kFull, st == 2); slow; slow &= slow - 1u) {
@@ -312,8 +321,8 @@ __global__ void __launch_bounds__(kK23Threads, kK23BlocksPerSM) k2_filter3(const
                             const float sx = __shfl_sync(kFull, q[3 * e], src);
                             const float sy = __shfl_sync(kFull, q[3 * e + 1], src);
                             const float sz = __shfl_sync(kFull, q[3 * e + 2], src);
-                            const unsigned long long sm = __shfl_sync(kFull, mask, src);
-                            const bool k = slow_coop(g, sx, sy, sz, sm, lane, &nexact);
+                            const unsigned sw = __shfl_sync(kFull, cw, src);
+                            const bool k = slow_coop(g, sx, sy, sz, cell_mask(g, G, sw), lane, &nexact);
                             if ((int)lane == src && k) b |= 1u << e;
                         }
                     }
@@ -390,9 +399,20 @@ __global__ void __launch_bounds__(kK23Threads, kK23BlocksPerSM) k2_filter3(const
             const unsigned long long cap = p.capacity > ex ? p.capacity - ex : 0ull;
             const unsigned lim = (unsigned)(cap < total ? cap : total);
             for (unsigned j = tid; j < lim; j += kK23Threads) p.out_idx[ex + j] = gbase + g.sidx[j];
-            if (p.out_pts) {
+            if (p.out_pts) {   // xyz: a scalar head up to 16-byte alignment, then float4 stores
                 float* o = p.out_pts + 3ull * ex;
-                for (unsigned j = tid; j < 3u * lim; j += kK23Threads) o[j] = g.spts[j];
+                const unsigned nfl = 3u * lim;
+                unsigned h = (unsigned)((16u - ((uintptr_t)o & 15u)) & 15u) / 4u;
+                if (h > nfl) h = nfl;
+                if (tid < h) o[tid] = g.spts[tid];
+                const unsigned nb = (nfl - h) / 4u;
+                float4* o4 = reinterpret_cast<float4*>(o + h);
+                for (unsigned j = tid; j < nb; j += kK23Threads) {
+                    const unsigned s0 = h + 4u * j;
+                    o4[j] = make_float4(g.spts[s0], g.spts[s0 + 1], g.spts[s0 + 2], g.spts[s0 + 3]);
+                }
+                const unsigned t0 = h + 4u * nb;
+                if (tid < nfl - t0) o[t0 + tid] = g.spts[t0 + tid];
             }
         }
         if (!live) break;
