@@ -10,17 +10,21 @@
 //    streams 16 KiB sub-tiles global -> shared with cp.async.bulk (SASS
 //    UBLKCP) into a kNst-deep ring guarded by a transaction-counting "full"
 //    mbarrier and an "empty" mbarrier the compute warps release; an EMIT warp
-//    does the ordered compaction's bookkeeping and writes the survivors; the
-//    compute warps only classify.  After set-up there is no block barrier.
+//    does the ordered compaction's bookkeeping (group scan, look-back,
+//    publish) and writes the survivors; the compute warps classify (and
+//    write their own lists when the emit warp falls behind).  After set-up
+//    there is no block barrier.
 //  * Ownership: compute warp w owns the contiguous 256 points [256w, 256w+256)
-//    of each sub-tile, lane l the points r*32+l (round r = 0..7, one float2
-//    each).  The groups of the ordered compaction are the 8 * kW (sub-tile,
-//    warp) chunks, in index order.
+//    of each sub-tile, lane l the eight points 8l..8l+7 (four float4 pairs,
+//    read in a rotated order that keeps LDS.128 conflict-free).  The groups of
+//    the ordered compaction are the 8 * kW (sub-tile, warp) chunks, in index
+//    order.
 //  * Pass A: one fast test per point (inner disk or inner box, whichever the
 //    host found larger; a warp-uniform switch).  Points it cannot decide are
-//    queued in INDEX order (one ballot per round), so the per-warp survivor
-//    list comes out sorted and a survivor's rank inside its group is its list
-//    position minus the group's start: no per-group ballots.
+//    queued in INDEX order (lane prefix of the per-lane counts by four
+//    bit-sliced ballots, then each lane writes its own), so the per-warp
+//    survivor list comes out sorted and a survivor's rank inside its group is
+//    its list position minus the group's start: no per-group ballots.
 //  * Queue pass: sector table (inner/outer radius of the bucket), then for
 //    the thin undecided band the 1-2 edges the bucket's rays can exit through
 //    (coefficients in shared memory), then the exact predicate.  Survivors go
@@ -31,8 +35,11 @@
 //    done and survivor total).  The emit warp then scans the 8 * kW group
 //    counts of k, resolves the PREVIOUS super-tile's prefix (decoupled
 //    look-back one tile-time after its aggregate went out: no spinning),
-//    publishes its inclusive prefix, writes its survivors (index + float2)
-//    and hands its list buffer back ("buf free").
+//    publishes its inclusive prefix, posts the exclusive one ("resolved")
+//    and writes the survivors (index + float2) list by list.  A compute warp
+//    that needs its list buffer back (three tiles later) before the emit warp
+//    got to its list claims the list and writes it itself, so dense inputs
+//    are written by all warps, sparse ones off the compute warps' path.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -64,7 +71,7 @@ constexpr int kBufs = kK2Bufs;                       // survivor-list buffers (t
 constexpr int kNst = 4;
 constexpr unsigned kL = 96;
 
-using SurvT = SurvEntry;   // meta = (sub << 8) | loc, loc = r*32 + lane = point offset in the warp chunk
+using SurvT = SurvEntry;   // meta = (sub << 8) | loc, loc = 8*lane + k = point offset in the warp chunk
 static_assert(kK2Bufs == 3 && kK2WarpPts == kK2Sub * 2 * (int)kChunkPairs && kW <= kK2MaxWarps, "layout");
 
 struct TileT {
@@ -73,6 +80,7 @@ struct TileT {
     unsigned off[kGroups];              // exclusive offset of group sub*kW + warp in the super-tile
     unsigned total;
     unsigned tile;                      // super-tile id (kNone: end of work)
+    unsigned long long ex;              // exclusive prefix of the super-tile (emit warp -> compute warps)
 };
 
 struct SmemT {
@@ -81,7 +89,9 @@ struct SmemT {
     unsigned long long empty[kNst];
     TileT ts[kBufs];
     unsigned long long tile_done[kBufs];   // compute warps -> emit warp (count kW)
-    unsigned long long buf_free[kBufs];    // emit warp -> compute warps (count 1)
+    unsigned long long resolved[kBufs];    // emit warp -> compute warps: off[] and ex are ready (count 1)
+    unsigned claim[kBufs][kW];             // list (buffer, warp) of local tile j claimed for writing: j + 1
+    unsigned emitted[kBufs][kW];           // ... written by the emit warp: j + 1
     unsigned long long agg[kBufs];         // (compute warps done << 32) | survivors so far
     unsigned char qslot[kW][8 * 32];
     float2 sec[CUDAPRE_SECTORS + 1];               // {inner r^2, outer r^2} per bucket
@@ -90,6 +100,21 @@ struct SmemT {
     GeomLite geo;                                  // scalars, coefficients, ring (rare paths)
     unsigned stile[kNst];   // super-tile id of the sub-tile-0 stage (kNone = end)
 };
+
+__device__ __forceinline__ unsigned ld_acquire_s(const unsigned* a) {
+    unsigned v;
+    asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(a)) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_s(unsigned* a, unsigned v) {
+    asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(smem_u32(a)), "r"(v) : "memory");
+}
+// warp-uniform: did this warp win list (b, w) of local tile tag - 1?
+__device__ __forceinline__ bool claim_list(unsigned* c, unsigned tag, unsigned lane) {
+    unsigned won = 0;
+    if (lane == 0) won = atomicMax(c, tag) < tag;
+    return __shfl_sync(kFull, won, 0) != 0u;
+}
 
 __device__ __forceinline__ float rcp_approx(float a) {
     float r;
@@ -155,16 +180,16 @@ __device__ __forceinline__ unsigned chunk_point(unsigned sub, unsigned warp, uns
     return sub * (2u * kSubPairsT) + warp * (2u * kChunkPairs) + loc;
 }
 
-// write the survivors of super-tile `tile` kept by warp `warp` from exclusive
-// prefix ex: list entries [0, kL) from shared memory, the overflow [kL, wc)
-// from the block's global scratch (written by the compute warp before it
-// signalled the tile done; L2-coherent loads)
+// compute warp `warp` writes its own survivors of super-tile `tile` from the
+// tile's exclusive prefix ex: list entries [0, kL) from shared memory, the
+// overflow [kL, wc) from the warp's global scratch (written by this warp's
+// lanes before a __syncwarp)
+template <int kU>
 __device__ __forceinline__ void emit_t(const K2Params& p, const TileT& ts, const SurvT* ovf, unsigned tile,
                                        unsigned long long ex, unsigned warp, unsigned lane) {
     const unsigned long long tpt = (unsigned long long)tile * (2u * kTilePairsT);
     float2* out_pts = reinterpret_cast<float2*>(p.out_pts);
     const unsigned wc = ts.lstart[warp][kK2Sub];
-    constexpr int kU = 4;
     for (unsigned r0 = 0; r0 < wc; r0 += 32 * kU) {
         SurvT e[kU];
 #pragma unroll
@@ -222,7 +247,8 @@ __global__ void __launch_bounds__(kBlock, 2) k2_filter_tma(const __grid_constant
         }
         for (int k = 0; k < kBufs; ++k) {
             mbar_init(&S.tile_done[k], (unsigned)kW);
-            mbar_init(&S.buf_free[k], 1u);
+            mbar_init(&S.resolved[k], 1u);
+            for (int w = 0; w < kW; ++w) S.claim[k][w] = S.emitted[k][w] = 0u;
             S.agg[k] = 0ull;
         }
         mbar_fence_init();
@@ -230,7 +256,7 @@ __global__ void __launch_bounds__(kBlock, 2) k2_filter_tma(const __grid_constant
     __syncthreads();   // the only whole-block barrier
     // shared-window addresses of the mbarriers and the ring (hot loops use these)
     const unsigned a_full = smem_u32(&S.full[0]), a_empty = smem_u32(&S.empty[0]);
-    const unsigned a_done = smem_u32(&S.tile_done[0]), a_free = smem_u32(&S.buf_free[0]);
+    const unsigned a_done = smem_u32(&S.tile_done[0]), a_res = smem_u32(&S.resolved[0]);
     const unsigned a_ring = smem_u32(&S.ring[0][0]);
 
     // ================================================================ producer warp
@@ -271,10 +297,11 @@ __global__ void __launch_bounds__(kBlock, 2) k2_filter_tma(const __grid_constant
     // ================================================================ emit warp
     // Per super-tile k (list buffer k % kBufs), once all compute warps are done
     // with it (the last of them has published the tile's aggregate; tile 0:
-    // its inclusive prefix): scan its 64 group counts; then resolve the PREVIOUS super-tile (decoupled look-back one
-    // tile-time after its aggregate went out: no spinning), publish its
-    // inclusive prefix, write its survivors and hand its buffer back.  The
-    // compute warps never wait for any of this.
+    // its inclusive prefix): scan its 64 group counts; then resolve the
+    // PREVIOUS super-tile (decoupled look-back one tile-time after its
+    // aggregate went out: no spinning), publish its inclusive prefix and hand
+    // its exclusive prefix to the compute warps ("resolved"), which write the
+    // survivors.
     if (warp == kEmitWarp) {
         unsigned lb_rounds = 0, lb_spins = 0;
         unsigned pend = kNone, pbuf = 0;
@@ -325,14 +352,20 @@ __global__ void __launch_bounds__(kBlock, 2) k2_filter_tma(const __grid_constant
                         if (pend == p.num_tiles - 1) p.ws->count = ex + prv.total;
                     }
                 }
-                // per-warp passes (measured faster than one flat pass over the tile:
-                // a quicker emit warp reaches the next look-back before the
-                // other blocks' aggregates are out and spins; r01_experiments.md)
+                if (lane == 0) {
+                    prv.ex = ex;
+                    mbar_arrive_a(a_res + 8u * pbuf);   // release: ex and off[] before the phase flips
+                }
+                // write the lists no compute warp has claimed (a compute warp that
+                // needs its buffer back before this warp got to its list writes
+                // it itself: dense inputs, where one writer is the bottleneck)
 #pragma unroll 1
-                for (unsigned w = 0; w < (unsigned)kW; ++w)
-                    emit_t(p, prv, sbase + (size_t)(pbuf * kW + w) * kK2WarpPts, pend, ex, w, lane);
-                __syncwarp();
-                if (lane == 0) mbar_arrive_a(a_free + 8u * pbuf);
+                for (unsigned w = 0; w < (unsigned)kW; ++w) {
+                    if (!claim_list(&S.claim[pbuf][w], k, lane)) continue;   // tag: local tile k-1, + 1
+                    emit_t<4>(p, prv, sbase + (size_t)(pbuf * kW + w) * kK2WarpPts, pend, ex, w, lane);
+                    __syncwarp();
+                    if (lane == 0) st_release_s(&S.emitted[pbuf][w], k);
+                }
             }
             if (tile == kNone) break;
             pend = tile;
@@ -362,14 +395,33 @@ __global__ void __launch_bounds__(kBlock, 2) k2_filter_tma(const __grid_constant
     const int fast = S.geo.fast, mode = S.geo.mode;
     const float gox = S.geo.ox, goy = S.geo.oy, gr2 = S.geo.r2, ge2 = S.geo.e2max;
     const float gbx0 = S.geo.bx0, gbx1 = S.geo.bx1, gby0 = S.geo.by0, gby1 = S.geo.by1;
-    unsigned seq = 0;
-    for (unsigned k = 0;; ++k) {
+    const unsigned rot = (lane >> 1) & 3u;
+    // make sure this warp's list of local super-tile j (buffer j % kBufs,
+    // global id t) has been written: normally the emit warp has done it; else
+    // wait until the tile is resolved and write it here unless the emit warp
+    // claims it first (then, if `wait`, until it is done)
+    auto emit_own = [&](unsigned j, unsigned t, bool wait) {
+        const unsigned bj = j % kBufs, tag = j + 1u;
+        if (ld_acquire_s(&S.emitted[bj][warp]) == tag) return;
+        mbar_sleep_wait(a_res + 8u * bj, (j / kBufs) & 1u);
+        if (claim_list(&S.claim[bj][warp], tag, lane)) {
+            emit_t<2>(p, S.ts[bj], sbase + (size_t)(bj * kW + warp) * kK2WarpPts, t, S.ts[bj].ex, warp, lane);
+        } else if (wait) {
+            while (ld_acquire_s(&S.emitted[bj][warp]) != tag) __nanosleep(64);
+        }
+    };
+    unsigned seq = 0, t1 = 0, t2 = 0, t3 = 0;   // global ids of local super-tiles k-1, k-2, k-3
+    unsigned k = 0;
+    for (;; ++k) {
         const unsigned bi = k % kBufs;
         TileT& cur = S.ts[bi];
         mbar_sleep_wait(a_full + 8u * (seq % kNst), (seq / kNst) & 1u);
         const unsigned tile = S.stile[seq % kNst];
         const bool have = tile != kNone;
-        if (k >= (unsigned)kBufs) mbar_sleep_wait(a_free + 8u * bi, ((k / kBufs) - 1u) & 1u);
+        if (have && k >= (unsigned)kBufs) {
+            emit_own(k - kBufs, t3, true);   // frees this warp's part of buffer bi
+            __syncwarp();
+        }
         if (have) {
             unsigned wc = 0;
             SurvT* const wscr = sbase + (size_t)(bi * kW + warp) * kK2WarpPts;
@@ -380,55 +432,66 @@ __global__ void __launch_bounds__(kBlock, 2) k2_filter_tma(const __grid_constant
                 const unsigned np = bytes / 16u;   // full pairs of this sub-tile in memory
                 const float4* chunk = &S.ring[st][warp * kChunkPairs];
                 mbar_sleep_wait(a_full + 8u * st, (seq / kNst) & 1u);
-                // warp-chunk points loc = r*32 + lane (round r = 0..7): one float2
-                // per lane per round, so the index order inside the chunk is
-                // (round, lane) and one ballot per round orders the queue
-                const float2* chunk2 = reinterpret_cast<const float2*>(chunk);
-                unsigned needy = 0u;   // bit r: point r*32 + lane not decided by the fast test
+                // lane l owns the chunk's points loc = 8l + k (k = 0..7), read as
+                // four 16-B pairs in the rotated order j -> (j + rot) & 3, so the
+                // eight lanes of each quarter-warp hit eight distinct 16-B bank
+                // groups (conflict-free LDS.128).  Bit j of m holds pair
+                // (j + rot) & 3; one rotate at the end puts point k at bit k.
+                unsigned needy = 0u;   // bit k: point 8*lane + k not decided by the fast test
                 if (np == (unsigned)kSubPairsT) {
                     if (fast == 0) {
+                        unsigned m = 0u;
 #pragma unroll
-                        for (int r = 0; r < 8; ++r) {
-                            const float2 v = chunk2[r * 32 + lane];
-                            needy |= (in_disk(gox, goy, gr2, v.x, v.y) ? 0u : 1u) << r;
+                        for (int j = 0; j < 4; ++j) {
+                            const float4 v = chunk[lane * 4u + ((j + rot) & 3u)];
+                            m |= (in_disk(gox, goy, gr2, v.x, v.y) ? 0u : 1u) << (2 * j);
+                            m |= (in_disk(gox, goy, gr2, v.z, v.w) ? 0u : 2u) << (2 * j);
                         }
+                        needy = ((m << (2u * rot)) | (m >> (8u - 2u * rot))) & 0xffu;
                     } else if (fast == 1) {
+                        unsigned m = 0u;
 #pragma unroll
-                        for (int r = 0; r < 8; ++r) {
-                            const float2 v = chunk2[r * 32 + lane];
-                            needy |= (in_box(gbx0, gbx1, gby0, gby1, v.x, v.y) ? 0u : 1u) << r;
+                        for (int j = 0; j < 4; ++j) {
+                            const float4 v = chunk[lane * 4u + ((j + rot) & 3u)];
+                            m |= (in_box(gbx0, gbx1, gby0, gby1, v.x, v.y) ? 0u : 1u) << (2 * j);
+                            m |= (in_box(gbx0, gbx1, gby0, gby1, v.z, v.w) ? 0u : 2u) << (2 * j);
                         }
+                        needy = ((m << (2u * rot)) | (m >> (8u - 2u * rot))) & 0xffu;
                     } else {   // no fast test (degenerate / exact-only rings): queue everything
                         needy = 0xffu;
                     }
                 } else {   // last super-tile only: ragged end (+ the unpaired last point)
                     const unsigned qs = tile * kTilePairsT + sub * kSubPairsT;   // first pair of the sub-tile
+                    const float2* chunk2 = reinterpret_cast<const float2*>(chunk);
 #pragma unroll
-                    for (int r = 0; r < 8; ++r) {
-                        const unsigned pt = warp * (2u * kChunkPairs) + r * 32 + lane;   // point in the sub-tile
+                    for (int k = 0; k < 8; ++k) {
+                        const unsigned pt = warp * (2u * kChunkPairs) + lane * 8u + k;   // point in the sub-tile
                         bool valid = false;
                         float2 v = make_float2(0.f, 0.f);
                         if (pt < 2u * np) {
-                            v = chunk2[r * 32 + lane];
+                            v = chunk2[lane * 8u + k];
                             valid = true;
                         } else if (odd && 2u * qs + pt == 2u * full_pairs) {
                             v = __ldg(reinterpret_cast<const float2*>(p.pts) + 2u * full_pairs);
                             valid = true;
                         }
-                        needy |= (valid && !fast_inside(S.geo, v.x, v.y) ? 1u : 0u) << r;
+                        needy |= (valid && !fast_inside(S.geo, v.x, v.y) ? 1u : 0u) << k;
                     }
                 }
-                // ---- index-ordered queue: slot of (r, lane) = (needy points of
-                //      rounds < r) + (needy points of round r in lanes < lane)
+                // ---- index-ordered queue: slot of loc = 8l + k = (needy points of
+                //      lanes < l) + (needy points of lane l below k).  The lane
+                //      prefix of the counts (0..8, four bits) by bit-sliced ballots.
                 if (lane == 0) cur.lstart[warp][sub] = wc;
-                unsigned qtotal = 0;
+                const unsigned cnt = __popc(needy);
+                unsigned slot = 0, qtotal = 0;
 #pragma unroll
-                for (int r = 0; r < 8; ++r) {
-                    const unsigned nb = (needy >> r) & 1u;
-                    const unsigned b = __ballot_sync(kFull, nb);
-                    if (nb) S.qslot[warp][qtotal + __popc(b & lt)] = (unsigned char)((r << 5) | lane);
-                    qtotal += __popc(b);
+                for (int b = 0; b < 4; ++b) {
+                    const unsigned bb = __ballot_sync(kFull, (cnt >> b) & 1u);
+                    slot += __popc(bb & lt) << b;
+                    qtotal += __popc(bb) << b;
                 }
+                for (unsigned m = needy; m; m &= m - 1u)
+                    S.qslot[warp][slot++] = (unsigned char)(lane * 8u + (__ffs(m) - 1));
                 if (qtotal) {
                     __syncwarp();
                     for (unsigned base = 0; base < qtotal; base += 32) {
@@ -462,7 +525,6 @@ __global__ void __launch_bounds__(kBlock, 2) k2_filter_tma(const __grid_constant
             if (lane == 0) cur.lstart[warp][kK2Sub] = wc;
         }
         if (warp == 0 && lane == 0) cur.tile = have ? tile : kNone;
-        if (have && cur.lstart[warp][kK2Sub] > kL) __threadfence_block();   // scratch writes before the signal
         __syncwarp();
         if (lane == 0) {
             if (have) {
@@ -485,6 +547,17 @@ __global__ void __launch_bounds__(kBlock, 2) k2_filter_tma(const __grid_constant
             mbar_arrive_a(a_done + 8u * bi);
         }
         if (!have) break;
+        t3 = t2;
+        t2 = t1;
+        t1 = tile;
+    }
+    // the end marker went out as local tile k: help with the last (up to)
+    // kBufs super-tiles, resolved once their successor's tile_done arrived
+#pragma unroll 1
+    for (unsigned i = 0; i < 3u; ++i) {
+        if (k + i >= 3u) emit_own(k + i - 3u, t3, false);
+        t3 = t2;
+        t2 = t1;
     }
 }
 
