@@ -128,6 +128,13 @@ __device__ __noinline__ bool queue_keep_rare(const GeomLite& G, float x, float y
     return queue_keep<EDGES>(G, x, y);
 }
 
+// look-back loads per lane: first round / later rounds (A/B-measured)
+#ifndef K2_LB_FIRST
+#define K2_LB_FIRST 2
+#endif
+#ifndef K2_LB_NEXT
+#define K2_LB_NEXT 8
+#endif
 // ---------------------------------------------------------------- look-back
 // Status word of super-tile t: [epoch:30 | flag:2 | count:32] at
 // status[t * kStatusStride] (one per 128-byte line).  publish() writes it with
@@ -148,7 +155,8 @@ __device__ __forceinline__ void publish(const K2Params& p, unsigned tile, unsign
 __device__ __forceinline__ unsigned long long resolve(const K2Params& p, unsigned tile,
                                                       unsigned epoch, unsigned lane,
                                                       unsigned& rounds, unsigned& spins) {
-    constexpr int kPer = 8;
+    constexpr int kPer = K2_LB_NEXT;   // loads per lane in later rounds
+    int per = K2_LB_FIRST;              // ... and in the first (the nearest prefix is usually close)
     const unsigned long long PF = (unsigned long long)kFlagP << 32;
     const unsigned long long E = (unsigned long long)(epoch & kEpochMask) << 34;
     unsigned long long ex = 0;
@@ -157,23 +165,24 @@ __device__ __forceinline__ unsigned long long resolve(const K2Params& p, unsigne
         unsigned long long w[kPer];
 #pragma unroll
         for (int k = 0; k < kPer; ++k) {
-            const long long t = pred - (long long)(kPer * lane + k);
-            w[k] = (t >= 0) ? ld_status(&p.status[(size_t)t * kStatusStride]) : (E | PF);
+            const long long t = pred - (long long)(per * (int)lane + k);
+            w[k] = (k < per && t >= 0) ? ld_status(&p.status[(size_t)t * kStatusStride]) : (E | PF);
         }
-        int kp = kPer;
+        int kp = per;
         bool inval = false;
         unsigned long long sum = 0;
 #pragma unroll
         for (int k = 0; k < kPer; ++k) {
+            if (k >= per) break;
             const unsigned flag =
                 ((unsigned)(w[k] >> 34) == (epoch & kEpochMask)) ? (unsigned)((w[k] >> 32) & 3u) : 0u;
-            if (kp == kPer) {
+            if (kp == per) {
                 if (flag == 0u) inval = true;
                 sum += w[k] & 0xffffffffull;
                 if (flag == kFlagP) kp = k;
             }
         }
-        const unsigned pmask = __ballot_sync(kFull, kp < kPer);
+        const unsigned pmask = __ballot_sync(kFull, kp < per);
         const unsigned imask = __ballot_sync(kFull, inval);
         const unsigned lim = pmask ? (unsigned)(__ffs(pmask) - 1) : 31u;
         const unsigned need = (lim == 31u) ? kFull : ((2u << lim) - 1u);
@@ -188,7 +197,8 @@ __device__ __forceinline__ unsigned long long resolve(const K2Params& p, unsigne
         for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
         ex += v;
         if (pmask) break;
-        pred -= 32 * kPer;
+        pred -= 32 * per;
+        per = kPer;
     }
     return ex;
 }

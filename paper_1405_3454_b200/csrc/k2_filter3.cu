@@ -44,6 +44,13 @@ constexpr unsigned kFlagA = 1u;
 constexpr unsigned kFlagP = 2u;
 constexpr unsigned kEpochMask = 0x3fffffffu;
 constexpr int kWarps = kK23Threads / 32;
+// look-back loads per lane: first round / later rounds (A/B-measured)
+#ifndef K23_LB_FIRST
+#define K23_LB_FIRST 2
+#endif
+#ifndef K23_LB_NEXT
+#define K23_LB_NEXT 2
+#endif
 
 struct Smem3 {
     unsigned clist[kCells];
@@ -81,7 +88,8 @@ __device__ __forceinline__ void publish(const K23Params& p, unsigned tile, unsig
 // exclusive prefix of `tile` (warp 0): walk back 32*8 predecessors per round,
 // summing aggregates up to the nearest inclusive prefix.
 __device__ unsigned long long resolve(const K23Params& p, unsigned tile, unsigned epoch, unsigned lane) {
-    constexpr int kPer = 8;
+    constexpr int kPer = K23_LB_NEXT;   // loads per lane in later rounds
+    int per = K23_LB_FIRST;             // ... and in the first (the nearest prefix is usually close)
     const unsigned long long PF = (unsigned long long)kFlagP << 32;
     const unsigned long long E = (unsigned long long)(epoch & kEpochMask) << 34;
     unsigned long long ex = 0;
@@ -90,23 +98,24 @@ __device__ unsigned long long resolve(const K23Params& p, unsigned tile, unsigne
         unsigned long long w[kPer];
 #pragma unroll
         for (int k = 0; k < kPer; ++k) {
-            const long long t = pred - (long long)(kPer * lane + k);
-            w[k] = (t >= 0) ? ld_status(&p.status[(size_t)t * kStatus3Stride]) : (E | PF);
+            const long long t = pred - (long long)(per * (int)lane + k);
+            w[k] = (k < per && t >= 0) ? ld_status(&p.status[(size_t)t * kStatus3Stride]) : (E | PF);
         }
-        int kp = kPer;
+        int kp = per;
         bool inval = false;
         unsigned long long sum = 0;
 #pragma unroll
         for (int k = 0; k < kPer; ++k) {
+            if (k >= per) break;
             const unsigned flag =
                 ((unsigned)(w[k] >> 34) == (epoch & kEpochMask)) ? (unsigned)((w[k] >> 32) & 3u) : 0u;
-            if (kp == kPer) {
+            if (kp == per) {
                 if (flag == 0u) inval = true;
                 sum += w[k] & 0xffffffffull;
                 if (flag == kFlagP) kp = k;
             }
         }
-        const unsigned pmask = __ballot_sync(kFull, kp < kPer);
+        const unsigned pmask = __ballot_sync(kFull, kp < per);
         const unsigned imask = __ballot_sync(kFull, inval);
         const unsigned lim = pmask ? (unsigned)(__ffs(pmask) - 1) : 31u;
         const unsigned need = (lim == 31u) ? kFull : ((2u << lim) - 1u);
@@ -119,7 +128,8 @@ __device__ unsigned long long resolve(const K23Params& p, unsigned tile, unsigne
         for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
         ex += v;
         if (pmask) break;
-        pred -= 32 * kPer;
+        pred -= 32 * per;
+        per = kPer;
     }
     return ex;
 }
