@@ -45,10 +45,6 @@ struct alignas(16) WsHeader {
     cudapre_extremes_t result;   // K1 final result
 };
 static_assert(sizeof(WsHeader) <= 2048, "header too large");
-// perf experiments only (CUDAPRE_K2_DEBUG=2): per-warp cycle counters of the
-// TMA K2 at this offset of the workspace header page (see scripts/k2_timing.py)
-constexpr size_t kWsDbgOffset = 2048;
-constexpr int kWsDbgWords = 48;
 
 struct K1Partial {
     double key;

@@ -30,8 +30,8 @@
 // nang screens; the others go to a per-warp queue screened in full 32-lane
 // batches.  Input: 16-B aligned data is streamed by a dedicated producer warp
 // (cp.async.bulk, 4 x 16 KiB ring, full / empty mbarriers) into shared
-// memory, so no register holds data in flight (CUDAPRE_K1_TMA=0: register
-// double-buffered 128-bit loads instead).
+// memory, so no register holds data in flight (8-byte aligned input:
+// register double-buffered 128-bit loads instead).
 // Thresholds start from a tiny seed kernel (float-only lower/upper bounds of
 // a sample, combined with atomicMax on an order-preserving encoding) so the
 // exact path stays rare from the first iteration on.  Candidates update a

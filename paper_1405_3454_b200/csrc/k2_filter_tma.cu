@@ -52,7 +52,8 @@ namespace {
 
 // kW compute warps per block.  A warp chunk is always 256 points; a sub-tile
 // is kW chunks, a super-tile 8 sub-tiles.  (10 compute warps measured the
-// same as 8, profiles/r01_experiments.md.)
+// same as 8, profiles/r01_experiments.md, and round 2 at 2 blocks/SM with
+// 80 registers: no better, r02_experiments.md.)
 constexpr int kW = 8;
 constexpr int kGroups = kK2Sub * kW;                 // groups (sub, warp) per super-tile
 constexpr unsigned kChunkPairs = 128;                // 256 points per warp chunk
