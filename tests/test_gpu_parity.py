@@ -193,6 +193,19 @@ def test_config_full_size(name):
     print(f"{name}: n={n} survivors={len(idx)} ({100 * len(idx) / n:.4f}%)")
 
 
+@pytest.mark.parametrize("eps", [0.1, 0.04])
+def test_mid_density_survivor_lists(eps):
+    """Survivor densities between the BASELINE configs' (C5 3.4 %, C4 98.5 %):
+    in the TMA K2 both the emit warp and the compute warps write survivor
+    lists in the same launch (the claim protocol) and many
+    lists overflow into the scratch; survivors, coordinates and hull equal
+    the oracle's."""
+    n = 20_000_000
+    xy = synth.generate("circle", n, seed=31, eps=eps)
+    ext, idx, want = _assert_parity(xy, "A", check_hull=True)
+    assert 0.1 < len(idx) / n < 0.9, len(idx) / n
+
+
 def test_config_c5_full():
     """C5 at its full 2e9 points on one GPU, the bench workload and launch
     configuration (device generator, 16-byte aligned):
