@@ -418,9 +418,15 @@ cudapre_status cudapre_pipeline_comm(const cudapre_pt* d_pts, int64_t n_local, i
  * global index order (the single-GPU survivor array) in d_out_idx /
  * d_out_pts (root only; capacity out_capacity, ignored on other ranks).
  * *h_total = the number of survivors, on every rank.  An all-gather of
- * (count, capacity) (16 bytes per rank), then one grouped ncclSend /
- * ncclRecv; blocks.  CAPACITY on every rank alike if the total exceeds the
- * root's out_capacity (nothing is sent; *h_total says how much is needed). */
+ * (count, the root's capacity, whether the root takes points, whether this
+ * rank's arguments are usable) — 32 bytes per rank — then one grouped
+ * ncclSend / ncclRecv; blocks.  Every rank takes the same decision from the
+ * gathered words, so errors are collective (no rank is left waiting):
+ * CAPACITY on every rank if the total exceeds the root's out_capacity (or
+ * the root passed no d_out_idx; nothing is sent, *h_total says how much is
+ * needed); INVALID_ARGUMENT on every rank if some rank passed count < 0, a
+ * NULL d_idx with count > 0, or no d_pts while the root takes points
+ * (d_out_pts != NULL).                                                      */
 cudapre_status cudapre_gather_survivors(cudapre_comm_t* comm, const int64_t* d_idx, const cudapre_pt* d_pts,
                                         int64_t count, int32_t root, int64_t* d_out_idx, cudapre_pt* d_out_pts,
                                         int64_t out_capacity, void* stream, int64_t* h_total);
@@ -430,7 +436,8 @@ cudapre_status cudapre_gather_survivors(cudapre_comm_t* comm, const int64_t* d_i
  * gathered on the root, the root's monotone chain over them: hull(U S_r) =
  * hull(U hull(S_r)).  The root gets the canonical ring of the whole set (as
  * cudapre_hull on all survivors) in h_ring; other ranks get *h_ring_len = 0.
- * Blocks.                                                                   */
+ * Blocks.  Errors are collective: a rank whose local hull fails still takes
+ * part in the counts exchange, and every rank then returns an error.       */
 cudapre_status cudapre_hull_comm(cudapre_comm_t* comm, const cudapre_pt* d_pts, const int64_t* d_ids, int64_t m,
                                  const cudapre_polygon_t* h_poly, void* d_scratch, size_t scratch_bytes,
                                  int32_t root, void* stream, int64_t* h_ring, int64_t ring_capacity,

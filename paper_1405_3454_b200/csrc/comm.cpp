@@ -114,12 +114,28 @@ cudapre_status need_nccl() {
 
 }  // namespace
 
+// int64 words every rank contributes to the exchanges below
+constexpr int kRec = 4;
+
 struct cudapre_comm {
     ncclComm_t nc = nullptr;
     int rank = 0, world = 1, device = 0;
-    long long* d_counts = nullptr;   // 2 * world int64 (count, root capacity per rank), device
+    long long* d_counts = nullptr;   // kRec * world int64 exchanged per rank (see gather_survivors), device
     long long* h_counts = nullptr;   // pinned host copy
 };
+
+// All-gather of kRec int64 words per rank (v[0..kRec)), read back into
+// c->h_counts on every rank.
+static cudapre_status exchange_words(cudapre_comm_t* c, const long long* v, cudaStream_t s) {
+    for (int k = 0; k < kRec; ++k) c->h_counts[kRec * c->rank + k] = v[k];
+    CUDA_TRYC(cudaMemcpyAsync(c->d_counts + kRec * c->rank, c->h_counts + kRec * c->rank, kRec * sizeof(long long),
+                              cudaMemcpyHostToDevice, s));
+    NCCL_TRY(nccl().AllGather(c->d_counts + kRec * c->rank, c->d_counts, kRec, ncclInt64, c->nc, s));
+    CUDA_TRYC(cudaMemcpyAsync(c->h_counts, c->d_counts, kRec * sizeof(long long) * (size_t)c->world,
+                              cudaMemcpyDeviceToHost, s));
+    CUDA_TRYC(cudaStreamSynchronize(s));
+    return CUDAPRE_OK;
+}
 
 extern "C" {
 
@@ -152,8 +168,8 @@ cudapre_status cudapre_comm_create(const void* h_id, int32_t rank, int32_t world
         delete c;
         return cfail(CUDAPRE_ERR_NCCL, "ncclCommInitRank: %s", nccl().GetErrorString(r));
     }
-    if (cudaMalloc(&c->d_counts, 2 * sizeof(long long) * (size_t)world) != cudaSuccess ||
-        cudaHostAlloc(&c->h_counts, 2 * sizeof(long long) * (size_t)world, cudaHostAllocPortable) != cudaSuccess) {
+    if (cudaMalloc(&c->d_counts, kRec * sizeof(long long) * (size_t)world) != cudaSuccess ||
+        cudaHostAlloc(&c->h_counts, kRec * sizeof(long long) * (size_t)world, cudaHostAllocPortable) != cudaSuccess) {
         cudapre_comm_destroy(c);
         return cfail(CUDAPRE_ERR_CUDA, "comm buffers");
     }
@@ -232,51 +248,57 @@ cudapre_status cudapre_gather_survivors(cudapre_comm_t* c, const int64_t* d_idx,
                                         int64_t count, int32_t root, int64_t* d_out_idx, cudapre_pt* d_out_pts,
                                         int64_t out_capacity, void* stream, int64_t* h_total) {
     api_fail(CUDAPRE_OK, "");
-    if (!c || !h_total || count < 0 || root < 0 || root >= c->world)
+    if (!c || !h_total || root < 0 || root >= c->world)   // (a bad root differs per rank only by misuse)
         return cfail(CUDAPRE_ERR_INVALID_ARGUMENT, "bad gather arguments");
-    if (count > 0 && !d_idx) return cfail(CUDAPRE_ERR_INVALID_ARGUMENT, "d_idx is NULL");
     cudaStream_t s = (cudaStream_t)stream;
     const bool me_root = c->rank == root;
-    // 1. all-gather of (count, out_capacity) per rank (16 bytes), read back on
-    //    every rank: all ranks see the counts and the root's capacity, so they
-    //    take the same decision
-    c->h_counts[2 * c->rank] = count;
-    c->h_counts[2 * c->rank + 1] = out_capacity;
-    CUDA_TRYC(cudaMemcpyAsync(c->d_counts + 2 * c->rank, c->h_counts + 2 * c->rank, 2 * sizeof(long long),
-                              cudaMemcpyHostToDevice, s));
-    NCCL_TRY(nccl().AllGather(c->d_counts + 2 * c->rank, c->d_counts, 2, ncclInt64, c->nc, s));
-    CUDA_TRYC(cudaMemcpyAsync(c->h_counts, c->d_counts, 2 * sizeof(long long) * (size_t)c->world,
-                              cudaMemcpyDeviceToHost, s));
-    CUDA_TRYC(cudaStreamSynchronize(s));
+    // 1. all-gather of (count, root capacity, root wants points, this rank's
+    //    arguments are usable) per rank: every rank sees the same numbers and
+    //    takes the same decision, so an error on one rank never leaves another
+    //    blocked in a send or receive
+    const bool ok = count >= 0 && (count == 0 || d_idx);
+    const long long mine[kRec] = {ok ? count : 0, me_root && d_out_idx ? (long long)out_capacity : 0,
+                                  me_root && d_out_pts ? 1 : 0, (ok ? 1 : 0) | (d_pts ? 2 : 0)};
+    cudapre_status st = exchange_words(c, mine, s);
+    if (st) return st;
+    const long long* w = c->h_counts;
     std::vector<long long> off((size_t)c->world + 1, 0);
-    for (int r = 0; r < c->world; ++r) off[r + 1] = off[r] + c->h_counts[2 * r];
+    bool all_ok = true, pts_ok = true;
+    for (int r = 0; r < c->world; ++r) {
+        off[r + 1] = off[r] + w[kRec * r];
+        all_ok &= (w[kRec * r + 3] & 1) != 0;
+        pts_ok &= w[kRec * r] == 0 || (w[kRec * r + 3] & 2) != 0;
+    }
+    const bool with_pts = w[kRec * root + 2] != 0;   // the root decides: it has a place for them
     *h_total = off[c->world];
-    if (off[c->world] > c->h_counts[2 * root + 1])
-        return cfail(CUDAPRE_ERR_CAPACITY, "%lld survivors > root capacity %lld", off[c->world],
-                     c->h_counts[2 * root + 1]);
-    if (me_root && off[c->world] > 0 && (!d_out_idx)) return cfail(CUDAPRE_ERR_INVALID_ARGUMENT, "d_out_idx NULL");
-    const bool with_pts = d_pts != nullptr;
-    // 2. grouped point-to-point: rank r's survivors land at off[r] on the root
-    NCCL_TRY(nccl().GroupStart());
+    if (!all_ok) return cfail(CUDAPRE_ERR_INVALID_ARGUMENT, "bad gather arguments on some rank (count < 0 or NULL d_idx)");
+    if (with_pts && !pts_ok)
+        return cfail(CUDAPRE_ERR_INVALID_ARGUMENT, "the root takes points: every rank with survivors must pass d_pts");
+    if (off[c->world] > w[kRec * root + 1])
+        return cfail(CUDAPRE_ERR_CAPACITY, "%lld survivors > root capacity %lld", off[c->world], w[kRec * root + 1]);
+    // 2. the root's own part (a device copy), then grouped point-to-point:
+    //    rank r's survivors land at off[r] on the root
+    if (me_root && count > 0) {
+        CUDA_TRYC(cudaMemcpyAsync(d_out_idx + off[root], d_idx, (size_t)count * sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
+        if (with_pts)
+            CUDA_TRYC(cudaMemcpyAsync(d_out_pts + off[root], d_pts, (size_t)count * sizeof(cudapre_pt),
+                                      cudaMemcpyDeviceToDevice, s));
+    }
+    ncclResult_t r0 = nccl().GroupStart();
     if (me_root) {
-        for (int r = 0; r < c->world; ++r) {
-            const size_t m = (size_t)c->h_counts[2 * r];
-            if (!m) continue;
-            if (r == root) {
-                CUDA_TRYC(cudaMemcpyAsync(d_out_idx + off[r], d_idx, m * sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
-                if (with_pts && d_out_pts)
-                    CUDA_TRYC(cudaMemcpyAsync(d_out_pts + off[r], d_pts, m * sizeof(cudapre_pt),
-                                              cudaMemcpyDeviceToDevice, s));
-                continue;
-            }
-            NCCL_TRY(nccl().Recv(d_out_idx + off[r], m, ncclInt64, r, c->nc, s));
-            if (with_pts && d_out_pts) NCCL_TRY(nccl().Recv(d_out_pts + off[r], 2 * m, ncclFloat32, r, c->nc, s));
+        for (int r = 0; r < c->world && r0 == ncclSuccess; ++r) {
+            const size_t m = (size_t)w[kRec * r];
+            if (!m || r == root) continue;
+            r0 = nccl().Recv(d_out_idx + off[r], m, ncclInt64, r, c->nc, s);
+            if (r0 == ncclSuccess && with_pts) r0 = nccl().Recv(d_out_pts + off[r], 2 * m, ncclFloat32, r, c->nc, s);
         }
     } else if (count > 0) {
-        NCCL_TRY(nccl().Send(d_idx, (size_t)count, ncclInt64, root, c->nc, s));
-        if (with_pts) NCCL_TRY(nccl().Send(d_pts, 2 * (size_t)count, ncclFloat32, root, c->nc, s));
+        r0 = nccl().Send(d_idx, (size_t)count, ncclInt64, root, c->nc, s);
+        if (r0 == ncclSuccess && with_pts) r0 = nccl().Send(d_pts, 2 * (size_t)count, ncclFloat32, root, c->nc, s);
     }
-    NCCL_TRY(nccl().GroupEnd());
+    const ncclResult_t r1 = nccl().GroupEnd();   // always closed, also after an error inside
+    if (r0 != ncclSuccess || r1 != ncclSuccess)
+        return cfail(CUDAPRE_ERR_NCCL, "survivor gather: %s", nccl().GetErrorString(r0 != ncclSuccess ? r0 : r1));
     return CUDAPRE_OK;
 }
 
@@ -297,20 +319,31 @@ cudapre_status cudapre_hull_comm(cudapre_comm_t* c, const cudapre_pt* d_pts, con
     std::vector<int64_t> ring((size_t)(m > 0 ? m : 1) + 1);
     std::vector<cudapre_pt> rpt((size_t)(m > 0 ? m : 1) + 1);
     int64_t len = 0, rem = 0;
-    cudapre_status st = cudapre_hull_device_ex(d_pts, d_ids, m, h_poly, d_scratch, scratch_bytes, stream,
-                                               ring.data(), rpt.data(), (int64_t)ring.size(), &len, &rem);
-    if (st) return st;
+    const cudapre_status st = cudapre_hull_device_ex(d_pts, d_ids, m, h_poly, d_scratch, scratch_bytes, stream,
+                                                     ring.data(), rpt.data(), (int64_t)ring.size(), &len, &rem);
+    const std::string local_err = st ? cudapre_last_error() : "";
     // gather (len, ids, points) of every rank on the root through the comm's
-    // device buffers: counts all-gather, then grouped send / recv
+    // device buffers: a counts all-gather (a rank whose local hull failed still
+    // takes part, with len = -1, so every rank returns the error instead of
+    // waiting in a collective), then grouped send / recv
+    const bool ring_ok = c->rank != root || (h_ring && ring_capacity >= 0);
+    const long long mine[kRec] = {st ? -1 : (long long)len, ring_ok ? 1 : 0, 0, 0};
+    cudapre_status xs = exchange_words(c, mine, s);
+    if (xs) return xs;
+    std::vector<long long> off((size_t)c->world + 1, 0);
+    int failed = -1;
+    bool root_ok = true;
+    for (int r = 0; r < c->world; ++r) {
+        const long long k = c->h_counts[kRec * r];
+        if (k < 0 && failed < 0) failed = r;
+        root_ok &= c->h_counts[kRec * r + 1] != 0;
+        off[r + 1] = off[r] + (k > 0 ? k : 0);
+    }
+    if (st) return cfail(st, "%s", local_err.c_str());
+    if (failed >= 0) return cfail(CUDAPRE_ERR_CUDA, "the local hull failed on rank %d", failed);
+    if (!root_ok) return cfail(CUDAPRE_ERR_INVALID_ARGUMENT, "h_ring is NULL on the root");
     void* d_buf = nullptr;
     const size_t rec = sizeof(int64_t) + sizeof(cudapre_pt);
-    c->h_counts[c->rank] = len;
-    CUDA_TRYC(cudaMemcpyAsync(c->d_counts + c->rank, c->h_counts + c->rank, sizeof(long long), cudaMemcpyHostToDevice, s));
-    NCCL_TRY(nccl().AllGather(c->d_counts + c->rank, c->d_counts, 1, ncclInt64, c->nc, s));
-    CUDA_TRYC(cudaMemcpyAsync(c->h_counts, c->d_counts, sizeof(long long) * (size_t)c->world, cudaMemcpyDeviceToHost, s));
-    CUDA_TRYC(cudaStreamSynchronize(s));
-    std::vector<long long> off((size_t)c->world + 1, 0);
-    for (int r = 0; r < c->world; ++r) off[r + 1] = off[r] + c->h_counts[r];
     const long long tot = off[c->world];
     CUDA_TRYC(cudaMalloc(&d_buf, rec * (size_t)(tot > 0 ? tot : 1)));
     int64_t* d_gid = reinterpret_cast<int64_t*>(d_buf);
@@ -324,7 +357,7 @@ cudapre_status cudapre_hull_comm(cudapre_comm_t* c, const cudapre_pt* d_pts, con
     cudapre_status out = CUDAPRE_OK;
     ncclResult_t r0 = nccl().GroupStart();
     for (int r = 0; r < c->world && r0 == ncclSuccess; ++r) {
-        const size_t k = (size_t)c->h_counts[r];
+        const size_t k = (size_t)c->h_counts[kRec * r];
         if (!k) continue;
         if (c->rank == root && r != root) {
             r0 = nccl().Recv(d_gid + off[r], k, ncclInt64, r, c->nc, s);
