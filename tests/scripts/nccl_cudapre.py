@@ -66,6 +66,27 @@ def main():
     assert np.array_equal(o_idx[:m].cpu().numpy(), idx.cpu().numpy()), "pipeline_comm"
     assert np.array_equal(o_pts[:m].cpu().numpy(), xy[o_idx[:m].cpu().numpy() - base]), "pipeline_comm points"
     g_idx, g_pts, g_tot = cp.gather_survivors(comm, o_idx, o_pts, m, root=0)
+    # collective errors: every rank returns the same status, none waits in a
+    # send / receive — a NULL d_idx on the last rank, then a root that takes
+    # points while the last rank passes none
+    L = cp.lib()
+    total = cp.ctypes.c_int64()
+    last = rank == world - 1
+    r_idx = torch.empty(max(g_tot, 1), dtype=torch.int64, device="cuda") if rank == 0 else None
+    r_pts = torch.empty((max(g_tot, 1), 2), dtype=torch.float32, device="cuda") if rank == 0 else None
+    vp = cp.ctypes.c_void_p
+    for bad_idx, bad_pts in ((True, False), (False, True)):
+        st = L.cudapre_gather_survivors(
+            comm.handle, None if (last and bad_idx) else vp(o_idx.data_ptr()),
+            None if (last and bad_pts) else vp(o_pts.data_ptr()), max(m, 1), 0,
+            vp(r_idx.data_ptr()) if rank == 0 else None, vp(r_pts.data_ptr()) if rank == 0 else None,
+            max(g_tot, 1), None, cp.ctypes.byref(total))
+        assert st == cp.ERR_ARG, (rank, bad_idx, bad_pts, st)
+    # capacity: every rank sees CAPACITY and the total it needs
+    st = L.cudapre_gather_survivors(comm.handle, vp(o_idx.data_ptr()), None, m, 0,
+                                    vp(r_idx.data_ptr()) if rank == 0 else None, None, 0, None,
+                                    cp.ctypes.byref(total))
+    assert (st == cp.ERR_CAPACITY) == (g_tot > 0) and total.value == g_tot, (rank, st, total.value)
     poly = cp.polygon(ext_c)
     ring_c = cp.hull_comm(comm, o_pts, o_idx, m, poly, root=0)
     # an empty shard on the last rank (world > 1): extremes_comm still gives the global answer
