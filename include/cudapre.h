@@ -403,10 +403,12 @@ cudapre_status cudapre_extremes_comm(const cudapre_pt* d_pts, int64_t n_local, i
                                      void* stream, cudapre_extremes_t* h_out);
 
 /* Steps 1-3 of a sharded set on the stream, no host synchronisation: K1 on
- * the local shard (n_local > 0), the all-gather into d_parts, the merge and
- * Step 2 on the device (every rank builds the same polygon), Step 3 on the
- * local shard.  Survivors (ascending global indices of this shard) in
- * d_surv_idx / d_surv_pts, their number in *d_count (device int64).        */
+ * the local shard, the all-gather into d_parts, the merge and Step 2 on the
+ * device (every rank builds the same polygon), Step 3 on the local shard.
+ * Survivors (ascending global indices of this shard) in d_surv_idx /
+ * d_surv_pts, their number in *d_count (device int64).  An empty shard
+ * (n_local == 0, d_pts may be NULL) takes part in the collective with an
+ * empty Step-1 block and gets *d_count = 0.                                 */
 cudapre_status cudapre_pipeline_comm(const cudapre_pt* d_pts, int64_t n_local, int64_t index_base,
                                      int32_t nang, const double* c, const double* s, int64_t* d_surv_idx,
                                      cudapre_pt* d_surv_pts, int64_t capacity, void* d_ws, size_t ws_bytes,

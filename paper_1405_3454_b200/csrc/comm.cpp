@@ -229,17 +229,23 @@ cudapre_status cudapre_pipeline_comm(const cudapre_pt* d_pts, int64_t n_local, i
                                      cudapre_pt* d_surv_pts, int64_t capacity, void* d_ws, size_t ws_bytes,
                                      cudapre_comm_t* c, cudapre_extremes_t* d_parts, void* stream,
                                      int64_t* d_count) {
-    if (!c || !d_parts) return cfail(CUDAPRE_ERR_INVALID_ARGUMENT, "NULL argument");
-    if (n_local <= 0)
-        return cfail(CUDAPRE_ERR_INVALID_ARGUMENT,
-                     "cudapre_pipeline_comm needs a non-empty shard (use cudapre_extremes_comm for empty ones)");
-    cudapre_status st = cudapre_extremes(d_pts, n_local, index_base, nang, cc, ss, d_ws, ws_bytes, stream, nullptr,
+    if (!c || !d_parts || n_local < 0) return cfail(CUDAPRE_ERR_INVALID_ARGUMENT, "bad pipeline_comm arguments");
+    // an empty shard takes part in the collective with an empty Step-1 block
+    // (every idx = -1: never wins the merge) and has no survivors
+    cudapre_extremes_t* d_res =
+        n_local == 0 ? reinterpret_cast<cudapre_extremes_t*>(reinterpret_cast<char*>(d_ws) + CUDAPRE_WS_RESULT_OFFSET)
+                     : nullptr;
+    cudapre_status st = cudapre_extremes(d_pts, n_local, index_base, nang, cc, ss, d_ws, ws_bytes, stream, d_res,
                                          nullptr, nullptr);
-    if (st) return st;
+    if (st && !(n_local == 0 && st == CUDAPRE_ERR_EMPTY_INPUT)) return st;
     st = cudapre_comm_allgather_extremes(c, d_ws, d_parts, stream);
     if (st) return st;
     st = cudapre_polygon_device(d_parts, c->world, d_ws, ws_bytes, stream, nullptr);
     if (st) return st;
+    if (n_local == 0) {
+        if (d_count) CUDA_TRYC(cudaMemsetAsync(d_count, 0, sizeof(int64_t), (cudaStream_t)stream));
+        return CUDAPRE_OK;
+    }
     return cudapre_filter_geom(d_pts, n_local, index_base, d_surv_idx, d_surv_pts, capacity, d_ws, ws_bytes, stream,
                                d_count);
 }

@@ -95,6 +95,16 @@ def main():
         e_pts = pts if rank < world - 1 else torch.empty((0, 2), dtype=torch.float32, device="cuda")
         ext_e = cp.extremes_comm(e_pts, comm, "A", index_base=e_base)
         assert ext_e.n == N - shard(N, world - 1, world)[0], "empty-shard extremes_comm"
+    # pipeline_comm with an empty shard on the last rank (world 1: the only one)
+    e_pts = pts if rank < world - 1 else torch.empty((0, 2), dtype=torch.float32, device="cuda")
+    e_base = base if rank < world - 1 else N
+    pe_idx, _, pe_cnt = cp.pipeline_comm(e_pts, comm, "A", index_base=e_base, return_points=False)
+    torch.cuda.synchronize()
+    pe = pe_idx[: int(pe_cnt.item())].cpu().numpy()
+    if rank == world - 1:
+        assert len(pe) == 0, "empty shard: no survivors"
+    pe_all = [None] * world
+    dist.all_gather_object(pe_all, pe)
     # 4. the 3D extension
     n3 = N // 3
     n3_local, base3 = shard(n3, rank, world)
@@ -116,6 +126,10 @@ def main():
         assert np.array_equal(g_idx.cpu().numpy(), want["survivors"]), "gathered survivors"
         assert np.array_equal(g_pts.cpu().numpy(), full[want["survivors"]]), "gathered points"
         assert ring_c.tolist() == oracle.hull(full).tolist(), "hull_comm"
+        n_e = N - shard(N, world - 1, world)[0]   # the set without the last shard
+        if n_e > 0:
+            want_e = oracle.cudapre(full[:n_e], "A", threads=os.cpu_count())
+            assert np.array_equal(np.concatenate(pe_all), want_e["survivors"]), "pipeline_comm, empty last shard"
         full3 = synth.generate3("ball", n3, seed=7)
         want3 = oracle.cudapre3(full3, "A", threads=os.cpu_count())
         assert ext3.idx.tolist() == want3["ext_idx"].tolist(), "3D Step 1"
