@@ -44,15 +44,32 @@ constexpr size_t kStageGeomOff = 4096;
 constexpr size_t kStageBytes = kStageGeomOff + 65536;   // either dimension's geometry page (2D 32 KiB, 3D 64 KiB)
 struct Staging {
     void* p = nullptr;
+    cudaEvent_t busy = nullptr;   // recorded after an H2D from p that the call did not wait for
+    bool pending = false;
     ~Staging() {
         if (p) cudaFreeHost(p);
+        if (busy) cudaEventDestroy(busy);
     }
 };
 thread_local Staging g_stage;
 
+// The calling thread's pinned staging buffer, free to overwrite: a copy out
+// of it that an earlier call left in flight (cudapre_pipeline_host returns
+// without waiting, and the next call may use another stream) is waited for.
 cudapre_status staging(void** out) {
     if (!g_stage.p) CUDA_TRY(cudaHostAlloc(&g_stage.p, kStageBytes, cudaHostAllocPortable));
+    if (g_stage.pending) {
+        CUDA_TRY(cudaEventSynchronize(g_stage.busy));
+        g_stage.pending = false;
+    }
     *out = g_stage.p;
+    return CUDAPRE_OK;
+}
+// mark the staging buffer in use by work enqueued on strm
+cudapre_status staging_in_flight(cudaStream_t strm) {
+    if (!g_stage.busy) CUDA_TRY(cudaEventCreateWithFlags(&g_stage.busy, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventRecord(g_stage.busy, strm));
+    g_stage.pending = true;
     return CUDAPRE_OK;
 }
 
@@ -585,6 +602,8 @@ cudapre_status cudapre_pipeline_host(const cudapre_pt* d_pts, int64_t n_local, i
     k2_params(p, d_pts, n_local, index_base, d_surv_idx, d_surv_pts, capacity, d_ws, ws_bytes);
     p.edges = poly.nv <= 16 ? 16 : 32;
     CUDA_TRY(cudaMemcpyAsync(ws_geom(d_ws), hg, sizeof(K2Geom), cudaMemcpyHostToDevice, strm));
+    st = staging_in_flight(strm);   // the next call waits for this copy before reusing the buffer
+    if (st) return st;
     int launches = 0;
     CUDA_TRY(launch_filter(p, (((uintptr_t)d_pts & 15u) == 0), stream, &launches));
     if (d_count)
