@@ -354,6 +354,26 @@ __global__ void __launch_bounds__(kK23Threads, kK23BlocksPerSM) k2_filter3(const
                 if (lane == 31) g.wsum[w][warp] = incl[w];
             }
         }
+        // warp 0, done with its share of tile k: resolve the previous tile now,
+        // while the other warps still classify (its aggregate went out a tile
+        // ago, so predecessors are normally published: no spinning), instead
+        // of between the two barriers with every other warp waiting
+        if (warp == 0) {
+            if (have_prev) {
+                unsigned total = 0;
+#pragma unroll
+                for (int w = 0; w < kP; ++w) {
+                    const unsigned tot = g.total[par ^ 1][w];
+                    total += (tot & 0xffffu) + (tot >> 16);
+                }
+                const unsigned long long ex = prev_tile == 0 ? 0ull : resolve(p, prev_tile, epoch, lane);
+                if (lane == 0) {
+                    if (prev_tile != 0) publish(p, prev_tile, kFlagP, ex + total, epoch);
+                    g.ex = ex;
+                    if (prev_tile == p.num_tiles - 1) p.ws->count = ex + total;
+                }
+            }
+        }
         __syncthreads();
         if (warp == 0) {
             if (live) {
@@ -379,20 +399,6 @@ __global__ void __launch_bounds__(kK23Threads, kK23BlocksPerSM) k2_filter3(const
                     g.tile[par ^ 1] = t;
                     const unsigned ahead = t + gridDim.x;
                     if (VEC && ahead < full_tiles) prefetch_l2(p.pts + 3ull * kK23TilePts * ahead, 12u * kK23TilePts);
-                }
-            }
-            if (have_prev) {
-                unsigned total = 0;
-#pragma unroll
-                for (int w = 0; w < kP; ++w) {
-                    const unsigned tot = g.total[par ^ 1][w];
-                    total += (tot & 0xffffu) + (tot >> 16);
-                }
-                const unsigned long long ex = prev_tile == 0 ? 0ull : resolve(p, prev_tile, epoch, lane);
-                if (lane == 0) {
-                    if (prev_tile != 0) publish(p, prev_tile, kFlagP, ex + total, epoch);
-                    g.ex = ex;
-                    if (prev_tile == p.num_tiles - 1) p.ws->count = ex + total;
                 }
             }
         }
