@@ -289,9 +289,10 @@ __global__ void __launch_bounds__(kK23Threads, kK23BlocksPerSM) k2_filter3(const
     bool have_prev = false;
     unsigned prev_tile = 0;
     int par = 0;
-    // the first tile; every later one is claimed by thread 0 right after the
-    // previous tile's aggregate is published (the barrier that follows makes
-    // it visible), so the loop needs no barrier of its own at the top
+    // the first tile; every later one is claimed by thread 0 once warp 0 is
+    // done classifying its share of the current tile (the barriers that
+    // follow make it visible), so the loop needs no barrier of its own at the
+    // top
     if (tid == 0) {
         const unsigned t = atomicAdd(&p.ws->k2_ticket, 1u);
         g.tile[0] = t;
@@ -354,11 +355,18 @@ __global__ void __launch_bounds__(kK23Threads, kK23BlocksPerSM) k2_filter3(const
                 if (lane == 31) g.wsum[w][warp] = incl[w];
             }
         }
-        // warp 0, done with its share of tile k: resolve the previous tile now,
-        // while the other warps still classify (its aggregate went out a tile
-        // ago, so predecessors are normally published: no spinning), instead
-        // of between the two barriers with every other warp waiting
+        // warp 0, done with its share of tile k: take the next ticket and
+        // resolve the previous tile now, while the other warps still classify
+        // (its aggregate went out a tile ago, so predecessors are normally
+        // published: no spinning), instead of between the two barriers with
+        // every other warp waiting
         if (warp == 0) {
+            if (live && lane == 0) {   // the next tile (read after the barriers)
+                const unsigned t = atomicAdd(&p.ws->k2_ticket, 1u);
+                g.tile[par ^ 1] = t;
+                const unsigned ahead = t + gridDim.x;
+                if (VEC && ahead < full_tiles) prefetch_l2(p.pts + 3ull * kK23TilePts * ahead, 12u * kK23TilePts);
+            }
             if (have_prev) {
                 unsigned total = 0;
 #pragma unroll
@@ -395,10 +403,6 @@ __global__ void __launch_bounds__(kK23Threads, kK23BlocksPerSM) k2_filter3(const
                 if (lane == 0) {
                     publish(p, tile, tile == 0 ? kFlagP : kFlagA, total, epoch);
                     if (tile == 0 && tile == p.num_tiles - 1) p.ws->count = total;
-                    const unsigned t = atomicAdd(&p.ws->k2_ticket, 1u);   // the next tile
-                    g.tile[par ^ 1] = t;
-                    const unsigned ahead = t + gridDim.x;
-                    if (VEC && ahead < full_tiles) prefetch_l2(p.pts + 3ull * kK23TilePts * ahead, 12u * kK23TilePts);
                 }
             }
         }
