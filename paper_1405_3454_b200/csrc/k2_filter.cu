@@ -117,9 +117,10 @@ __device__ __forceinline__ void emit(const K2Params& p, const TileState& ts, uns
 
 // One super-tile = kK2Sub sub-tiles of kK2SubPairs point pairs (128 KiB).
 //   pass A(k):   stream + classify tile k, ballots and survivor list into
-//                ts[k&1]; block scan; publish tile k's aggregate;
-//   resolve(k-1): exclusive prefix of tile k-1 (its predecessors published
-//                long ago), publish its inclusive prefix;
+//                ts[k&1]; warp 0, once done with its share, resolves tile
+//                k-1 (exclusive prefix by look-back, its predecessors published
+//                long ago; publishes its inclusive prefix) while the other
+//                warps finish; block scan; publish tile k's aggregate;
 //   pass B(k-1): write tile k-1's survivors.
 // The next tile's ticket is taken after pass A(k) and its first sub-tile is
 // prefetched into registers before resolve/pass B.
@@ -262,6 +263,20 @@ __global__ void __launch_bounds__(kK2Threads, 2) k2_filter(const __grid_constant
                 }
             }
             if (lane == 0) cur.wcnt[warp] = (mode == 1) ? kList + 1u : wc;
+            // warp 0, done with its pass A: resolve the pending super-tile now,
+            // while the other warps finish theirs (its aggregate went out a tile
+            // ago), rather than between two barriers with every warp waiting
+            if (warp == 0 && pend != 0xffffffffu) {   // resolve the pending super-tile (see above)
+                unsigned long long ex = 0;
+                if (pend != 0) {
+                    ex = resolve(p, pend, epoch, lane, lb_rounds, lb_spins);
+                    if (lane == 0) {
+                        publish(p, pend, kFlagP, ex + prv.total, epoch);
+                        if (pend == p.num_tiles - 1) p.ws->count = ex + prv.total;
+                    }
+                }
+                if (lane == 0) S.prefix = ex;
+            }
             // next ticket only now: a tile is never held while its block is busy
             if (threadIdx.x == 0) S.next = atomicAdd(&p.ws->k2_ticket, 1u);
             __syncthreads();
@@ -294,19 +309,8 @@ __global__ void __launch_bounds__(kK2Threads, 2) k2_filter(const __grid_constant
                     }
                 }
             }
-        } else if (threadIdx.x == 0) {
-            S.next = 0xffffffffu;
-        }
-        __syncthreads();
-        const unsigned next = have ? S.next : 0xffffffffu;
-        if (next < p.num_tiles) {   // prefetch the next super-tile's first sub-tile
-#pragma unroll
-            for (int u = 0; u < kK2Items; ++u)
-                v[u] = load_pair<VEC>(p.pts, next * kK2TilePairs + u * kK2Threads + threadIdx.x, p.n);
-        }
-        // ---------------- resolve + pass B of the pending super-tile
-        if (pend != 0xffffffffu) {
-            if (warp == 0) {
+        } else {
+            if (warp == 0 && pend != 0xffffffffu) {   // resolve the pending super-tile (see above)
                 unsigned long long ex = 0;
                 if (pend != 0) {
                     ex = resolve(p, pend, epoch, lane, lb_rounds, lb_spins);
@@ -317,9 +321,17 @@ __global__ void __launch_bounds__(kK2Threads, 2) k2_filter(const __grid_constant
                 }
                 if (lane == 0) S.prefix = ex;
             }
-            __syncthreads();
-            emit(p, prv, pend * kK2TilePairs, S.prefix, warp, lane, lt);
+            if (threadIdx.x == 0) S.next = 0xffffffffu;
         }
+        __syncthreads();
+        const unsigned next = have ? S.next : 0xffffffffu;
+        if (next < p.num_tiles) {   // prefetch the next super-tile's first sub-tile
+#pragma unroll
+            for (int u = 0; u < kK2Items; ++u)
+                v[u] = load_pair<VEC>(p.pts, next * kK2TilePairs + u * kK2Threads + threadIdx.x, p.n);
+        }
+        // ---------------- pass B of the pending super-tile (resolved by warp 0 above)
+        if (pend != 0xffffffffu) emit(p, prv, pend * kK2TilePairs, S.prefix, warp, lane, lt);
         __syncthreads();   // prv is reused by the next pass A
         if (!have) break;
         pend = tile;
