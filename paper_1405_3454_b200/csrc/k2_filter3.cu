@@ -65,6 +65,7 @@ struct Smem3 {
     unsigned tile[2];
     unsigned total[2][kK23Quads / 2];
     unsigned long long ex;
+    unsigned done;   // warps done classifying the current tile (the first one resolves)
     // the previous tile's survivors, compacted in order: tile-local index + xyz
     unsigned sidx[kK23TilePts];
     float spts[3 * kK23TilePts];
@@ -294,6 +295,7 @@ __global__ void __launch_bounds__(kK23Threads, kK23BlocksPerSM) k2_filter3(const
     // follow make it visible), so the loop needs no barrier of its own at the
     // top
     if (tid == 0) {
+        g.done = 0u;
         const unsigned t = atomicAdd(&p.ws->k2_ticket, 1u);
         g.tile[0] = t;
         const unsigned ahead = t + gridDim.x;
@@ -355,12 +357,14 @@ __global__ void __launch_bounds__(kK23Threads, kK23BlocksPerSM) k2_filter3(const
                 if (lane == 31) g.wsum[w][warp] = incl[w];
             }
         }
-        // warp 0, done with its share of tile k: take the next ticket and
-        // resolve the previous tile now, while the other warps still classify
+        // the first warp done with its share of tile k takes the next ticket and
+        // resolves the previous tile, while the other warps still classify
         // (its aggregate went out a tile ago, so predecessors are normally
         // published: no spinning), instead of between the two barriers with
         // every other warp waiting
-        if (warp == 0) {
+        unsigned first = 0;
+        if (lane == 0) first = atomicAdd(&g.done, 1u) == 0u;
+        if (__shfl_sync(kFull, first, 0)) {
             if (live && lane == 0) {   // the next tile (read after the barriers)
                 const unsigned t = atomicAdd(&p.ws->k2_ticket, 1u);
                 g.tile[par ^ 1] = t;
@@ -384,6 +388,7 @@ __global__ void __launch_bounds__(kK23Threads, kK23BlocksPerSM) k2_filter3(const
         }
         __syncthreads();
         if (warp == 0) {
+            if (lane == 0) g.done = 0u;   // (next counted after the coming barrier)
             if (live) {
                 unsigned total = 0;
 #pragma unroll
