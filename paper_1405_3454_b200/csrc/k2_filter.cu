@@ -62,6 +62,7 @@ struct K2Smem {
     unsigned char own[kK2Warps][32];   // keep bits returned to each owner lane
     unsigned wsum[kK2Warps];
     unsigned next;
+    unsigned done;   // warps done with pass A of the current super-tile (the first one resolves)
     unsigned long long prefix;
     GeomLite geo;   // polygon scalars + coefficients (copied from p.g)
 };
@@ -134,12 +135,15 @@ __global__ void __launch_bounds__(kK2Threads, 2) k2_filter(const __grid_constant
     const unsigned epoch = *(volatile unsigned*)&p.ws->epoch;
 
     load_geom_lite(S.geo, p.g, threadIdx.x, kK2Threads);
-    if (threadIdx.x == 0) S.next = atomicAdd(&p.ws->k2_ticket, 1u);
+    if (threadIdx.x == 0) {
+        S.done = 0u;
+        S.next = atomicAdd(&p.ws->k2_ticket, 1u);
+    }
     __syncthreads();
     const int mode = S.geo.mode;
     unsigned tile = S.next;
     unsigned pend = 0xffffffffu;   // super-tile awaiting resolve + pass B
-    unsigned lb_rounds = 0, lb_spins = 0;   // warp 0's look-back diagnostics
+    unsigned lb_rounds = 0, lb_spins = 0;   // look-back diagnostics of the warps that resolved
     float4 v[kK2Items];
     if (tile < p.num_tiles) {
 #pragma unroll
@@ -263,10 +267,14 @@ __global__ void __launch_bounds__(kK2Threads, 2) k2_filter(const __grid_constant
                 }
             }
             if (lane == 0) cur.wcnt[warp] = (mode == 1) ? kList + 1u : wc;
-            // warp 0, done with its pass A: resolve the pending super-tile now,
-            // while the other warps finish theirs (its aggregate went out a tile
-            // ago), rather than between two barriers with every warp waiting
-            if (warp == 0 && pend != 0xffffffffu) {   // resolve the pending super-tile (see above)
+            // the first warp done with its pass A resolves the pending
+            // super-tile now, while the other warps finish theirs (its
+            // aggregate went out a tile ago), rather than between two barriers
+            // with every warp waiting
+            unsigned first = 0;
+            if (lane == 0) first = atomicAdd(&S.done, 1u) == 0u;
+            first = __shfl_sync(kFull, first, 0);
+            if (first && pend != 0xffffffffu) {   // resolve the pending super-tile (see above)
                 unsigned long long ex = 0;
                 if (pend != 0) {
                     ex = resolve(p, pend, epoch, lane, lb_rounds, lb_spins);
@@ -300,6 +308,7 @@ __global__ void __launch_bounds__(kK2Threads, 2) k2_filter(const __grid_constant
                 }
                 cur.off[threadIdx.x] = wpre + incl - c;
                 if (threadIdx.x == 0) {
+                    S.done = 0u;   // (counted again after the coming barriers)
                     cur.total = total;
                     if (tile == 0) {   // first tile: its inclusive prefix is known now
                         publish(p, 0, kFlagP, total, epoch);
@@ -339,9 +348,11 @@ __global__ void __launch_bounds__(kK2Threads, 2) k2_filter(const __grid_constant
     }
     // last block out resets the ticket and bumps the epoch (all blocks have
     // read `epoch` and taken their final ticket before incrementing k2_done)
-    if (threadIdx.x == 0) {
+    if (lane == 0) {   // (any warp may have resolved some super-tiles)
         if (lb_rounds) atomicAdd(&p.ws->lb_rounds, lb_rounds);
         if (lb_spins) atomicAdd(&p.ws->lb_spins, lb_spins);
+    }
+    if (threadIdx.x == 0) {
         __threadfence();
         const unsigned d = atomicAdd(&p.ws->k2_done, 1u);
         if (d == gridDim.x - 1) {
