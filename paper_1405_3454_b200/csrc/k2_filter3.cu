@@ -23,9 +23,11 @@
 // A direction too short for the reciprocal (or NaN) takes every facet.
 // Compaction: persistent blocks take tiles of kK23Quads * 1024 points from an
 // atomic ticket; each thread classifies kK23Quads quads; packed (two 16-bit
-// halves per word) block scans order the survivors; warp 0 resolves the tile's exclusive
-// prefix by a decoupled look-back over epoch-tagged status words (one per
-// 128-byte line), deferred by one tile so that it never waits; survivors'
+// halves per word) block scans order the survivors; the first warp done
+// classifying a tile takes the next ticket and resolves the PREVIOUS tile's
+// exclusive prefix by a decoupled look-back over epoch-tagged status words
+// (one per 128-byte line) while the others still classify — deferred by one
+// tile, so it never waits, and off the barrier-to-barrier path; survivors'
 // int64 index (+ xyz) are staged in shared memory and written in order with
 // coalesced stores.
 #include <cuda_runtime.h>
