@@ -172,3 +172,53 @@ def test_device_path_single_repeated_point_and_empty():
     with pytest.raises(cp.CudaPreError) as e:
         cp.pipeline(torch.empty((0, 2), device="cuda"), "A")
     assert e.value.status == cp.ERR_EMPTY
+
+
+@pytest.mark.parametrize("family", ["square", "disk", "gauss", "circle"])
+@pytest.mark.parametrize("angles", ["A", "D"])
+def test_pipeline_host_matches_oracle(family, angles):
+    """cudapre_pipeline_host — the paper's host Step 2 between the kernels in
+    one call (K1 writes the picks into mapped host memory): survivors,
+    coordinates and the polygon equal the oracle's, for 16- and 8-byte
+    aligned input (TMA and register kernels), ragged sizes and an
+    index_base."""
+    for n, base, misalign in ((1_000_003, 0, False), (65_537, 7_000_000_000, False), (300_007, 0, True), (5, 0, False)):
+        xy = synth.generate(family, n, seed=21)
+        want = oracle.cudapre(xy, angles, threads=THREADS)
+        if misalign:
+            buf = torch.empty((n + 1, 2), dtype=torch.float32, device="cuda")
+            buf[1:] = torch.from_numpy(xy).cuda()
+            pts = buf[1:]
+        else:
+            pts = torch.from_numpy(xy).cuda()
+        polys = []
+        out_idx, out_pts, count = cp.pipeline_host(pts, angles, index_base=base, polygon_out=polys)
+        torch.cuda.synchronize()
+        m = int(count.item())
+        got = out_idx[:m].cpu().numpy()
+        assert np.array_equal(got - base, want["survivors"]), (family, angles, n)
+        assert np.array_equal(out_pts[:m].cpu().numpy(), xy[want["survivors"]])
+        poly = polys[0][0]
+        assert poly.degenerate == want["degenerate"]
+        if not want["degenerate"]:
+            assert (poly.vidx - base).tolist() == want["ring"].tolist()
+
+
+def test_pipeline_host_alternating_streams():
+    """Back-to-back pipeline_host calls on two streams and two inputs (the
+    per-thread staging buffer is reused: a call waits for the previous
+    call's geometry copy before overwriting it) give each input its own
+    oracle survivors."""
+    xa = synth.generate("disk", 2_000_003, seed=31)
+    xb = synth.generate("square", 1_500_001, seed=32)
+    wa = oracle.cudapre(xa, "A", threads=THREADS)["survivors"]
+    wb = oracle.cudapre(xb, "A", threads=THREADS)["survivors"]
+    pa, pb = torch.from_numpy(xa).cuda(), torch.from_numpy(xb).cuda()
+    wsa, wsb = cp.Workspace(len(xa)), cp.Workspace(len(xb))
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    for _ in range(4):
+        ia, _, ca = cp.pipeline_host(pa, "A", ws=wsa, stream=s1, return_points=False)
+        ib, _, cb = cp.pipeline_host(pb, "A", ws=wsb, stream=s2, return_points=False)
+        torch.cuda.synchronize()
+        assert np.array_equal(ia[: int(ca.item())].cpu().numpy(), wa)
+        assert np.array_equal(ib[: int(cb.item())].cpu().numpy(), wb)
