@@ -71,3 +71,16 @@ def test_hull_device_after_device_pipeline():
         ws.tensor[cp.WS_POLY_OFFSET:cp.WS_POLY_OFFSET + ctypes.sizeof(cp.PolygonT)].cpu().numpy().tobytes())
     ring = cp.hull_device(out_pts, out_idx, m, raw)
     assert ring.tolist() == oracle.hull(xy).tolist()
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 7, 33, 4_097])
+@pytest.mark.parametrize("angles", ["A", "D"])
+def test_hull_device_tiny_inputs(n, angles):
+    """Tiny sets (a single point, two, collinear triples, sets where every
+    point is an extreme) through Steps 1-3 and the GPU hull, for the default
+    and the 8-angle preset (up to 32-vertex polygons)."""
+    for family in ("square", "disk", "circle"):
+        xy = synth.generate(family, n, seed=100 + n)
+        _check(xy, angles)
+    dup = np.repeat(synth.generate("disk", max(1, n // 3), seed=7), 3, axis=0)[:n]   # exact duplicates
+    _check(np.ascontiguousarray(dup), angles)
