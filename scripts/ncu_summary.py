@@ -50,8 +50,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("rep")
     ap.add_argument("launches", nargs="?")
-    ap.add_argument("--round", default="r01")
-    ap.add_argument("--config", default="C5")
+    ap.add_argument("--round", required=True, help="round tag of the output files, e.g. r02c (never overwrite another round's summary)")
+    ap.add_argument("--config", required=True)
     ap.add_argument("--n-local", type=int, default=2_000_000_000)
     ap.add_argument("--note", default="")
     a = ap.parse_args()
